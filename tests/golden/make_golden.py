@@ -1,0 +1,160 @@
+"""Generate golden fixtures by running the REAL reference package.
+
+Run here (the container that has /root/reference), never on the GPU box:
+
+    python tests/golden/make_golden.py [--ref-src /tmp/refpkg/src]
+
+The reference is built from a scratch copy (``/root/reference`` is
+read-only): ``cp -r /root/reference/pkg /tmp/refpkg && cd /tmp/refpkg &&
+python setup.py build_ext --inplace``; this script does that when the copy
+is missing.  Only the reference's *outputs* are written, into
+tests/golden/*.npz: no reference source is copied into the repo.
+
+Fixtures
+  corpus.npz  handcrafted graphs (tests/corpus.py:16-41 in the reference)
+              plus seeded random corpora (corpus.py:44-69, seeds used by the
+              reference's own tests) -- full arrays: graph build, classify,
+              IFP2 split, sync_simulate (ifp1/ifp2/fp-full) final state and
+              trace, ifp1_run/ifp2_run vectors, power vectors, dense oracle.
+  c1.npz      BASELINE config C1 (paper_2302_03245_b200.synthetic seed 0):
+              sha256 digests of the integer arrays, full float vectors.
+  synth42.npz the reference acceptance graph synth.generate(10_000, 100_000,
+              0.2, seed=42) (test_acceptance.py:41-45): edges + outputs.
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import os
+import shutil
+import subprocess
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+XI = 1e-12
+
+
+def ensure_reference(ref_src: str) -> None:
+    if not os.path.isdir(ref_src):
+        root = os.path.dirname(ref_src)
+        shutil.copytree("/root/reference/pkg", root)
+        subprocess.run([sys.executable, "setup.py", "build_ext", "--inplace"], cwd=root,
+                       check=True, stdout=subprocess.DEVNULL)
+    sys.path.insert(0, ref_src)
+    sys.path.insert(0, "/root/reference/pkg/tests")   # read-only import of corpus.py
+
+
+def digest(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.int64).tobytes()).hexdigest()
+
+
+def reference_outputs(P, g, prefix: str, out: dict, full_ints: bool, dense: bool) -> None:
+    cls = P.classify(g)
+    pg = P.preprocess_ifp2(g, cls)
+    from pushrank.graph import dangling_target_counts
+    dtc = dangling_target_counts(g, cls)
+    ints = {
+        "out_offsets": g.out_offsets, "out_targets": g.out_targets,
+        "in_offsets": g.in_offsets, "in_sources": g.in_sources,
+        "dangling": cls.dangling, "unreferenced": cls.unreferenced,
+        "weak_dangling": cls.weak_dangling, "weak_unreferenced": cls.weak_unreferenced,
+        "dtc": dtc, "live_offsets": pg.live_offsets, "live_targets": pg.live_targets,
+        "live_degree": pg.live_degree, "dangling_ids": pg.dangling_ids,
+        "source_offsets": pg.source_offsets, "source_ids": pg.source_ids,
+    }
+    for k, v in ints.items():
+        if full_ints:
+            out[f"{prefix}{k}"] = np.asarray(v, np.int64)
+        else:
+            out[f"{prefix}{k}_sha256"] = np.array(digest(v))
+    out[f"{prefix}n"] = np.int64(g.n)
+    out[f"{prefix}m"] = np.int64(g.m)
+    out[f"{prefix}m_d"] = np.int64(cls.dangling_edge_count)
+    cfg = P.SolverConfig(threshold=XI)
+    for variant in ("ifp1", "ifp2", "fp-full"):
+        last = {}
+
+        def cb(t, reserved, pushing, last=last):
+            last["r"] = reserved.copy()
+            last["h"] = pushing.copy()
+
+        subject = pg if variant == "ifp2" else g
+        vec, tr = P.sync_simulate(subject, cfg, variant=variant, cls=cls, on_iteration=cb)
+        key = f"{prefix}sync_{variant.replace('-', '_')}_"
+        out[key + "values"] = vec.values
+        if last:
+            out[key + "reserved_pre_settle"] = last["r"]
+            out[key + "h_pre_settle"] = last["h"]
+        for col in ("h_l1", "converged", "alpha", "work", "push_ops", "push_ops_dangling",
+                    "active_mass", "carry_mass"):
+            out[key + col] = np.asarray(tr.column(col))
+        out[key + "iterations"] = np.int64(tr.meta["iterations"])
+    v1, t1 = P.ifp1_run(g, cls, cfg, workers=4, backend="c")
+    v2, t2 = P.ifp2_run(pg, cfg, workers=4, backend="c")
+    out[f"{prefix}ifp1_values"] = v1.values
+    out[f"{prefix}ifp1_push_ops_dangling"] = np.int64(t1.final.push_ops_dangling)
+    out[f"{prefix}ifp2_values"] = v2.values
+    out[f"{prefix}ifp2_push_ops_dangling"] = np.int64(t2.final.push_ops_dangling)
+    out[f"{prefix}ifp2_phase1_push_ops"] = np.int64(t2.samples[-2].push_ops)
+    pv, ptr = P.power_method(g, P.SolverConfig(max_iterations=210))
+    out[f"{prefix}power_values"] = pv.values
+    out[f"{prefix}power_deltas"] = np.asarray(ptr.column("h_l1"))
+    if dense:
+        out[f"{prefix}dense_values"] = P.dense_oracle(g, P.SolverConfig()).values
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ref-src", default="/tmp/refpkg/src")
+    args = ap.parse_args()
+    ensure_reference(args.ref_src)
+    import pushrank as P
+    import corpus
+    from pushrank import synth
+
+    sys.path.insert(0, REPO)
+    from paper_2302_03245_b200 import synthetic
+
+    meta = {"numpy": np.__version__, "reference_version": P.__version__, "xi": XI}
+
+    # --- corpus (full arrays)
+    graphs = corpus.handcrafted()
+    for seed, count in ((20260811, 20), (31, 12), (101, 10), (55, 1), (83, 1)):
+        graphs += corpus.random_corpus(count, seed=seed)
+    out = {"count": np.int64(len(graphs))}
+    for i, g in enumerate(graphs):
+        src = np.repeat(np.arange(g.n), np.diff(g.out_offsets))
+        out[f"g{i}_src"] = src.astype(np.int64)
+        out[f"g{i}_dst"] = np.asarray(g.out_targets, np.int64)
+        out[f"g{i}_name"] = np.array(g.name)
+        reference_outputs(P, g, f"g{i}_", out, full_ints=True, dense=g.n <= 2000)
+    out["meta"] = np.array(repr(meta))
+    np.savez_compressed(os.path.join(HERE, "corpus.npz"), **out)
+    print("corpus.npz:", len(graphs), "graphs")
+
+    # --- C1 (digests + vectors)
+    n, src, dst = synthetic.make("c1", seed=0)
+    g = P.from_edges(n, src, dst, name="c1")
+    out = {"edges_sha256": np.array(digest(np.stack([src, dst])))}
+    reference_outputs(P, g, "", out, full_ints=False, dense=False)
+    out["meta"] = np.array(repr(meta))
+    np.savez_compressed(os.path.join(HERE, "c1.npz"), **out)
+    print("c1.npz: n", g.n, "m", g.m)
+
+    # --- acceptance synthetic (edges stored)
+    g = synth.generate(10_000, 100_000, dangling_fraction=0.2, seed=42)
+    src = np.repeat(np.arange(g.n), np.diff(g.out_offsets))
+    out = {"n_in": np.int64(g.n), "src": src.astype(np.int32),
+           "dst": np.asarray(g.out_targets, np.int32)}
+    reference_outputs(P, g, "", out, full_ints=False, dense=False)
+    out["meta"] = np.array(repr(meta))
+    np.savez_compressed(os.path.join(HERE, "synth42.npz"), **out)
+    print("synth42.npz: n", g.n, "m", g.m)
+
+
+if __name__ == "__main__":
+    main()
