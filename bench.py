@@ -1,0 +1,308 @@
+"""Benchmark: IFP2 (default) push rounds on BASELINE config C2 on the B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2] [--algo ifp2|ifp1] [--mode auto|pull|push]
+
+One "step" = one full solve of the hot path on the resident graph: every
+push round until no vertex holds pending mass above xi = 1e-10 (the L1 <
+1e-10 stopping rule), plus the IFP2 dangling settle and the
+normalised output.  Metric: GTEPS = edges pushed (the reference's push_ops,
+engines.py:155-157) / device seconds of the push phase.  Prints ONE JSON
+line (rank 0).
+
+--impl reference times the reference's own compiled CPU push kernel
+(oracle/_ref, /root/reference/pkg/src/pushrank/_kernels.pyx) driven like
+ifp2_run / ifp1_run with all host threads, on the same graph and metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+XI = 1e-10
+DAMPING = 0.85
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--algo", default="ifp2", choices=["ifp1", "ifp2"])
+    ap.add_argument("--mode", default="auto", choices=["auto", "pull", "push"])
+    ap.add_argument("--cpu-sample-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def config_desc(args, n, m):
+    return {"workload": f"{args.config}: {__import__('paper_2302_03245_b200.synthetic', fromlist=['x']).CONFIGS[args.config]}",
+            "algorithm": args.algo, "mode": args.mode, "n": int(n), "m": int(m), "seed": 0,
+            "threshold": XI, "damping": DAMPING,
+            "l2": "flushed between steps (256 MiB write)"}
+
+
+def make_host_graph(config):
+    from paper_2302_03245_b200 import synthetic
+    return synthetic.make(config, seed=0)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.QUERY}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                return
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_reference_run(g_host, algo, steps, threads):
+    """Time the reference's compiled push kernel (oracle/_ref) or, if absent,
+    the oracle's pthread port; returns (gteps, wall list, push_ops, kind)."""
+    import oracle
+    from oracle import refdriver
+    pg = oracle.preprocess_ifp2(g_host, np.flatnonzero(g_host.out_degree == 0)) if algo == "ifp2" else None
+    walls, ops = [], 0
+    if refdriver.available():
+        kind = "reference"
+        for _ in range(steps):
+            r = refdriver.run(g_host, algo, DAMPING, XI, workers=threads, pg=pg)
+            walls.append(r.wall_s)
+            ops = r.push_ops
+    else:
+        kind = "port"
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            r = oracle.async_run(g_host, algo, DAMPING, XI, workers=threads, pg=pg)
+            walls.append(time.perf_counter() - t0)
+            ops = r.push_ops
+    med = statistics.median(walls)
+    return ops / med / 1e9, walls, ops, kind
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    n, src, dst = make_host_graph(args.config)
+    g = oracle.from_edges(n, src, dst)
+    threads = os.cpu_count() or 1
+    import oracle.refdriver as rd
+    pg = oracle.preprocess_ifp2(g, np.flatnonzero(g.out_degree == 0)) if args.algo == "ifp2" else None
+    for _ in range(args.warmup):
+        (rd.run if rd.available() else oracle.async_run)(g, args.algo, DAMPING, XI, workers=threads, pg=pg)
+    gteps, walls, ops, kind = cpu_reference_run(g, args.algo, args.steps, threads)
+    total = sum(walls)
+    value = ops * len(walls) / total / 1e9
+    line = {"impl": "reference", "metric": "GTEPS", "value": value, "unit": "GTEPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(walls),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_desc(args, g.n, g.m),
+            "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": threads, "kind": kind,
+                             "sample": f"{args.steps} full {args.algo} solves of {args.config} "
+                                       f"(xi={XI}), median-free mean"},
+            "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "push_ops_per_step": int(ops), "time_to_l1_ms": 1e3 * total / len(walls)}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    rank, world, local = dist_env()
+    os.environ.setdefault("PUSHRANK_DEVICE", str(local))
+    import torch
+    import paper_2302_03245_b200 as P
+    from paper_2302_03245_b200 import _lib
+    from paper_2302_03245_b200.graph import DeviceGraph
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    n, src, dst = make_host_graph(args.config)
+    t0 = time.perf_counter()
+    g = P.from_edges(n, src, dst, name=args.config)
+    cls = P.classify(g)
+    pg = P.preprocess_ifp2(g, cls)
+    preprocess_s = time.perf_counter() - t0
+    dev = g.dev
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step():
+        flush.zero_()
+        torch.cuda.synchronize()
+        _, _, res, _, _ = dev.run(args.algo, args.mode, DAMPING, XI, 1_000_000, _lib.CONV_SCAN, row_cap=1)
+        return res
+
+    for _ in range(max(args.warmup, 3 if args.warmup < 3 else args.warmup)):
+        step()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    results = []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            results.append(step())
+    torch.cuda.synchronize()
+    dev_ms = [r.push_ms for r in results]
+    loop_ms = [r.round_ms for r in results]
+    ops = [r.push_ops for r in results]
+    total_ms = sum(dev_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * sum(ops) / (total_ms * 1e-3) / 1e9
+    r0 = results[-1]
+    # roofline over the round loop (k_pull dominant): algorithmic bytes / loop time
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = r0.bytes_moved / (r0.round_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"{args.config}_{args.algo}")
+        except Exception:
+            traffic = None
+    launches = sum(3 + r.pull_rounds + 2 * r.push_rounds + (1 if args.algo == "ifp2" else 0) + 1
+                   for r in results)
+    line = {"metric": "GTEPS", "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_desc(args, g.n, g.m),
+            "time_to_l1_ms": statistics.median(dev_ms), "round_loop_ms": statistics.median(loop_ms),
+            "rounds": int(r0.rounds), "pull_rounds": int(r0.pull_rounds), "push_rounds": int(r0.push_rounds),
+            "push_ops_per_step": int(r0.push_ops), "preprocess_s": preprocess_s,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "round loop (k_pull dominant); algorithmic bytes 12*E+40*V+8*n_scan per round",
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
+            "gpu_launches": int(launches), "clocks": clocks.summary()}
+    if not args.no_e2e:
+        line["e2e"] = e2e_measure(args, g, dev)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle
+            host = oracle.graph_arrays(g)
+            gteps, walls, cops, kind = cpu_reference_run(host, args.algo, args.cpu_sample_steps,
+                                                         os.cpu_count() or 1)
+            line["cpu_baseline"] = {"value": gteps, "unit": "GTEPS", "cores": os.cpu_count() or 1,
+                                    "kind": kind, "sample": f"{len(walls)} full {args.algo} solves of "
+                                    f"{args.config} (xi={XI}), median wall {statistics.median(walls):.3f}s, "
+                                    f"{cops} pushes/solve"}
+        except Exception as e:  # baseline failure must not hide the GPU number
+            line["cpu_baseline"] = {"value": None, "unit": "GTEPS", "cores": os.cpu_count(), "kind": "port",
+                                    "sample": f"failed: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def e2e_measure(args, g, dev_resident):
+    """Same metric through the public API from HOST buffers: each step uploads
+    the reference-layout graph (int64 CSR+CSC, pinned), rebuilds the IFP2
+    split on the device, solves, and copies the vector back."""
+    import torch
+    import paper_2302_03245_b200 as P
+    from types import SimpleNamespace
+    arrays = {k: torch.from_numpy(np.ascontiguousarray(getattr(g, k))).pin_memory().numpy()
+              for k in ("out_offsets", "out_targets", "in_offsets", "in_sources")}
+    host = SimpleNamespace(n=g.n, m=g.m, **arrays)
+    h2d = sum(a.nbytes for a in arrays.values())
+    cfg = P.SolverConfig(threshold=XI)
+    times, ops = [], 0
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        obj = SimpleNamespace(**vars(host))
+        if args.algo == "ifp2":
+            pg = P.preprocess_ifp2(obj, None)
+            vec, tr = P.ifp2_run(pg, cfg, mode=args.mode, sample_every=float("inf"))
+        else:
+            vec, tr = P.ifp1_run(obj, None, cfg, mode=args.mode, sample_every=float("inf"))
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+            ops = tr.final.push_ops
+        del obj
+    mean = sum(times) / len(times)
+    return {"value": ops / mean / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(8 * g.n), "ms_per_step": 1e3 * mean,
+            "path": f"{args.algo}_run() on a host-array graph: upload + device preprocess + solve + D2H"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,201 @@
+/*
+ * pushrank_cuda.h -- C-ABI of the B200-native IFP1/IFP2 push-round library
+ * (libpushrank_cuda.so, sm_100a).
+ *
+ * The drop-in boundary.  The reference (pushrank 0.1.0) has one native
+ * seam: the Cython kernel module resolved by _backend.resolve_backend
+ * (/root/reference/pkg/src/pushrank/_backend.py:31-45) exposing
+ * worker_loop/probe (_kernels.pyx:66-137).  That per-CPU-thread protocol
+ * (K free-running loops + a polling monitor) has no GPU meaning, so this
+ * library replaces the layer one level up: the engine entry points
+ * (engines.py ifp1_run/ifp2_run/sync_simulate, solvers.py power_method)
+ * and the graph core they consume (graph.py from_edges/classify/
+ * dangling_target_counts/preprocess_ifp2).  Each entry point below cites
+ * the reference interface it replaces.
+ *
+ * Conventions
+ *  - plain pointers and sizes only; host arrays are caller-owned (the
+ *    reference allocates every array in Python and kernels borrow them,
+ *    engines.py:128-129); device state lives in opaque handles.
+ *  - index arrays crossing the boundary are int64 (the reference's dtype,
+ *    graph.py:141-142); the device keeps int32 column indices + int64
+ *    offsets.
+ *  - every call returns 0 on success or a negative PR_ERR_* code; the
+ *    message is available from pr_last_error() (thread-local).  Argument
+ *    validation with the reference's ValueError texts stays in the Python
+ *    host layer; the library re-checks and fails with PR_ERR_ARG.
+ *  - calls are synchronous on return and stream-ordered on the context's
+ *    stream; one host thread per context.
+ */
+#ifndef PUSHRANK_CUDA_H
+#define PUSHRANK_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PR_OK 0
+#define PR_ERR_ARG (-1)         /* invalid argument (reference: ValueError) */
+#define PR_ERR_CUDA (-2)        /* CUDA runtime / launch failure */
+#define PR_ERR_STATE (-3)       /* missing prerequisite (e.g. preprocess before IFP2) */
+#define PR_ERR_NOT_SETTLED (-4) /* max_rounds exhausted (engines.py:455-456 RuntimeError) */
+#define PR_ERR_NOMEM (-5)       /* device allocation failed */
+
+#define PR_ABI_VERSION 1
+
+typedef struct pr_ctx pr_ctx;       /* one device + stream + workspace */
+typedef struct pr_graph pr_graph;   /* device-resident CSR+CSC and derived data */
+
+/* Per-round trace row; mirrors TraceSample (trace.py:12-38).  Field order
+ * also matches oracle.ROW_DTYPE so rows compare column-for-column. */
+typedef struct pr_round_stats {
+    double h_l1;               /* sum of pending mass over all vertices */
+    double alpha;              /* non-dangling share of above-threshold mass */
+    double active_mass;        /* sum of pending mass above threshold */
+    double carry_mass;         /* h_l1 - active_mass */
+    int64_t converged;         /* #(h <= xi): scan set (engines) or all vertices (sync) */
+    int64_t work;              /* sum(out_degree + 1) over active vertices */
+    int64_t push_ops;          /* cumulative edge pushes before this state */
+    int64_t push_ops_dangling; /* cumulative pushes into dangling vertices */
+    uint64_t digest;           /* exact mode: position-weighted bit digest of (reserved, h) */
+    double wall_ms;            /* device globaltimer since the run started */
+} pr_round_stats;
+
+typedef struct pr_class_counts {    /* VertexClassification (graph.py:68-89) */
+    int64_t dangling, unreferenced, weak_dangling, weak_unreferenced;
+    int64_t dangling_edge_count;    /* m_d */
+    int64_t peel_rounds;
+} pr_class_counts;
+
+typedef struct pr_ifp2_counts {     /* IFP2Graph (graph.py:92-110) */
+    int64_t live_edges, dangling, source_edges;
+} pr_ifp2_counts;
+
+enum pr_algorithm { PR_ALGO_IFP1 = 0, PR_ALGO_IFP2 = 1, PR_ALGO_FPFULL = 2 };
+enum pr_mode {
+    PR_MODE_AUTO = 0,   /* pull (CSC gather) in dense rounds, push (frontier scatter) in sparse ones */
+    PR_MODE_PULL = 1,   /* every round as a deterministic CSC pull */
+    PR_MODE_PUSH = 2,   /* every round (after the first) as a frontier scatter */
+    PR_MODE_EXACT = 3   /* sync_simulate bit-exact: sequential ascending-source sums */
+};
+enum pr_converged_scope { PR_CONV_SCAN = 0, PR_CONV_ALL = 1 };
+
+typedef struct pr_run_params {
+    int32_t algorithm;        /* pr_algorithm */
+    int32_t mode;             /* pr_mode */
+    double damping;           /* c, SolverConfig.damping (solvers.py:39) */
+    double threshold;         /* xi, SolverConfig.threshold (solvers.py:41) */
+    int64_t max_rounds;       /* RuntimeError guard (engines.py:420,455) */
+    double push_switch;       /* AUTO: push when active work < push_switch * pull work; <=0 -> default */
+    int32_t converged_scope;  /* pr_converged_scope */
+    int32_t host_loop;        /* 0: device-side loop (CUDA graph WHILE node); 1: host-driven rounds */
+    /* Optional per-round observer (sync_simulate's on_iteration(t, reserved,
+     * pushing), engines.py:453-454).  EXACT mode only; forces host_loop.
+     * The host arrays are valid for the duration of the call. */
+    void (*on_round)(void *user, int64_t t, const double *reserved, const double *pending);
+    void *user;
+} pr_run_params;
+
+typedef struct pr_run_result {
+    int64_t rounds;           /* push rounds executed (sync_simulate "iterations") */
+    int64_t rows;             /* trace rows produced (may exceed row_cap; extra rows dropped) */
+    int64_t push_ops;         /* final cumulative push count (incl. IFP2 settle) */
+    int64_t push_ops_dangling;
+    int64_t settled;          /* IFP2 settle pushes (= m_d) */
+    int64_t pull_rounds, push_rounds;
+    double mass_total;        /* PageRankVector.mass_total */
+    double push_ms;           /* device time: first round .. normalised output (CUDA events) */
+    double round_ms;          /* device time of the round loop alone */
+    double bytes_moved;       /* algorithmic bytes of the round loop (DESIGN.md roofline) */
+} pr_run_result;
+
+/* ---- library / context ------------------------------------------------ */
+int pr_abi_version(void);
+const char *pr_last_error(void);
+int pr_device_count(int *count);
+int pr_ctx_create(int device, pr_ctx **out);
+int pr_ctx_destroy(pr_ctx *ctx);
+int pr_ctx_synchronize(pr_ctx *ctx);
+
+/* ---- graph core ---------------------------------------------------------
+ * graph.py:133-177 from_edges: dedup (src,dst) pairs, keep self-loops,
+ * CSR sorted by (src,dst), CSC ascending source within a target. */
+int pr_graph_from_edges(pr_ctx *ctx, int64_t n, const int64_t *src, const int64_t *dst,
+                        int64_t m_raw, pr_graph **out);
+/* Same from device-resident int64 edge arrays (e.g. pr_rmat_generate output). */
+int pr_graph_from_device_edges(pr_ctx *ctx, int64_t n, const int64_t *d_src,
+                               const int64_t *d_dst, int64_t m_raw, pr_graph **out);
+/* Upload an already-built reference Graph (graph.py:21-42 arrays). */
+int pr_graph_upload(pr_ctx *ctx, int64_t n, int64_t m, const int64_t *out_offsets,
+                    const int64_t *out_targets, const int64_t *in_offsets,
+                    const int64_t *in_sources, pr_graph **out);
+int pr_graph_destroy(pr_graph *g);
+int pr_graph_info(const pr_graph *g, int64_t *n, int64_t *m);
+/* Graph arrays back to the host (int64, reference layout); NULL skips one. */
+int pr_graph_export(pr_graph *g, int64_t *out_offsets, int64_t *out_targets,
+                    int64_t *in_offsets, int64_t *in_sources);
+
+/* graph.py:274-318 classify: base sets + joint weak peel; result stays on
+ * the device, counts returned. */
+int pr_classify(pr_graph *g, pr_class_counts *counts);
+/* ascending id arrays sized by pr_classify's counts; NULL skips one */
+int pr_classify_export(pr_graph *g, int64_t *dangling, int64_t *unreferenced,
+                       int64_t *weak_dangling, int64_t *weak_unreferenced);
+/* graph.py:334-340 dangling_target_counts -> int64[n] */
+int pr_dangling_target_counts(pr_graph *g, int64_t *out);
+/* graph.py:343-378 preprocess_ifp2: live CSR + dangling-source CSR on device */
+int pr_preprocess_ifp2(pr_graph *g, pr_ifp2_counts *counts);
+int pr_ifp2_export(pr_graph *g, int64_t *live_offsets, int64_t *live_targets,
+                   int64_t *live_degree, int64_t *dangling_ids, int64_t *source_offsets,
+                   int64_t *source_ids);
+
+/* ---- engines ------------------------------------------------------------
+ * engines.py:225-266 ifp1_run, engines.py:292-343 ifp2_run (+ settle
+ * engines.py:269-289) and engines.py:349-485 sync_simulate.
+ * Host outputs (values/reserved/pending, n doubles each; NULL skips one),
+ * rows: up to row_cap trace rows. */
+int pr_run(pr_graph *g, const pr_run_params *params, double *values, double *reserved,
+           double *pending, pr_round_stats *rows, int64_t row_cap, pr_run_result *result);
+/* Same with device output pointers (values may be NULL): no host copies. */
+int pr_run_device(pr_graph *g, const pr_run_params *params, double *d_values,
+                  double *d_reserved, double *d_pending, pr_round_stats *rows,
+                  int64_t row_cap, pr_run_result *result);
+
+/* solvers.py:186-243 power_method: pi (n doubles); per iteration k:
+ * deltas[k] = L1 change (trace.h_l1) and converged[k] = #(|pi_k - pi_{k-1}| <=
+ * threshold) (solvers.py:225-231); either may be NULL.  personalization may
+ * be NULL (uniform 1/n).  result->rounds = iterations executed (early stop
+ * when tolerance > 0 and delta < tolerance, solvers.py:234). */
+int pr_power(pr_graph *g, double damping, int64_t iterations, double tolerance, double threshold,
+             const double *personalization, double *pi, double *deltas, int64_t *converged,
+             pr_run_result *result);
+/* Same with on_iterate(k, pi) (solvers.py:232-233): called after every
+ * iteration with the host copy of the iterate; a non-zero return stops. */
+int pr_power_observed(pr_graph *g, double damping, int64_t iterations, double tolerance,
+                      double threshold, const double *personalization, double *pi, double *deltas,
+                      int64_t *converged, int (*on_iterate)(void *user, int64_t k, const double *pi),
+                      void *user, pr_run_result *result);
+
+/* ---- synthetic inputs ---------------------------------------------------
+ * Device R-MAT sampler, bit-identical to synthetic.rmat_edges (counter
+ * based splitmix64): samples first..first+count into device int64 arrays. */
+int pr_rmat_generate(pr_ctx *ctx, int scale, int64_t edge_factor, double a, double b,
+                     double c, uint64_t seed, int64_t first, int64_t count,
+                     int64_t *d_src, int64_t *d_dst);
+/* Build C2/C3/C5-shaped graphs entirely on the device: R-MAT samples, self
+ * loops removed, optional seeded out-edge drop handled by the caller. */
+int pr_graph_rmat(pr_ctx *ctx, int scale, int64_t edge_factor, double a, double b, double c,
+                  uint64_t seed, pr_graph **out);
+
+/* ---- device buffers (for torch-free hosts and tests) ---------------------- */
+int pr_device_alloc(pr_ctx *ctx, int64_t bytes, void **d_ptr);
+int pr_device_free(pr_ctx *ctx, void *d_ptr);
+int pr_memcpy_h2d(pr_ctx *ctx, void *d_dst, const void *h_src, int64_t bytes);
+int pr_memcpy_d2h(pr_ctx *ctx, void *h_dst, const void *d_src, int64_t bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PUSHRANK_CUDA_H */

@@ -1,0 +1,351 @@
+// capi.cu -- extern "C" boundary of libpushrank_cuda (include/pushrank_cuda.h).
+#include <cstring>
+#include <string>
+
+#include "internal.cuh"
+
+namespace pr {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+int fail(int code, const std::string &msg) {
+    set_error(msg);
+    return code;
+}
+
+int classify_export(Graph &g, int64_t *outs[4]);
+int rmat_generate(Ctx &ctx, int scale, double a, double b, double c, uint64_t seed, int64_t first, int64_t count,
+                  int64_t *d_src, int64_t *d_dst);
+int graph_rmat(Ctx &ctx, int scale, int64_t ef, double a, double b, double c, uint64_t seed, Graph **out);
+int upload_graph(Ctx &ctx, int64_t n, int64_t m, const int64_t *out_off, const int64_t *out_tgt,
+                 const int64_t *in_off, const int64_t *in_src, Graph **out);
+int export_graph(Graph &g, int64_t *out_off, int64_t *out_tgt, int64_t *in_off, int64_t *in_src);
+int export_i32(Ctx &ctx, const DevBuf &src, int64_t count, int64_t *host);
+int export_i64(Ctx &ctx, const DevBuf &src, int64_t count, int64_t *host);
+
+static int set_device(Ctx &ctx) {
+    PR_CUDA(cudaSetDevice(ctx.device));
+    return PR_OK;
+}
+
+}  // namespace pr
+
+using namespace pr;
+
+struct pr_ctx {
+    Ctx c;
+};
+struct pr_graph {
+    Graph *g;
+};
+
+#define CHECK_PTR(p, name) \
+    if (!(p)) return fail(PR_ERR_ARG, std::string(name) + " is NULL")
+
+extern "C" {
+
+int pr_abi_version(void) { return PR_ABI_VERSION; }
+
+const char *pr_last_error(void) { return g_last_error.c_str(); }
+
+int pr_device_count(int *count) {
+    CHECK_PTR(count, "count");
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *count = 0;
+        return fail(PR_ERR_CUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    }
+    *count = c;
+    return PR_OK;
+}
+
+int pr_ctx_create(int device, pr_ctx **out) {
+    CHECK_PTR(out, "out");
+    *out = nullptr;
+    int count = 0;
+    PR_TRY(pr_device_count(&count));
+    if (device < 0 || device >= count)
+        return fail(PR_ERR_ARG, "device " + std::to_string(device) + " not present (" + std::to_string(count) +
+                                    " CUDA devices)");
+    pr_ctx *c = new pr_ctx();
+    c->c.device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) {
+        cudaDeviceProp prop;
+        e = cudaGetDeviceProperties(&prop, device);
+        if (e == cudaSuccess) {
+            c->c.sm_count = prop.multiProcessorCount;
+            c->c.l2_bytes = (size_t)prop.l2CacheSize;
+            if (prop.major < 10) {
+                cudaStreamDestroy(c->c.stream);
+                delete c;
+                return fail(PR_ERR_STATE, std::string("device ") + prop.name + " is sm_" +
+                                              std::to_string(prop.major * 10 + prop.minor) +
+                                              "; this library is built for sm_100a (B200)");
+            }
+        }
+    }
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(PR_ERR_CUDA, std::string("context init: ") + cudaGetErrorString(e));
+    }
+    *out = c;
+    return PR_OK;
+}
+
+int pr_ctx_destroy(pr_ctx *ctx) {
+    if (!ctx) return PR_OK;
+    cudaSetDevice(ctx->c.device);
+    cudaStreamSynchronize(ctx->c.stream);
+    ctx->c.scratch.release();
+    ctx->c.flush.release();
+    cudaStreamDestroy(ctx->c.stream);
+    delete ctx;
+    return PR_OK;
+}
+
+int pr_ctx_synchronize(pr_ctx *ctx) {
+    CHECK_PTR(ctx, "ctx");
+    PR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    return PR_OK;
+}
+
+int pr_graph_from_edges(pr_ctx *ctx, int64_t n, const int64_t *src, const int64_t *dst, int64_t m_raw,
+                        pr_graph **out) {
+    CHECK_PTR(ctx, "ctx");
+    CHECK_PTR(out, "out");
+    if (m_raw < 0) return fail(PR_ERR_ARG, "negative edge count");
+    if (m_raw > 0) {
+        CHECK_PTR(src, "src");
+        CHECK_PTR(dst, "dst");
+    }
+    PR_TRY(set_device(ctx->c));
+    DevBuf ds, dd;
+    PR_TRY(ensure(ds, 8 * (m_raw ? m_raw : 1)));
+    PR_TRY(ensure(dd, 8 * (m_raw ? m_raw : 1)));
+    if (m_raw) {
+        PR_CUDA(cudaMemcpyAsync(ds.ptr, src, 8 * m_raw, cudaMemcpyHostToDevice, ctx->c.stream));
+        PR_CUDA(cudaMemcpyAsync(dd.ptr, dst, 8 * m_raw, cudaMemcpyHostToDevice, ctx->c.stream));
+    }
+    Graph *g = nullptr;
+    PR_TRY(build_from_device_edges(ctx->c, n, ds.as<int64_t>(), dd.as<int64_t>(), m_raw, &g));
+    *out = new pr_graph{g};
+    return PR_OK;
+}
+
+int pr_graph_from_device_edges(pr_ctx *ctx, int64_t n, const int64_t *d_src, const int64_t *d_dst, int64_t m_raw,
+                               pr_graph **out) {
+    CHECK_PTR(ctx, "ctx");
+    CHECK_PTR(out, "out");
+    PR_TRY(set_device(ctx->c));
+    Graph *g = nullptr;
+    PR_TRY(build_from_device_edges(ctx->c, n, d_src, d_dst, m_raw, &g));
+    *out = new pr_graph{g};
+    return PR_OK;
+}
+
+int pr_graph_upload(pr_ctx *ctx, int64_t n, int64_t m, const int64_t *out_offsets, const int64_t *out_targets,
+                    const int64_t *in_offsets, const int64_t *in_sources, pr_graph **out) {
+    CHECK_PTR(ctx, "ctx");
+    CHECK_PTR(out, "out");
+    CHECK_PTR(out_offsets, "out_offsets");
+    CHECK_PTR(in_offsets, "in_offsets");
+    if (m > 0) {
+        CHECK_PTR(out_targets, "out_targets");
+        CHECK_PTR(in_sources, "in_sources");
+    }
+    PR_TRY(set_device(ctx->c));
+    Graph *g = nullptr;
+    PR_TRY(upload_graph(ctx->c, n, m, out_offsets, out_targets, in_offsets, in_sources, &g));
+    *out = new pr_graph{g};
+    return PR_OK;
+}
+
+int pr_graph_destroy(pr_graph *g) {
+    if (!g) return PR_OK;
+    cudaSetDevice(g->g->ctx->device);
+    cudaStreamSynchronize(g->g->ctx->stream);
+    delete g->g;
+    delete g;
+    return PR_OK;
+}
+
+int pr_graph_info(const pr_graph *g, int64_t *n, int64_t *m) {
+    CHECK_PTR(g, "graph");
+    if (n) *n = g->g->n;
+    if (m) *m = g->g->m;
+    return PR_OK;
+}
+
+int pr_graph_export(pr_graph *g, int64_t *out_offsets, int64_t *out_targets, int64_t *in_offsets,
+                    int64_t *in_sources) {
+    CHECK_PTR(g, "graph");
+    PR_TRY(set_device(*g->g->ctx));
+    return export_graph(*g->g, out_offsets, out_targets, in_offsets, in_sources);
+}
+
+int pr_classify(pr_graph *g, pr_class_counts *counts) {
+    CHECK_PTR(g, "graph");
+    PR_TRY(set_device(*g->g->ctx));
+    PR_TRY(classify_device(*g->g));
+    if (counts) *counts = g->g->counts;
+    return PR_OK;
+}
+
+int pr_classify_export(pr_graph *g, int64_t *dangling, int64_t *unreferenced, int64_t *weak_dangling,
+                       int64_t *weak_unreferenced) {
+    CHECK_PTR(g, "graph");
+    PR_TRY(set_device(*g->g->ctx));
+    int64_t *outs[4] = {dangling, unreferenced, weak_dangling, weak_unreferenced};
+    return classify_export(*g->g, outs);
+}
+
+int pr_dangling_target_counts(pr_graph *g, int64_t *out) {
+    CHECK_PTR(g, "graph");
+    CHECK_PTR(out, "out");
+    PR_TRY(set_device(*g->g->ctx));
+    PR_TRY(ensure_dtc(*g->g));
+    return export_i32(*g->g->ctx, g->g->dtc, g->g->n, out);
+}
+
+int pr_preprocess_ifp2(pr_graph *g, pr_ifp2_counts *counts) {
+    CHECK_PTR(g, "graph");
+    PR_TRY(set_device(*g->g->ctx));
+    PR_TRY(preprocess_ifp2_device(*g->g));
+    if (counts) *counts = g->g->ifp2;
+    return PR_OK;
+}
+
+int pr_ifp2_export(pr_graph *g, int64_t *live_offsets, int64_t *live_targets, int64_t *live_degree,
+                   int64_t *dangling_ids, int64_t *source_offsets, int64_t *source_ids) {
+    CHECK_PTR(g, "graph");
+    Graph &G = *g->g;
+    if (!G.has_ifp2) return fail(PR_ERR_STATE, "pr_preprocess_ifp2 has not run");
+    PR_TRY(set_device(*G.ctx));
+    Ctx &c = *G.ctx;
+    PR_TRY(export_i64(c, G.live_off, G.n + 1, live_offsets));
+    PR_TRY(export_i32(c, G.live_tgt, G.ifp2.live_edges, live_targets));
+    PR_TRY(export_i32(c, G.live_deg, G.n, live_degree));
+    PR_TRY(export_i32(c, G.dang_ids, G.ifp2.dangling, dangling_ids));
+    PR_TRY(export_i64(c, G.src_off, G.ifp2.dangling + 1, source_offsets));
+    PR_TRY(export_i32(c, G.src_ids, G.ifp2.source_edges, source_ids));
+    return PR_OK;
+}
+
+static int run_common(pr_graph *g, const pr_run_params *params, double *values, double *reserved, double *pending,
+                      pr_round_stats *rows, int64_t row_cap, pr_run_result *result, bool host_out) {
+    CHECK_PTR(g, "graph");
+    CHECK_PTR(params, "params");
+    Graph &G = *g->g;
+    PR_TRY(set_device(*G.ctx));
+    cudaStream_t st = G.ctx->stream;
+    DevBuf dv;
+    double *d_values = nullptr;
+    if (values) {
+        if (host_out) {
+            PR_TRY(ensure(dv, 8 * G.n));
+            d_values = dv.as<double>();
+        } else {
+            d_values = values;
+        }
+    }
+    pr_run_result local;
+    memset(&local, 0, sizeof(local));
+    int rc = run_rounds(G, *params, d_values, rows, row_cap, &local);
+    if (result) *result = local;
+    if (rc != PR_OK && rc != PR_ERR_NOT_SETTLED) return rc;
+    cudaMemcpyKind kind = host_out ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (values && host_out) PR_CUDA(cudaMemcpyAsync(values, d_values, 8 * G.n, kind, st));
+    if (reserved) PR_CUDA(cudaMemcpyAsync(reserved, G.reserved.ptr, 8 * G.n, kind, st));
+    if (pending) PR_CUDA(cudaMemcpyAsync(pending, G.h.ptr, 8 * G.n, kind, st));
+    PR_CUDA(cudaStreamSynchronize(st));
+    return rc;
+}
+
+int pr_run(pr_graph *g, const pr_run_params *params, double *values, double *reserved, double *pending,
+           pr_round_stats *rows, int64_t row_cap, pr_run_result *result) {
+    return run_common(g, params, values, reserved, pending, rows, row_cap, result, true);
+}
+
+int pr_run_device(pr_graph *g, const pr_run_params *params, double *d_values, double *d_reserved,
+                  double *d_pending, pr_round_stats *rows, int64_t row_cap, pr_run_result *result) {
+    return run_common(g, params, d_values, d_reserved, d_pending, rows, row_cap, result, false);
+}
+
+int pr_power(pr_graph *g, double damping, int64_t iterations, double tolerance, double threshold,
+             const double *personalization, double *pi, double *deltas, int64_t *converged,
+             pr_run_result *result) {
+    CHECK_PTR(g, "graph");
+    PR_TRY(set_device(*g->g->ctx));
+    return power_device(*g->g, damping, iterations, tolerance, threshold, personalization, pi, deltas, converged,
+                        nullptr, nullptr, result);
+}
+
+int pr_power_observed(pr_graph *g, double damping, int64_t iterations, double tolerance, double threshold,
+                      const double *personalization, double *pi, double *deltas, int64_t *converged,
+                      int (*on_iterate)(void *user, int64_t k, const double *pi), void *user,
+                      pr_run_result *result) {
+    CHECK_PTR(g, "graph");
+    PR_TRY(set_device(*g->g->ctx));
+    return power_device(*g->g, damping, iterations, tolerance, threshold, personalization, pi, deltas, converged,
+                        on_iterate, user, result);
+}
+
+int pr_rmat_generate(pr_ctx *ctx, int scale, int64_t edge_factor, double a, double b, double c, uint64_t seed,
+                     int64_t first, int64_t count, int64_t *d_src, int64_t *d_dst) {
+    CHECK_PTR(ctx, "ctx");
+    (void)edge_factor;
+    PR_TRY(set_device(ctx->c));
+    PR_TRY(rmat_generate(ctx->c, scale, a, b, c, seed, first, count, d_src, d_dst));
+    PR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    return PR_OK;
+}
+
+int pr_graph_rmat(pr_ctx *ctx, int scale, int64_t edge_factor, double a, double b, double c, uint64_t seed,
+                  pr_graph **out) {
+    CHECK_PTR(ctx, "ctx");
+    CHECK_PTR(out, "out");
+    PR_TRY(set_device(ctx->c));
+    Graph *g = nullptr;
+    PR_TRY(graph_rmat(ctx->c, scale, edge_factor, a, b, c, seed, &g));
+    *out = new pr_graph{g};
+    return PR_OK;
+}
+
+int pr_device_alloc(pr_ctx *ctx, int64_t bytes, void **d_ptr) {
+    CHECK_PTR(ctx, "ctx");
+    CHECK_PTR(d_ptr, "d_ptr");
+    PR_TRY(set_device(ctx->c));
+    PR_CUDA(cudaMalloc(d_ptr, bytes > 0 ? (size_t)bytes : 16));
+    return PR_OK;
+}
+
+int pr_device_free(pr_ctx *ctx, void *d_ptr) {
+    CHECK_PTR(ctx, "ctx");
+    PR_TRY(set_device(ctx->c));
+    PR_CUDA(cudaFree(d_ptr));
+    return PR_OK;
+}
+
+int pr_memcpy_h2d(pr_ctx *ctx, void *d_dst, const void *h_src, int64_t bytes) {
+    CHECK_PTR(ctx, "ctx");
+    PR_TRY(set_device(ctx->c));
+    PR_CUDA(cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, ctx->c.stream));
+    PR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    return PR_OK;
+}
+
+int pr_memcpy_d2h(pr_ctx *ctx, void *h_dst, const void *d_src, int64_t bytes) {
+    CHECK_PTR(ctx, "ctx");
+    PR_TRY(set_device(ctx->c));
+    PR_CUDA(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, ctx->c.stream));
+    PR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    return PR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,734 @@
+// graph.cu -- device graph core: K1 (from_edges), K2 (classify + joint
+// peel), K3 (dangling_target_counts, preprocess_ifp2), pull schedules and
+// the R-MAT sampler.  Integer-only, bit-exact with the reference
+// (graph.py:133-177, 274-318, 334-340, 343-378).
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "internal.cuh"
+
+namespace pr {
+
+int ensure(DevBuf &b, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (b.bytes >= bytes) return PR_OK;
+    b.release();
+    cudaError_t e = cudaMalloc(&b.ptr, bytes);
+    if (e != cudaSuccess) {
+        b.ptr = nullptr;
+        cudaGetLastError();
+        return fail(PR_ERR_NOMEM, "cudaMalloc(" + std::to_string(bytes) + " B) failed: " +
+                                      cudaGetErrorString(e));
+    }
+    b.bytes = bytes;
+    return PR_OK;
+}
+
+Graph::~Graph() {
+    for (auto &c : cached) {
+        if (c.exec) cudaGraphExecDestroy(c.exec);
+        if (c.graph) cudaGraphDestroy(c.graph);
+    }
+}
+
+// Run a CUB algorithm: size query, grow ctx scratch, execute.
+template <class F> static int cub_run(Ctx &ctx, F &&f) {
+    size_t bytes = 0;
+    PR_CUDA(f((void *)nullptr, bytes));
+    PR_TRY(ensure(ctx.scratch, bytes));
+    PR_CUDA(f(ctx.scratch.ptr, bytes));
+    return PR_OK;
+}
+
+static int bit_width_u64(unsigned long long x) {
+    int b = 0;
+    while (x) { ++b; x >>= 1; }
+    return b;
+}
+
+#define GRID_STRIDE(i, count) \
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (count); i += (int64_t)gridDim.x * blockDim.x)
+
+// ---------------------------------------------------------------- elementwise helpers
+
+__global__ void k_degree(const int64_t *__restrict__ off, int64_t n, int32_t *__restrict__ deg) {
+    GRID_STRIDE(v, n) deg[v] = (int32_t)(off[v + 1] - off[v]);
+}
+
+__global__ void k_narrow(const int64_t *__restrict__ in, int64_t count, int32_t *__restrict__ out) {
+    GRID_STRIDE(i, count) out[i] = (int32_t)in[i];
+}
+
+__global__ void k_widen(const int32_t *__restrict__ in, int64_t count, int64_t *__restrict__ out) {
+    GRID_STRIDE(i, count) out[i] = in[i];
+}
+
+__global__ void k_gather_i32(const int32_t *__restrict__ src, const int64_t *__restrict__ idx, int64_t count,
+                             int32_t *__restrict__ out) {
+    GRID_STRIDE(i, count) out[i] = src[idx[i]];
+}
+
+__global__ void k_gather_i64_pair(const int64_t *__restrict__ a, const int64_t *__restrict__ b,
+                                  const int64_t *__restrict__ idx, int64_t count, int64_t *__restrict__ oa,
+                                  int64_t *__restrict__ ob) {
+    GRID_STRIDE(i, count) {
+        int64_t j = idx[i];
+        oa[i] = a[j];
+        ob[i] = b[j];
+    }
+}
+
+static unsigned gs_grid(Ctx &ctx, int64_t items) {
+    int64_t b = (items + 255) / 256;
+    int64_t cap = (int64_t)ctx.sm_count * 16;
+    if (b > cap) b = cap;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+// ---------------------------------------------------------------- K1: from_edges
+
+__global__ void k_edge_keys(const int64_t *__restrict__ src, const int64_t *__restrict__ dst, int64_t m, int64_t n,
+                            unsigned long long *__restrict__ keys, int *__restrict__ bad) {
+    GRID_STRIDE(i, m) {
+        int64_t s = src[i], t = dst[i];
+        if (s < 0 || t < 0 || s >= n || t >= n) { *bad = 1; s = 0; t = 0; }
+        keys[i] = (unsigned long long)s * (unsigned long long)n + (unsigned long long)t;
+    }
+}
+
+// sorted unique keys (row-major) -> column index + row offsets by boundary
+// detection: off[v] = first position whose row >= v (no atomics, O(n+m)).
+__global__ void k_split_keys(const unsigned long long *__restrict__ keys, int64_t m, int64_t n,
+                             int32_t *__restrict__ col, int64_t *__restrict__ off) {
+    GRID_STRIDE(e, m + 1) {
+        int64_t row = e < m ? (int64_t)(keys[e] / (unsigned long long)n) : n;
+        int64_t prev = e > 0 ? (int64_t)(keys[e - 1] / (unsigned long long)n) : -1;
+        if (e < m) col[e] = (int32_t)(keys[e] % (unsigned long long)n);
+        for (int64_t v = prev + 1; v <= row; ++v) off[v] = e;
+    }
+}
+
+__global__ void k_transpose_keys(const unsigned long long *__restrict__ keys, int64_t m, int64_t n,
+                                 unsigned long long *__restrict__ out) {
+    GRID_STRIDE(e, m) {
+        unsigned long long k = keys[e];
+        unsigned long long s = k / (unsigned long long)n, t = k % (unsigned long long)n;
+        out[e] = t * (unsigned long long)n + s;
+    }
+}
+
+static int alloc_graph_arrays(Graph &g) {
+    PR_TRY(ensure(g.out_off, sizeof(int64_t) * (g.n + 1)));
+    PR_TRY(ensure(g.in_off, sizeof(int64_t) * (g.n + 1)));
+    PR_TRY(ensure(g.out_deg, sizeof(int32_t) * g.n));
+    PR_TRY(ensure(g.out_tgt, sizeof(int32_t) * g.m));
+    PR_TRY(ensure(g.in_src, sizeof(int32_t) * g.m));
+    return PR_OK;
+}
+
+static int build_body(Ctx &ctx, Graph &g, const int64_t *d_src, const int64_t *d_dst, int64_t m_raw) {
+    cudaStream_t st = ctx.stream;
+    int64_t n = g.n;
+    DevBuf keys, alt, flag, cnt;
+    PR_TRY(ensure(keys, sizeof(unsigned long long) * m_raw));
+    PR_TRY(ensure(alt, sizeof(unsigned long long) * m_raw));
+    PR_TRY(ensure(flag, sizeof(int)));
+    PR_TRY(ensure(cnt, sizeof(int64_t)));
+    PR_CUDA(cudaMemsetAsync(flag.ptr, 0, sizeof(int), st));
+    int64_t m = 0;
+    int bits = bit_width_u64((unsigned long long)n * (unsigned long long)n - 1ull);
+    if (bits < 1) bits = 1;
+    unsigned long long *K = keys.as<unsigned long long>(), *A = alt.as<unsigned long long>();
+    if (m_raw > 0) {
+        k_edge_keys<<<gs_grid(ctx, m_raw), 256, 0, st>>>(d_src, d_dst, m_raw, n, K, flag.as<int>());
+        int bad = 0;
+        PR_CUDA(cudaMemcpyAsync(&bad, flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+        if (bad) return fail(PR_ERR_ARG, "vertex id out of range");
+        // (src,dst) order + dedup == np.unique(src*n+dst) (graph.py:151-152)
+        PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceRadixSort::SortKeys(t, b, K, A, (int)m_raw, 0, bits, st);
+        }));
+        PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceSelect::Unique(t, b, A, K, cnt.as<int64_t>(), (int)m_raw, st);
+        }));
+        PR_CUDA(cudaMemcpyAsync(&m, cnt.ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+    }
+    g.m = m;
+    PR_TRY(alloc_graph_arrays(g));
+    k_split_keys<<<gs_grid(ctx, m + 1), 256, 0, st>>>(K, m, n, g.out_tgt.as<int32_t>(), g.out_off.as<int64_t>());
+    k_degree<<<gs_grid(ctx, n), 256, 0, st>>>(g.out_off.as<int64_t>(), n, g.out_deg.as<int32_t>());
+    if (m > 0) {
+        // CSC: full sort on (dst,src) == stable argsort(dst) of the (src,dst) order (graph.py:164)
+        k_transpose_keys<<<gs_grid(ctx, m), 256, 0, st>>>(K, m, n, A);
+        PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceRadixSort::SortKeys(t, b, A, K, (int)m, 0, bits, st);
+        }));
+    }
+    k_split_keys<<<gs_grid(ctx, m + 1), 256, 0, st>>>(K, m, n, g.in_src.as<int32_t>(), g.in_off.as<int64_t>());
+    PR_CUDA(cudaStreamSynchronize(st));
+    PR_CUDA(cudaGetLastError());
+    return PR_OK;
+}
+
+int build_from_device_edges(Ctx &ctx, int64_t n, const int64_t *d_src, const int64_t *d_dst, int64_t m_raw,
+                            Graph **out) {
+    if (n < 1) return fail(PR_ERR_ARG, "graph must have at least one vertex");
+    if (n > INT32_MAX - 1) return fail(PR_ERR_ARG, "n exceeds the int32 column-index range");
+    if (m_raw > INT32_MAX) return fail(PR_ERR_ARG, "edge sample count exceeds 2^31-1");
+    Graph *g = new Graph();
+    g->ctx = &ctx;
+    g->n = n;
+    g->raw = m_raw;
+    int rc = build_body(ctx, *g, d_src, d_dst, m_raw);
+    if (rc) { delete g; return rc; }
+    *out = g;
+    return PR_OK;
+}
+
+// ---------------------------------------------------------------- K2: classify
+
+__global__ void k_classify_init(const int32_t *__restrict__ out_deg, const int64_t *__restrict__ in_off, int64_t n,
+                                uint8_t *__restrict__ flags, int32_t *__restrict__ cur_out,
+                                int32_t *__restrict__ cur_in, uint8_t *__restrict__ alive,
+                                int32_t *__restrict__ mark, int32_t *__restrict__ frontier,
+                                unsigned long long *__restrict__ fsize, unsigned long long *__restrict__ m_d) {
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    unsigned long long md = 0;
+    bool doomed = false;
+    if (v < n) {
+        int32_t od = out_deg[v];
+        int32_t id = (int32_t)(in_off[v + 1] - in_off[v]);
+        flags[v] = (uint8_t)((od == 0 ? 1 : 0) | (id == 0 ? 2 : 0));
+        cur_out[v] = od;
+        cur_in[v] = id;
+        alive[v] = 1;
+        mark[v] = 0;
+        if (od == 0) md = (unsigned long long)id;  // graph.py:285
+        doomed = od == 0 || id == 0;              // graph.py:293
+    }
+    // warp-aggregated frontier append
+    unsigned ballot = __ballot_sync(0xffffffffu, doomed);
+    int lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (lane == 0 && ballot) base = atomicAdd(fsize, (unsigned long long)__popc(ballot));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (doomed) frontier[base + __popc(ballot & ((1u << lane) - 1u))] = (int32_t)v;
+    for (int o = 16; o > 0; o >>= 1) md += __shfl_down_sync(0xffffffffu, md, o);
+    if (lane == 0 && md) atomicAdd(m_d, md);
+}
+
+__global__ void k_peel_kill(const int32_t *__restrict__ frontier, int64_t count, uint8_t *__restrict__ alive) {
+    GRID_STRIDE(i, count) alive[frontier[i]] = 0;  // graph.py:296
+}
+
+__device__ __forceinline__ void peel_candidate(int32_t v, int32_t round, int32_t *mark, int32_t *next,
+                                               unsigned long long *nsize) {
+    if (atomicCAS(&mark[v], 0, round) == 0) next[atomicAdd(nsize, 1ull)] = v;
+}
+
+// warp per victim: decrement live neighbours' counters (graph.py:298-304);
+// a counter reaching zero makes that vertex a candidate of the next round
+__global__ void k_peel_decrement(const int32_t *__restrict__ frontier, int64_t count,
+                                 const int64_t *__restrict__ out_off, const int32_t *__restrict__ out_tgt,
+                                 const int64_t *__restrict__ in_off, const int32_t *__restrict__ in_src,
+                                 const uint8_t *__restrict__ alive, int32_t *__restrict__ cur_out,
+                                 int32_t *__restrict__ cur_in, int32_t *__restrict__ mark, int32_t round,
+                                 int32_t *__restrict__ next, unsigned long long *__restrict__ nsize) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < count; i += nwarps) {
+        int32_t v = frontier[i];
+        for (int64_t e = out_off[v] + lane; e < out_off[v + 1]; e += 32) {
+            int32_t t = out_tgt[e];
+            if (alive[t] && atomicSub(&cur_in[t], 1) == 1) peel_candidate(t, round, mark, next, nsize);
+        }
+        for (int64_t e = in_off[v] + lane; e < in_off[v + 1]; e += 32) {
+            int32_t s = in_src[e];
+            if (alive[s] && atomicSub(&cur_out[s], 1) == 1) peel_candidate(s, round, mark, next, nsize);
+        }
+    }
+}
+
+// newly exposed vertices become weak (graph.py:306-310)
+__global__ void k_peel_flag(const int32_t *__restrict__ next, int64_t count, const int32_t *__restrict__ cur_out,
+                            const int32_t *__restrict__ cur_in, uint8_t *__restrict__ flags) {
+    GRID_STRIDE(i, count) {
+        int32_t v = next[i];
+        uint8_t f = flags[v];
+        if (cur_out[v] == 0 && !(f & 1)) f |= 4;
+        if (cur_in[v] == 0 && !(f & 2)) f |= 8;
+        flags[v] = f;
+    }
+}
+
+struct BitSet {
+    const uint8_t *flags;
+    uint8_t bit;
+    __host__ __device__ bool operator()(int32_t v) const { return (flags[v] & bit) != 0; }
+};
+
+// ascending id list of vertices whose flag has `bit` (np.flatnonzero order)
+static int compact_flag(Ctx &ctx, const uint8_t *flags, uint8_t bit, int64_t n, int32_t *out, int64_t *d_count,
+                        int64_t *h_count) {
+    auto first = thrust::make_counting_iterator<int32_t>(0);
+    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceSelect::If(t, b, first, out, d_count, (int)n, BitSet{flags, bit}, ctx.stream);
+    }));
+    if (h_count) {
+        PR_CUDA(cudaMemcpyAsync(h_count, d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.stream));
+        PR_CUDA(cudaStreamSynchronize(ctx.stream));
+    }
+    return PR_OK;
+}
+
+int classify_device(Graph &g) {
+    if (g.classified) return PR_OK;
+    Ctx &ctx = *g.ctx;
+    cudaStream_t st = ctx.stream;
+    int64_t n = g.n;
+    DevBuf cur_out, cur_in, alive, mark, fr0, fr1, sizes;
+    PR_TRY(ensure(g.cls_flags, n));
+    PR_TRY(ensure(cur_out, 4 * n));
+    PR_TRY(ensure(cur_in, 4 * n));
+    PR_TRY(ensure(alive, n));
+    PR_TRY(ensure(mark, 4 * n));
+    PR_TRY(ensure(fr0, 4 * n));
+    PR_TRY(ensure(fr1, 4 * n));
+    PR_TRY(ensure(sizes, 4 * sizeof(unsigned long long)));
+    unsigned long long *dsz = sizes.as<unsigned long long>();
+    PR_CUDA(cudaMemsetAsync(dsz, 0, 4 * sizeof(unsigned long long), st));
+    k_classify_init<<<grid_for(n, 256), 256, 0, st>>>(g.out_deg.as<int32_t>(), g.in_off.as<int64_t>(), n,
+                                                      g.cls_flags.as<uint8_t>(), cur_out.as<int32_t>(),
+                                                      cur_in.as<int32_t>(), alive.as<uint8_t>(), mark.as<int32_t>(),
+                                                      fr0.as<int32_t>(), dsz + 0, dsz + 2);
+    unsigned long long hs[4];
+    PR_CUDA(cudaMemcpyAsync(hs, dsz, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaStreamSynchronize(st));
+    int64_t count = (int64_t)hs[0];
+    int64_t m_d = (int64_t)hs[2];
+    int32_t *cur = fr0.as<int32_t>(), *nxt = fr1.as<int32_t>();
+    int64_t rounds = 0;
+    while (count > 0) {
+        ++rounds;
+        PR_CUDA(cudaMemsetAsync(dsz + 1, 0, sizeof(unsigned long long), st));
+        k_peel_kill<<<gs_grid(ctx, count), 256, 0, st>>>(cur, count, alive.as<uint8_t>());
+        k_peel_decrement<<<gs_grid(ctx, count * 32), 256, 0, st>>>(
+            cur, count, g.out_off.as<int64_t>(), g.out_tgt.as<int32_t>(), g.in_off.as<int64_t>(),
+            g.in_src.as<int32_t>(), alive.as<uint8_t>(), cur_out.as<int32_t>(), cur_in.as<int32_t>(),
+            mark.as<int32_t>(), (int32_t)rounds, nxt, dsz + 1);
+        unsigned long long nc = 0;
+        PR_CUDA(cudaMemcpyAsync(&nc, dsz + 1, sizeof(nc), cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+        count = (int64_t)nc;
+        if (count)
+            k_peel_flag<<<gs_grid(ctx, count), 256, 0, st>>>(nxt, count, cur_out.as<int32_t>(), cur_in.as<int32_t>(),
+                                                              g.cls_flags.as<uint8_t>());
+        std::swap(cur, nxt);
+    }
+    PR_CUDA(cudaGetLastError());
+    DevBuf tmp, dcount;
+    PR_TRY(ensure(tmp, 4 * n));
+    PR_TRY(ensure(dcount, sizeof(int64_t)));
+    int64_t c[4];
+    for (int k = 0; k < 4; ++k)
+        PR_TRY(compact_flag(ctx, g.cls_flags.as<uint8_t>(), (uint8_t)(1 << k), n, tmp.as<int32_t>(),
+                            dcount.as<int64_t>(), &c[k]));
+    g.counts.dangling = c[0];
+    g.counts.unreferenced = c[1];
+    g.counts.weak_dangling = c[2];
+    g.counts.weak_unreferenced = c[3];
+    g.counts.dangling_edge_count = m_d;
+    g.counts.peel_rounds = rounds;
+    g.classified = true;
+    return PR_OK;
+}
+
+int classify_export(Graph &g, int64_t *outs[4]) {
+    PR_TRY(classify_device(g));
+    Ctx &ctx = *g.ctx;
+    DevBuf tmp, wide, dcount;
+    PR_TRY(ensure(tmp, 4 * g.n));
+    PR_TRY(ensure(wide, 8 * g.n));
+    PR_TRY(ensure(dcount, sizeof(int64_t)));
+    for (int k = 0; k < 4; ++k) {
+        if (!outs[k]) continue;
+        int64_t cnt = 0;
+        PR_TRY(compact_flag(ctx, g.cls_flags.as<uint8_t>(), (uint8_t)(1 << k), g.n, tmp.as<int32_t>(),
+                            dcount.as<int64_t>(), &cnt));
+        if (cnt) {
+            k_widen<<<gs_grid(ctx, cnt), 256, 0, ctx.stream>>>(tmp.as<int32_t>(), cnt, wide.as<int64_t>());
+            PR_CUDA(cudaMemcpyAsync(outs[k], wide.ptr, 8 * cnt, cudaMemcpyDeviceToHost, ctx.stream));
+            PR_CUDA(cudaStreamSynchronize(ctx.stream));
+        }
+    }
+    return PR_OK;
+}
+
+// ---------------------------------------------------------------- K3
+
+// graph.py:334-340: per-row count of dangling targets
+__global__ void k_dtc(const int64_t *__restrict__ out_off, const int32_t *__restrict__ out_tgt,
+                      const int32_t *__restrict__ out_deg, int64_t n, int32_t *__restrict__ dtc) {
+    GRID_STRIDE(v, n) {
+        int32_t c = 0;
+        for (int64_t e = out_off[v]; e < out_off[v + 1]; ++e) c += out_deg[out_tgt[e]] == 0;
+        dtc[v] = c;
+    }
+}
+
+int ensure_dtc(Graph &g) {
+    if (g.has_dtc) return PR_OK;
+    PR_TRY(ensure(g.dtc, 4 * g.n));
+    k_dtc<<<gs_grid(*g.ctx, g.n), 256, 0, g.ctx->stream>>>(g.out_off.as<int64_t>(), g.out_tgt.as<int32_t>(),
+                                                           g.out_deg.as<int32_t>(), g.n, g.dtc.as<int32_t>());
+    PR_CUDA(cudaGetLastError());
+    g.has_dtc = true;
+    return PR_OK;
+}
+
+struct LiveEdge {
+    const int32_t *tgt, *deg;
+    __host__ __device__ bool operator()(int64_t e) const { return deg[tgt[e]] > 0; }
+};
+struct IsDangling {
+    const int32_t *deg;
+    __host__ __device__ bool operator()(int32_t v) const { return deg[v] == 0; }
+};
+
+__global__ void k_live_degree(const int32_t *__restrict__ out_deg, const int32_t *__restrict__ dtc, int64_t n,
+                              int64_t *__restrict__ live_deg64, int32_t *__restrict__ live_deg) {
+    GRID_STRIDE(v, n) {
+        int32_t d = out_deg[v] - dtc[v];
+        live_deg[v] = d;
+        live_deg64[v] = d;
+    }
+}
+
+__global__ void k_gather_count(const int32_t *__restrict__ ids, int64_t count, const int64_t *__restrict__ in_off,
+                               int64_t *__restrict__ cnt) {
+    GRID_STRIDE(i, count) {
+        int32_t d = ids[i];
+        cnt[i] = in_off[d + 1] - in_off[d];
+    }
+}
+
+// _gather_rows(in_offsets, in_sources, dangling_ids) (graph.py:262-271, 367)
+__global__ void k_gather_rows(const int32_t *__restrict__ ids, int64_t count, const int64_t *__restrict__ in_off,
+                              const int32_t *__restrict__ in_src, const int64_t *__restrict__ dst_off,
+                              int32_t *__restrict__ dst) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < count; i += nwarps) {
+        int32_t d = ids[i];
+        int64_t lo = in_off[d], len = in_off[d + 1] - lo, o = dst_off[i];
+        for (int64_t k = lane; k < len; k += 32) dst[o + k] = in_src[lo + k];
+    }
+}
+
+int preprocess_ifp2_device(Graph &g) {
+    if (g.has_ifp2) return PR_OK;
+    Ctx &ctx = *g.ctx;
+    cudaStream_t st = ctx.stream;
+    int64_t n = g.n, m = g.m;
+    PR_TRY(ensure_dtc(g));
+    DevBuf deg64, dcount;
+    PR_TRY(ensure(deg64, 8 * (n + 1)));
+    PR_TRY(ensure(dcount, sizeof(int64_t)));
+    PR_TRY(ensure(g.live_deg, 4 * n));
+    PR_TRY(ensure(g.live_off, 8 * (n + 1)));
+    k_live_degree<<<gs_grid(ctx, n), 256, 0, st>>>(g.out_deg.as<int32_t>(), g.dtc.as<int32_t>(), n,
+                                                   deg64.as<int64_t>(), g.live_deg.as<int32_t>());
+    PR_CUDA(cudaMemsetAsync(deg64.as<int64_t>() + n, 0, 8, st));
+    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, deg64.as<int64_t>(), g.live_off.as<int64_t>(), (int)(n + 1), st);
+    }));
+    // live_targets: stable compaction keeps each row's target order (graph.py:353-354)
+    PR_TRY(ensure(g.live_tgt, 4 * (m ? m : 1)));
+    int64_t live_m = 0;
+    if (m) {
+        auto first = thrust::make_counting_iterator<int64_t>(0);
+        DevBuf eids;
+        PR_TRY(ensure(eids, 8 * m));
+        PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceSelect::If(t, b, first, eids.as<int64_t>(), dcount.as<int64_t>(), m,
+                                         LiveEdge{g.out_tgt.as<int32_t>(), g.out_deg.as<int32_t>()}, st);
+        }));
+        PR_CUDA(cudaMemcpyAsync(&live_m, dcount.ptr, 8, cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+        if (live_m)
+            k_gather_i32<<<gs_grid(ctx, live_m), 256, 0, st>>>(g.out_tgt.as<int32_t>(), eids.as<int64_t>(), live_m,
+                                                               g.live_tgt.as<int32_t>());
+    }
+    // dangling ids (ascending) and their source CSR (graph.py:363-367)
+    int64_t nd = 0;
+    PR_TRY(ensure(g.dang_ids, 4 * n));
+    auto vfirst = thrust::make_counting_iterator<int32_t>(0);
+    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceSelect::If(t, b, vfirst, g.dang_ids.as<int32_t>(), dcount.as<int64_t>(), (int)n,
+                                     IsDangling{g.out_deg.as<int32_t>()}, st);
+    }));
+    PR_CUDA(cudaMemcpyAsync(&nd, dcount.ptr, 8, cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaStreamSynchronize(st));
+    PR_TRY(ensure(g.src_off, 8 * (nd + 1)));
+    DevBuf cnt;
+    PR_TRY(ensure(cnt, 8 * (nd + 1)));
+    PR_CUDA(cudaMemsetAsync(cnt.ptr, 0, 8 * (nd + 1), st));
+    if (nd)
+        k_gather_count<<<gs_grid(ctx, nd), 256, 0, st>>>(g.dang_ids.as<int32_t>(), nd, g.in_off.as<int64_t>(),
+                                                         cnt.as<int64_t>());
+    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, cnt.as<int64_t>(), g.src_off.as<int64_t>(), (int)(nd + 1), st);
+    }));
+    int64_t md = 0;
+    PR_CUDA(cudaMemcpyAsync(&md, g.src_off.as<int64_t>() + nd, 8, cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaStreamSynchronize(st));
+    PR_TRY(ensure(g.src_ids, 4 * (md ? md : 1)));
+    if (md)
+        k_gather_rows<<<gs_grid(ctx, nd * 32), 256, 0, st>>>(g.dang_ids.as<int32_t>(), nd, g.in_off.as<int64_t>(),
+                                                             g.in_src.as<int32_t>(), g.src_off.as<int64_t>(),
+                                                             g.src_ids.as<int32_t>());
+    PR_CUDA(cudaStreamSynchronize(st));
+    PR_CUDA(cudaGetLastError());
+    g.ifp2.live_edges = live_m;
+    g.ifp2.dangling = nd;
+    g.ifp2.source_edges = md;
+    g.has_ifp2 = true;
+    return PR_OK;
+}
+
+int count_dangling(Graph &g) {
+    if (g.n_dangling >= 0) return PR_OK;
+    Ctx &ctx = *g.ctx;
+    DevBuf tmp, dcount;
+    PR_TRY(ensure(tmp, 4 * g.n));
+    PR_TRY(ensure(dcount, 8));
+    auto first = thrust::make_counting_iterator<int32_t>(0);
+    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceSelect::If(t, b, first, tmp.as<int32_t>(), dcount.as<int64_t>(), (int)g.n,
+                                     IsDangling{g.out_deg.as<int32_t>()}, ctx.stream);
+    }));
+    int64_t c = 0;
+    PR_CUDA(cudaMemcpyAsync(&c, dcount.ptr, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    PR_CUDA(cudaStreamSynchronize(ctx.stream));
+    g.n_dangling = c;
+    return PR_OK;
+}
+
+// ---------------------------------------------------------------- pull schedules
+
+// in-degree bins: 0: <= 4 (thread per vertex), 1: <= 64 (8 lanes), 2: <= 2048 (warp), 3: CTA
+__host__ __device__ inline int pull_bin(int64_t d) { return d <= 4 ? 0 : d <= 64 ? 1 : d <= 2048 ? 2 : 3; }
+
+struct InBin {
+    const int64_t *in_off;
+    const int32_t *out_deg;
+    int which, bin;
+    __host__ __device__ bool operator()(int32_t v) const {
+        int64_t d = in_off[v + 1] - in_off[v];
+        bool member = which == 2 ? true : (d > 0 && (which == 0 || out_deg[v] > 0));
+        return member && pull_bin(d) == bin;
+    }
+};
+struct IsSeed {
+    const int64_t *in_off;
+    const int32_t *out_deg;
+    __host__ __device__ bool operator()(int32_t v) const { return in_off[v + 1] == in_off[v] && out_deg[v] > 0; }
+};
+
+int ensure_sched(Graph &g, int which) {
+    auto &S = g.sched[which];
+    if (S.built) return PR_OK;
+    Ctx &ctx = *g.ctx;
+    cudaStream_t st = ctx.stream;
+    int64_t n = g.n;
+    DevBuf dcount;
+    PR_TRY(ensure(dcount, 8));
+    PR_TRY(ensure(S.ids, 4 * n));
+    auto first = thrust::make_counting_iterator<int32_t>(0);
+    int64_t total = 0;
+    static const int per_block[4] = {256, 32, 8, 1};
+    for (int k = 0; k < 4; ++k) {
+        S.bin_start[k] = total;
+        int32_t *dst = S.ids.as<int32_t>() + total;
+        PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceSelect::If(t, b, first, dst, dcount.as<int64_t>(), (int)n,
+                                         InBin{g.in_off.as<int64_t>(), g.out_deg.as<int32_t>(), which, k}, st);
+        }));
+        int64_t c = 0;
+        PR_CUDA(cudaMemcpyAsync(&c, dcount.ptr, 8, cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+        S.blocks[k] = (c + per_block[k] - 1) / per_block[k];
+        total += c;
+    }
+    S.bin_start[4] = total;
+    S.count = total;
+    PR_TRY(ensure(S.seed_ids, 4 * n));
+    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceSelect::If(t, b, first, S.seed_ids.as<int32_t>(), dcount.as<int64_t>(), (int)n,
+                                     IsSeed{g.in_off.as<int64_t>(), g.out_deg.as<int32_t>()}, st);
+    }));
+    PR_CUDA(cudaMemcpyAsync(&S.n_seed, dcount.ptr, 8, cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaStreamSynchronize(st));
+    // edges covered by D rows (for the roofline byte count)
+    S.edges = 0;
+    S.built = true;
+    return PR_OK;
+}
+
+// ---------------------------------------------------------------- R-MAT sampler
+
+__host__ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+// identical integer arithmetic to synthetic.rmat_edges
+__global__ void k_rmat(int scale, unsigned long long key0, unsigned long long ta, unsigned long long tb,
+                       unsigned long long tc, int64_t first, int64_t count, int64_t *__restrict__ src,
+                       int64_t *__restrict__ dst) {
+    const unsigned long long G = 0x9E3779B97F4A7C15ull;
+    GRID_STRIDE(i, count) {
+        unsigned long long base = key0 + (unsigned long long)(first + i) * 64ull * G;
+        unsigned long long s = 0, d = 0;
+        for (int l = 0; l < scale; ++l) {
+            unsigned long long u = mix64(base + (unsigned long long)l * G) >> 32;
+            unsigned long long sb = u >= tb;
+            unsigned long long db = (u >= ta && u < tb) || u >= tc;
+            s = (s << 1) | sb;
+            d = (d << 1) | db;
+        }
+        src[i] = (int64_t)s;
+        dst[i] = (int64_t)d;
+    }
+}
+
+int rmat_generate(Ctx &ctx, int scale, double a, double b, double c, uint64_t seed, int64_t first, int64_t count,
+                  int64_t *d_src, int64_t *d_dst) {
+    if (scale < 1 || scale > 30) return fail(PR_ERR_ARG, "rmat scale must be in [1, 30]");
+    const double S = 4294967296.0;
+    unsigned long long ta = (unsigned long long)(a * S), tb = (unsigned long long)((a + b) * S),
+                       tc = (unsigned long long)((a + b + c) * S);
+    unsigned long long key0 = mix64((unsigned long long)seed);
+    if (count > 0)
+        k_rmat<<<gs_grid(ctx, count), 256, 0, ctx.stream>>>(scale, key0, ta, tb, tc, first, count, d_src, d_dst);
+    PR_CUDA(cudaGetLastError());
+    return PR_OK;
+}
+
+struct NotLoop {
+    const int64_t *s, *d;
+    __host__ __device__ bool operator()(int64_t i) const { return s[i] != d[i]; }
+};
+
+int graph_rmat(Ctx &ctx, int scale, int64_t ef, double a, double b, double c, uint64_t seed, Graph **out) {
+    if (scale < 1 || scale > 30) return fail(PR_ERR_ARG, "rmat scale must be in [1, 30]");
+    int64_t n = 1ll << scale, count = ef * n;
+    DevBuf src, dst, keep, cnt, s2, d2;
+    PR_TRY(ensure(src, 8 * count));
+    PR_TRY(ensure(dst, 8 * count));
+    PR_TRY(rmat_generate(ctx, scale, a, b, c, seed, 0, count, src.as<int64_t>(), dst.as<int64_t>()));
+    // drop self-loops (BASELINE configs: "duplicates and self-loops removed")
+    PR_TRY(ensure(keep, 8 * count));
+    PR_TRY(ensure(cnt, 8));
+    auto first = thrust::make_counting_iterator<int64_t>(0);
+    PR_TRY(cub_run(ctx, [&](void *t, size_t &bb) {
+        return cub::DeviceSelect::If(t, bb, first, keep.as<int64_t>(), cnt.as<int64_t>(), count,
+                                     NotLoop{src.as<int64_t>(), dst.as<int64_t>()}, ctx.stream);
+    }));
+    int64_t kept = 0;
+    PR_CUDA(cudaMemcpyAsync(&kept, cnt.ptr, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    PR_CUDA(cudaStreamSynchronize(ctx.stream));
+    PR_TRY(ensure(s2, 8 * kept));
+    PR_TRY(ensure(d2, 8 * kept));
+    k_gather_i64_pair<<<gs_grid(ctx, kept), 256, 0, ctx.stream>>>(src.as<int64_t>(), dst.as<int64_t>(),
+                                                                  keep.as<int64_t>(), kept, s2.as<int64_t>(),
+                                                                  d2.as<int64_t>());
+    PR_CUDA(cudaStreamSynchronize(ctx.stream));
+    src.release();
+    dst.release();
+    keep.release();
+    return build_from_device_edges(ctx, n, s2.as<int64_t>(), d2.as<int64_t>(), kept, out);
+}
+
+// ---------------------------------------------------------------- upload / export
+
+int upload_graph(Ctx &ctx, int64_t n, int64_t m, const int64_t *out_off, const int64_t *out_tgt,
+                 const int64_t *in_off, const int64_t *in_src, Graph **out) {
+    if (n < 1) return fail(PR_ERR_ARG, "graph must have at least one vertex");
+    if (n > INT32_MAX - 1) return fail(PR_ERR_ARG, "n exceeds the int32 column-index range");
+    if (out_off[0] != 0 || out_off[n] != m || in_off[0] != 0 || in_off[n] != m)
+        return fail(PR_ERR_ARG, "offsets inconsistent with n/m");
+    cudaStream_t st = ctx.stream;
+    Graph *g = new Graph();
+    g->ctx = &ctx;
+    g->n = n;
+    g->m = m;
+    g->raw = m;
+    int rc = alloc_graph_arrays(*g);
+    DevBuf stage;
+    if (!rc) rc = ensure(stage, 8 * (m > 0 ? m : 1));
+    if (!rc) {
+        cudaError_t e = cudaMemcpyAsync(g->out_off.ptr, out_off, 8 * (n + 1), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(g->in_off.ptr, in_off, 8 * (n + 1), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess && m) {
+            e = cudaMemcpyAsync(stage.ptr, out_tgt, 8 * m, cudaMemcpyHostToDevice, st);
+            k_narrow<<<gs_grid(ctx, m), 256, 0, st>>>(stage.as<int64_t>(), m, g->out_tgt.as<int32_t>());
+            if (e == cudaSuccess) e = cudaMemcpyAsync(stage.ptr, in_src, 8 * m, cudaMemcpyHostToDevice, st);
+            k_narrow<<<gs_grid(ctx, m), 256, 0, st>>>(stage.as<int64_t>(), m, g->in_src.as<int32_t>());
+        }
+        k_degree<<<gs_grid(ctx, n), 256, 0, st>>>(g->out_off.as<int64_t>(), n, g->out_deg.as<int32_t>());
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e == cudaSuccess) e = cudaGetLastError();
+        if (e != cudaSuccess) rc = fail(PR_ERR_CUDA, std::string("graph upload: ") + cudaGetErrorString(e));
+    }
+    if (rc) { delete g; return rc; }
+    *out = g;
+    return PR_OK;
+}
+
+int export_graph(Graph &g, int64_t *out_off, int64_t *out_tgt, int64_t *in_off, int64_t *in_src) {
+    Ctx &ctx = *g.ctx;
+    cudaStream_t st = ctx.stream;
+    DevBuf wide;
+    PR_TRY(ensure(wide, 8 * (g.m ? g.m : 1)));
+    if (out_off) PR_CUDA(cudaMemcpyAsync(out_off, g.out_off.ptr, 8 * (g.n + 1), cudaMemcpyDeviceToHost, st));
+    if (in_off) PR_CUDA(cudaMemcpyAsync(in_off, g.in_off.ptr, 8 * (g.n + 1), cudaMemcpyDeviceToHost, st));
+    if (out_tgt && g.m) {
+        k_widen<<<gs_grid(ctx, g.m), 256, 0, st>>>(g.out_tgt.as<int32_t>(), g.m, wide.as<int64_t>());
+        PR_CUDA(cudaMemcpyAsync(out_tgt, wide.ptr, 8 * g.m, cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+    }
+    if (in_src && g.m) {
+        k_widen<<<gs_grid(ctx, g.m), 256, 0, st>>>(g.in_src.as<int32_t>(), g.m, wide.as<int64_t>());
+        PR_CUDA(cudaMemcpyAsync(in_src, wide.ptr, 8 * g.m, cudaMemcpyDeviceToHost, st));
+    }
+    PR_CUDA(cudaStreamSynchronize(st));
+    return PR_OK;
+}
+
+int export_i32(Ctx &ctx, const DevBuf &src, int64_t count, int64_t *host) {
+    if (!host || count <= 0) return PR_OK;
+    DevBuf wide;
+    PR_TRY(ensure(wide, 8 * count));
+    k_widen<<<gs_grid(ctx, count), 256, 0, ctx.stream>>>(src.as<int32_t>(), count, wide.as<int64_t>());
+    PR_CUDA(cudaMemcpyAsync(host, wide.ptr, 8 * count, cudaMemcpyDeviceToHost, ctx.stream));
+    PR_CUDA(cudaStreamSynchronize(ctx.stream));
+    return PR_OK;
+}
+
+int export_i64(Ctx &ctx, const DevBuf &src, int64_t count, int64_t *host) {
+    if (!host || count <= 0) return PR_OK;
+    PR_CUDA(cudaMemcpyAsync(host, src.ptr, 8 * count, cudaMemcpyDeviceToHost, ctx.stream));
+    PR_CUDA(cudaStreamSynchronize(ctx.stream));
+    return PR_OK;
+}
+
+}  // namespace pr

@@ -1,0 +1,153 @@
+// internal.cuh -- shared definitions of libpushrank_cuda (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/pushrank_cuda.h"
+
+namespace pr {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+
+#define PR_CUDA(call)                                                                      \
+    do {                                                                                   \
+        cudaError_t _e = (call);                                                           \
+        if (_e != cudaSuccess)                                                             \
+            return ::pr::fail(PR_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e) + \
+                                               " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"); \
+    } while (0)
+
+#define PR_TRY(call)                   \
+    do {                               \
+        int _rc = (call);              \
+        if (_rc != PR_OK) return _rc;  \
+    } while (0)
+
+// ---------------------------------------------------------------- device buffers
+struct DevBuf {
+    void *ptr = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+    template <class T> T *as() const { return reinterpret_cast<T *>(ptr); }
+};
+// grows (never shrinks) a buffer; contents are not preserved
+int ensure(DevBuf &b, size_t bytes);
+
+struct Ctx {
+    int device = 0;
+    int sm_count = 148;
+    size_t l2_bytes = 0;
+    cudaStream_t stream = nullptr;
+    DevBuf scratch;          // CUB temporaries
+    DevBuf flush;            // L2 flush buffer (bench)
+};
+
+// Device-side control block of a round loop (one per run workspace).
+struct RunCtl {
+    int64_t round;            // index t of the state being drained next
+    int64_t rows;             // rows produced
+    int64_t push_ops, push_ops_dangling;
+    int64_t pull_rounds, push_rounds;
+    int64_t fsize[2];         // frontier sizes (ping-pong by round parity)
+    int32_t mode;             // 0 pull, 1 push (for the next round)
+    int32_t done;             // 1 = converged, 2 = max_rounds exhausted
+    uint32_t blocks_done;     // last-block arrival counter
+    uint32_t pad;
+    uint64_t t0_ns;           // globaltimer at prologue
+    double bytes;             // algorithmic bytes accumulated
+    // constant contributions of vertices outside the round set (rows >= 1)
+    double c_l1, c_above, c_nd_above;
+    int64_t c_conv_all, c_conv_scan;
+    double mass_total;
+    int64_t settled;
+};
+
+// Per-block partial statistics of one round (reduced in fixed order).
+struct Partial {
+    double l1, above, nd_above;
+    int64_t conv_all, conv_scan, nact, work, push_ops, push_dang;
+    uint64_t digest;
+};
+
+struct Graph {
+    Ctx *ctx = nullptr;
+    int64_t n = 0, m = 0, raw = 0;
+    DevBuf out_off;   // int64 [n+1]
+    DevBuf out_tgt;   // int32 [m]
+    DevBuf out_deg;   // int32 [n]
+    DevBuf in_off;    // int64 [n+1]
+    DevBuf in_src;    // int32 [m]
+    // classification (pr_classify)
+    bool classified = false;
+    pr_class_counts counts{};
+    DevBuf cls_flags;  // uint8 [n]: bit0 dangling, bit1 unreferenced, bit2 weak d, bit3 weak u
+    // dangling target counts (IFP1 push_ops_dangling), int32 [n]
+    bool has_dtc = false;
+    DevBuf dtc;
+    // IFP2 split (pr_preprocess_ifp2)
+    bool has_ifp2 = false;
+    pr_ifp2_counts ifp2{};
+    DevBuf live_off, live_tgt, live_deg;     // int64 [n+1], int32 [live_m], int32 [n]
+    DevBuf dang_ids, src_off, src_ids;       // int32 [n_d], int64 [n_d+1], int32 [m_d]
+    // pull schedules, built lazily: [0] ifp1/fp-full destinations, [1] ifp2, [2] power (all)
+    struct Sched {
+        bool built = false;
+        int64_t count = 0;        // |D|
+        int64_t bin_start[5] = {0, 0, 0, 0, 0};   // bin k = ids[bin_start[k] .. bin_start[k+1])
+        int64_t blocks[4] = {0, 0, 0, 0};
+        int64_t edges = 0;        // edges of D rows
+        DevBuf ids;               // int32 [|D|], bins concatenated, ascending id within a bin
+        int64_t n_seed = 0;       // vertices outside D that are active at round 0 (scatter seeds)
+        DevBuf seed_ids;          // int32
+    } sched[3];
+    // run workspace
+    DevBuf h, reserved, s2, act, in_d, frontier2, partials, ctl, rows;
+    int64_t rows_cap = 0;
+    int64_t max_blocks = 0;     // partial slots per region (partials holds 3 regions)
+    int64_t n_dangling = -1;    // #(out_degree == 0), computed lazily
+    DevBuf pw;                // power-method workspace
+    // cached instantiated round-loop graphs, keyed by run parameters
+    struct Cached {
+        bool valid = false;
+        pr_run_params key{};
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+    } cached[4];
+    ~Graph();
+};
+
+int ensure_dtc(Graph &g);
+int count_dangling(Graph &g);
+void invalidate_cache(Graph &g);
+int ensure_sched(Graph &g, int which);
+int build_from_device_edges(Ctx &ctx, int64_t n, const int64_t *d_src, const int64_t *d_dst,
+                            int64_t m_raw, Graph **out);
+int classify_device(Graph &g);
+int preprocess_ifp2_device(Graph &g);
+int run_rounds(Graph &g, const pr_run_params &p, double *d_values, pr_round_stats *rows,
+               int64_t row_cap, pr_run_result *res);
+int power_device(Graph &g, double damping, int64_t iterations, double tolerance, double threshold,
+                 const double *h_personalization, double *h_pi, double *h_deltas, int64_t *h_converged,
+                 int (*on_iterate)(void *, int64_t, const double *), void *user, pr_run_result *res);
+
+// small helpers
+inline unsigned grid_for(int64_t items, int per_block) {
+    int64_t b = (items + per_block - 1) / per_block;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+}  // namespace pr

@@ -1,0 +1,332 @@
+// power.cu -- K8: the Power-method baseline (solvers.py:186-243) on the
+// same degree-binned CSC gather as the dense push round.
+//
+// Per iteration (solvers.py:217-235):
+//   z_u   = (c * pi_u) * inv_deg_u            (solvers.py:173, inv_deg = 1/deg or 0)
+//   y_v   = sum_{u in in(v)} z_u               (_WalkMultiplier, in-adjacency order)
+//   nxt_v = y_v + restart * p_v,  restart = c * sum_{dangling} pi + (1 - c)
+//   pi'   = nxt / sum(nxt);  delta = ||pi' - pi||_1
+// Two launches per iteration: gather (+ sum of nxt) and normalise (+ delta,
+// converged count, next z, next dangling sum); both end with a
+// deterministic last-block reduction that also drives the graph's WHILE node.
+#include <cstring>
+#include <vector>
+
+#include "internal.cuh"
+#include "reduce.cuh"
+
+namespace pr {
+
+struct PowCtl {
+    int64_t k;               // iteration index
+    uint32_t blocks_done;
+    int32_t done;
+    double total;            // sum(nxt) of the current iteration
+    double restart;          // restart coefficient for the current iteration
+    double delta;
+};
+
+struct PowArgs {
+    int64_t n;
+    const int64_t *in_off;
+    const int32_t *in_src;
+    const int32_t *deg;
+    const int32_t *ids;
+    int64_t bin_start[5], blk_start[5];
+    const double *p;         // personalization (null: uniform 1/n)
+    double *pi, *nxt, *z;
+    double *deltas;          // device [iterations]
+    int64_t *conv;           // device [iterations]
+    Partial *partials;
+    PowCtl *ctl;
+    double c, tolerance, threshold, uniform_p;
+    int64_t iterations;
+    int32_t use_graph;
+    cudaGraphConditionalHandle h_loop;
+};
+
+__device__ __forceinline__ double pval(const PowArgs &A, int64_t v) { return A.p ? A.p[v] : A.uniform_p; }
+
+__device__ __forceinline__ double z_of(const PowArgs &A, int64_t v, double x) {
+    int32_t d = A.deg[v];
+    double inv = d > 0 ? __ddiv_rn(1.0, (double)d) : 0.0;
+    return __dmul_rn(__dmul_rn(A.c, x), inv);
+}
+
+// last-block protocol over Partial.l1 (sum) / .above (second sum) / .conv_all
+template <class Fin>
+__device__ void pow_finish(const PowArgs &A, Partial p, Fin fin) {
+    __shared__ bool is_last;
+    block_reduce(p);
+    if (threadIdx.x == 0) {
+        A.partials[blockIdx.x] = p;
+        __threadfence();
+        unsigned t = atomicAdd(&A.ctl->blocks_done, 1u);
+        is_last = t == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    Partial acc;
+    zero(acc);
+    for (int64_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) add(acc, load_partial(A.partials + b));
+    block_reduce(acc);
+    if (threadIdx.x == 0) {
+        A.ctl->blocks_done = 0;
+        fin(acc);
+    }
+}
+
+// pi = p; z = (c p) inv_deg; restart from the dangling mass of p
+__global__ void __launch_bounds__(256) k_pw_init(PowArgs A) {
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    Partial p;
+    zero(p);
+    if (v < A.n) {
+        double x = pval(A, v);
+        A.pi[v] = x;
+        A.z[v] = z_of(A, v, x);
+        if (A.deg[v] == 0) p.l1 = x;
+    }
+    pow_finish(A, p, [&](const Partial &acc) {
+        A.ctl->k = 0;
+        A.ctl->done = A.iterations <= 0;
+        A.ctl->restart = __dadd_rn(__dmul_rn(A.c, acc.l1), 1.0 - A.c);  // solvers.py:219
+        if (A.use_graph) cudaGraphSetConditional(A.h_loop, A.ctl->done ? 0u : 1u);
+    });
+}
+
+// nxt_v = sum z over in-edges + restart * p_v; block partial of sum(nxt)
+__global__ void __launch_bounds__(256) k_pw_gather(PowArgs A) {
+    __shared__ double red[8];
+    const double *__restrict__ z = A.z;
+    double restart = A.ctl->restart;
+    Partial p;
+    zero(p);
+    int64_t b = blockIdx.x;
+    int tid = threadIdx.x;
+    if (b < A.blk_start[1]) {
+        int64_t idx = A.bin_start[0] + b * 256 + tid;
+        if (idx < A.bin_start[1]) {
+            int32_t v = A.ids[idx];
+            double acc = 0.0;
+            for (int64_t e = A.in_off[v]; e < A.in_off[v + 1]; ++e) acc += __ldg(&z[A.in_src[e]]);
+            double x = __dadd_rn(acc, __dmul_rn(restart, pval(A, v)));
+            A.nxt[v] = x;
+            p.l1 += x;
+        }
+    } else if (b < A.blk_start[2]) {
+        int g = tid >> 3, l = tid & 7;
+        int64_t idx = A.bin_start[1] + (b - A.blk_start[1]) * 32 + g;
+        bool ok = idx < A.bin_start[2];
+        int32_t v = ok ? A.ids[idx] : 0;
+        double acc = 0.0;
+        if (ok)
+            for (int64_t e = A.in_off[v] + l; e < A.in_off[v + 1]; e += 8) acc += __ldg(&z[A.in_src[e]]);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        if (ok && l == 0) {
+            double x = __dadd_rn(acc, __dmul_rn(restart, pval(A, v)));
+            A.nxt[v] = x;
+            p.l1 += x;
+        }
+    } else if (b < A.blk_start[3]) {
+        int w = tid >> 5, l = tid & 31;
+        int64_t idx = A.bin_start[2] + (b - A.blk_start[2]) * 8 + w;
+        bool ok = idx < A.bin_start[3];
+        int32_t v = ok ? A.ids[idx] : 0;
+        double acc = 0.0;
+        if (ok)
+            for (int64_t e = A.in_off[v] + l; e < A.in_off[v + 1]; e += 32) acc += __ldg(&z[A.in_src[e]]);
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (ok && l == 0) {
+            double x = __dadd_rn(acc, __dmul_rn(restart, pval(A, v)));
+            A.nxt[v] = x;
+            p.l1 += x;
+        }
+    } else if (b < A.blk_start[4]) {
+        int64_t idx = A.bin_start[3] + (b - A.blk_start[3]);
+        int32_t v = A.ids[idx];
+        double acc = 0.0;
+        for (int64_t e = A.in_off[v] + tid; e < A.in_off[v + 1]; e += 256) acc += __ldg(&z[A.in_src[e]]);
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if ((tid & 31) == 0) red[tid >> 5] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            double tot = 0.0;
+            for (int k = 0; k < 8; ++k) tot += red[k];
+            double x = __dadd_rn(tot, __dmul_rn(restart, pval(A, v)));
+            A.nxt[v] = x;
+            p.l1 += x;
+        }
+    }
+    pow_finish(A, p, [&](const Partial &acc) { A.ctl->total = acc.l1; });
+}
+
+// pi' = nxt / total; delta, converged count; next z and dangling sum
+__global__ void __launch_bounds__(256) k_pw_norm(PowArgs A) {
+    double total = A.ctl->total;
+    Partial p;
+    zero(p);
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v < A.n) {
+        double x = __ddiv_rn(A.nxt[v], total);
+        double d = fabs(x - A.pi[v]);
+        p.l1 = d;                                       // delta (solvers.py:222)
+        p.conv_all = d <= A.threshold ? 1 : 0;          // solvers.py:227
+        A.pi[v] = x;
+        A.z[v] = z_of(A, v, x);
+        if (A.deg[v] == 0) p.above = x;                 // dangling mass for the next restart
+    }
+    pow_finish(A, p, [&](const Partial &acc) {
+        PowCtl *c = A.ctl;
+        int64_t k = c->k;
+        A.deltas[k] = acc.l1;
+        A.conv[k] = acc.conv_all;
+        c->delta = acc.l1;
+        c->restart = __dadd_rn(__dmul_rn(A.c, acc.above), 1.0 - A.c);
+        c->k = k + 1;
+        bool stop = (k + 1 >= A.iterations) || (A.tolerance > 0.0 && acc.l1 < A.tolerance);
+        c->done = stop;
+        if (A.use_graph) cudaGraphSetConditional(A.h_loop, stop ? 0u : 1u);
+    });
+}
+
+static int add_node(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t *deps, size_t nd, void *f,
+                    unsigned grid, void **args) {
+    cudaKernelNodeParams kp;
+    memset(&kp, 0, sizeof(kp));
+    kp.func = f;
+    kp.gridDim = dim3(grid);
+    kp.blockDim = dim3(256);
+    kp.kernelParams = args;
+    PR_CUDA(cudaGraphAddKernelNode(node, g, deps, nd, &kp));
+    return PR_OK;
+}
+
+int power_device(Graph &g, double damping, int64_t iterations, double tolerance, double threshold,
+                 const double *h_p, double *h_pi, double *h_deltas, int64_t *h_conv,
+                 int (*on_iterate)(void *, int64_t, const double *), void *user, pr_run_result *res) {
+    if (!(damping > 0.0 && damping < 1.0)) return fail(PR_ERR_ARG, "damping must be in (0,1)");
+    if (iterations < 0) return fail(PR_ERR_ARG, "max_iterations must be non-negative");
+    Ctx &ctx = *g.ctx;
+    cudaStream_t st = ctx.stream;
+    PR_TRY(ensure_sched(g, 2));
+    auto &S = g.sched[2];
+    int64_t n = g.n;
+    int64_t blk = 0;
+    PowArgs A;
+    memset(&A, 0, sizeof(A));
+    for (int k = 0; k < 4; ++k) {
+        A.bin_start[k] = S.bin_start[k];
+        A.blk_start[k] = blk;
+        blk += S.blocks[k];
+    }
+    A.bin_start[4] = S.bin_start[4];
+    A.blk_start[4] = blk;
+    int64_t maxb = blk > (n + 255) / 256 ? blk : (n + 255) / 256;
+    int64_t it_cap = iterations > 0 ? iterations : 1;
+    // workspace: pi, nxt, z, p (opt), deltas, conv, partials, ctl
+    size_t off_pi = 0, off_nxt = off_pi + 8 * n, off_z = off_nxt + 8 * n, off_p = off_z + 8 * n;
+    size_t off_d = off_p + (h_p ? 8 * n : 0), off_c = off_d + 8 * it_cap, off_part = off_c + 8 * it_cap;
+    size_t off_ctl = off_part + sizeof(Partial) * (maxb + 8);
+    size_t total = off_ctl + sizeof(PowCtl) + 64;
+    PR_TRY(ensure(g.pw, total));
+    char *base = g.pw.as<char>();
+    A.n = n;
+    A.in_off = g.in_off.as<int64_t>();
+    A.in_src = g.in_src.as<int32_t>();
+    A.deg = g.out_deg.as<int32_t>();
+    A.ids = S.ids.as<int32_t>();
+    A.pi = (double *)(base + off_pi);
+    A.nxt = (double *)(base + off_nxt);
+    A.z = (double *)(base + off_z);
+    A.p = h_p ? (const double *)(base + off_p) : nullptr;
+    A.deltas = (double *)(base + off_d);
+    A.conv = (int64_t *)(base + off_c);
+    A.partials = (Partial *)(base + off_part);
+    A.ctl = (PowCtl *)(base + off_ctl);
+    A.c = damping;
+    A.tolerance = tolerance;
+    A.threshold = threshold;
+    A.uniform_p = 1.0 / (double)n;
+    A.iterations = iterations;
+    if (h_p) PR_CUDA(cudaMemcpyAsync((void *)A.p, h_p, 8 * n, cudaMemcpyHostToDevice, st));
+    PR_CUDA(cudaMemsetAsync(A.ctl, 0, sizeof(PowCtl), st));
+    unsigned g_all = grid_for(n, 256), g_gather = (unsigned)(blk > 0 ? blk : 1);
+
+    cudaEvent_t e0, e1;
+    PR_CUDA(cudaEventCreate(&e0));
+    PR_CUDA(cudaEventCreate(&e1));
+    if (on_iterate) {
+        // host-driven iterations with a host copy of every iterate (solvers.py:232-233)
+        A.use_graph = 0;
+        std::vector<double> host_pi((size_t)n);
+        PR_CUDA(cudaEventRecord(e0, st));
+        k_pw_init<<<g_all, 256, 0, st>>>(A);
+        for (int64_t k = 0; k < iterations; ++k) {
+            k_pw_gather<<<g_gather, 256, 0, st>>>(A);
+            k_pw_norm<<<g_all, 256, 0, st>>>(A);
+            PR_CUDA(cudaGetLastError());
+            PowCtl hc;
+            PR_CUDA(cudaMemcpyAsync(&hc, A.ctl, sizeof(hc), cudaMemcpyDeviceToHost, st));
+            PR_CUDA(cudaMemcpyAsync(host_pi.data(), A.pi, 8 * n, cudaMemcpyDeviceToHost, st));
+            PR_CUDA(cudaStreamSynchronize(st));
+            if (on_iterate(user, k, host_pi.data())) break;
+            if (hc.done) break;
+        }
+        PR_CUDA(cudaEventRecord(e1, st));
+        PR_CUDA(cudaEventSynchronize(e1));
+    } else {
+        cudaGraph_t G;
+        PR_CUDA(cudaGraphCreate(&G, 0));
+        PR_CUDA(cudaGraphConditionalHandleCreate(&A.h_loop, G, 1, cudaGraphCondAssignDefault));
+        A.use_graph = 1;
+        void *args[] = {&A};
+        cudaGraphNode_t n_init, n_while, n_a, n_b;
+        PR_TRY(add_node(G, &n_init, nullptr, 0, (void *)k_pw_init, g_all, args));
+        cudaGraphNodeParams wp = {};
+        wp.type = cudaGraphNodeTypeConditional;
+        wp.conditional.handle = A.h_loop;
+        wp.conditional.type = cudaGraphCondTypeWhile;
+        wp.conditional.size = 1;
+        PR_CUDA(cudaGraphAddNode(&n_while, G, &n_init, 1, &wp));
+        cudaGraph_t body = wp.conditional.phGraph_out[0];
+        PR_TRY(add_node(body, &n_a, nullptr, 0, (void *)k_pw_gather, g_gather, args));
+        PR_TRY(add_node(body, &n_b, &n_a, 1, (void *)k_pw_norm, g_all, args));
+        cudaGraphExec_t ex;
+        PR_CUDA(cudaGraphInstantiate(&ex, G, 0));
+        PR_CUDA(cudaEventRecord(e0, st));
+        cudaError_t le = cudaGraphLaunch(ex, st);
+        PR_CUDA(cudaEventRecord(e1, st));
+        cudaError_t se = cudaEventSynchronize(e1);
+        cudaGraphExecDestroy(ex);
+        cudaGraphDestroy(G);
+        PR_CUDA(le);
+        PR_CUDA(se);
+    }
+    float ms = 0.f;
+    PR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    PowCtl hc;
+    PR_CUDA(cudaMemcpy(&hc, A.ctl, sizeof(hc), cudaMemcpyDeviceToHost));
+    int64_t k = hc.k;
+    if (h_pi) PR_CUDA(cudaMemcpy(h_pi, A.pi, 8 * n, cudaMemcpyDeviceToHost));
+    if (h_deltas && k) PR_CUDA(cudaMemcpy(h_deltas, A.deltas, 8 * k, cudaMemcpyDeviceToHost));
+    if (h_conv && k) PR_CUDA(cudaMemcpy(h_conv, A.conv, 8 * k, cudaMemcpyDeviceToHost));
+    if (res) {
+        memset(res, 0, sizeof(*res));
+        res->rounds = k;
+        res->rows = k;
+        res->push_ops = k * g.m;
+        res->mass_total = 1.0;
+        res->push_ms = ms;
+        res->round_ms = ms;
+        res->bytes_moved = (double)k * (12.0 * (double)g.m + 32.0 * (double)n);
+    }
+    return PR_OK;
+}
+
+}  // namespace pr

@@ -1,0 +1,885 @@
+// rounds.cu -- the IFP1/IFP2 push-round hot path on sm_100a.
+//
+// Reference semantics (engines.py:349-456 for the round form, _kernels.pyx:
+// 83-104 for the drain): every scanned vertex with pending mass h > xi
+// (strict) is drained -- reserved += frac*h, h = 0 -- and pushes
+// (c*h)/deg(v) along every (live) out-edge.  IFP1 scans non-dangling
+// vertices over the full out-CSR; IFP2 scans them over the live CSR (edges
+// into dangling vertices removed, weights still 1/out_degree) and settles
+// the dangling vertices once at the end (engines.py:269-289); fp-full (sync
+// twin only) scans everything and reserves 1-c.
+//
+// Fast engine (PR_MODE_AUTO/PULL/PUSH): one launch per round.
+//   * pull round (dense): CSC gather over the destination set D (vertices
+//     that can receive mass), degree-binned thread / 8-lane / warp / CTA per
+//     destination, fixed-order group reductions (deterministic, no
+//     atomics), double-buffered shares s, the next state's drain fused into
+//     the epilogue;
+//   * push round (sparse tail): frontier scatter with red.global.add.f64,
+//     then a scan kernel over D that fuses the drain;
+//   * every round kernel ends with a last-block reduction of per-block
+//     statistics (trace row, convergence test, next-mode choice) that also
+//     drives the CUDA-graph conditional WHILE/SWITCH nodes, so the whole
+//     solve is one graph launch with no host round trips.
+// Exact engine (PR_MODE_EXACT): thread per vertex, sequential ascending
+// source sums with explicit _rn intrinsics -- bit-identical reserved/h to
+// sync_simulate's np.bincount order.
+#include <cooperative_groups.h>
+
+#include <cstring>
+#include <vector>
+
+#include "internal.cuh"
+#include "reduce.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace pr {
+
+struct RunArgs {
+    int64_t n;
+    const int64_t *in_off;
+    const int32_t *in_src;
+    const int64_t *push_off;   // out CSR (ifp1, fp-full) or live CSR (ifp2)
+    const int32_t *push_tgt;
+    const int32_t *deg;        // original out-degree: push weight denominator
+    const int32_t *row_len;    // push row length for push_ops (out_deg or live_deg)
+    const int32_t *dtc;        // dangling-target counts (ifp1/fp-full) or null (ifp2)
+    const int32_t *ids;        // D, bins concatenated
+    int64_t bin_start[5];
+    int64_t blk_start[5];
+    int64_t d_count;
+    const int32_t *seeds;      // vertices outside D active at state 0
+    int64_t n_seed;
+    const uint8_t *in_d;       // membership mask of D
+    double *h, *reserved, *s;  // s: 2*n (ping-pong by state parity)
+    int32_t *frontier;         // 2*fcap
+    int64_t fcap;
+    uint8_t *act;              // exact engine
+    Partial *partials;         // 3 regions of max_blocks: round, constants, mass totals
+    int64_t max_blocks;
+    RunCtl *ctl;
+    pr_round_stats *rows;
+    int64_t rows_cap;
+    double c, xi, frac;
+    int32_t algo, policy, conv_all, use_graph;
+    int64_t max_rounds;
+    double push_work;          // AUTO: push when the next round's work < push_work
+    double n_scan;             // scan-set size (bytes model)
+    cudaGraphConditionalHandle h_loop, h_mode;
+};
+
+__device__ __forceinline__ uint64_t digest_term(int64_t v, double r, double h) {
+    uint64_t a = (uint64_t)__double_as_longlong(r), b = (uint64_t)__double_as_longlong(h);
+    uint64_t w = ((uint64_t)v * 0x9E3779B97F4A7C15ull) | 1ull;
+    return (a ^ (b * 0xBF58476D1CE4E5B9ull)) * w;
+}
+
+// warp-aggregated frontier append among the currently converged lanes
+__device__ __forceinline__ void frontier_append(bool pred, int32_t v, int32_t *F, int64_t *size) {
+    cg::coalesced_group g = cg::coalesced_threads();
+    unsigned bal = g.ballot(pred);
+    if (!bal) return;
+    unsigned long long base = 0;
+    if (g.thread_rank() == 0) base = atomicAdd((unsigned long long *)size, (unsigned long long)__popc(bal));
+    base = g.shfl(base, 0);
+    if (pred) F[base + __popc(bal & ((1u << g.thread_rank()) - 1u))] = v;
+}
+
+// Drain one vertex of state r given its pre-drain pending mass hv:
+// statistics, reservation, shares s[r&1], frontier append.
+__device__ __forceinline__ void epilogue(const RunArgs &A, int64_t v, double hv, int64_t r, Partial &p) {
+    int32_t dv = A.deg[v];
+    bool scan = A.algo == PR_ALGO_FPFULL || dv > 0;
+    bool above = hv > A.xi;  // strict (engines.py:421, _kernels.pyx:89)
+    p.l1 += hv;
+    if (above) {
+        p.above += hv;
+        if (dv > 0) p.nd_above += hv;
+    } else {
+        p.conv_all += 1;
+        if (scan) p.conv_scan += 1;
+    }
+    bool active = above && scan;
+    double *s_out = A.s + (r & 1) * A.n;
+    if (active) {
+        // (c*h)/deg with two roundings, never c*h*inv_deg (engines.py:444, _kernels.pyx:97)
+        double share = dv > 0 ? __ddiv_rn(__dmul_rn(A.c, hv), (double)dv) : 0.0;
+        s_out[v] = share;
+        A.reserved[v] = __dadd_rn(A.reserved[v], __dmul_rn(A.frac, hv));
+        A.h[v] = 0.0;
+        p.nact += 1;
+        p.work += (int64_t)dv + 1;
+        p.push_ops += A.row_len[v];
+        if (A.dtc) p.push_dang += A.dtc[v];
+    } else {
+        s_out[v] = 0.0;
+        A.h[v] = hv;
+    }
+    frontier_append(active, (int32_t)v, A.frontier + (r & 1) * A.fcap, &A.ctl->fsize[r & 1]);
+}
+
+// Thread 0 of the last block: write trace row r, decide what runs next,
+// drive the graph conditionals.
+__device__ void finalize_row(const RunArgs &A, const Partial &tot, int64_t r, bool fast) {
+    RunCtl *ctl = A.ctl;
+    double l1 = tot.l1, above = tot.above, nd_above = tot.nd_above;
+    int64_t conv_all = tot.conv_all, conv_scan = tot.conv_scan;
+    if (fast && r >= 1) {
+        l1 += ctl->c_l1;
+        above += ctl->c_above;
+        nd_above += ctl->c_nd_above;
+        conv_all += ctl->c_conv_all;
+        conv_scan += ctl->c_conv_scan;
+    }
+    if (r < A.rows_cap) {
+        pr_round_stats row;
+        row.h_l1 = l1;
+        row.alpha = above > 0.0 ? nd_above / above : 1.0;
+        row.active_mass = above;
+        row.carry_mass = l1 - above;
+        row.converged = A.conv_all ? conv_all : conv_scan;
+        row.work = tot.work;
+        row.push_ops = ctl->push_ops;
+        row.push_ops_dangling = ctl->push_ops_dangling;
+        row.digest = tot.digest;
+        row.wall_ms = (double)(globaltimer() - ctl->t0_ns) * 1e-6;
+        A.rows[r] = row;
+    }
+    ctl->rows = r + 1;
+    ctl->push_ops += tot.push_ops;
+    ctl->push_ops_dangling += tot.push_dang;
+    // algorithmic bytes of the round that drains this state
+    if (tot.nact > 0) ctl->bytes += 12.0 * (double)tot.push_ops + 40.0 * (double)tot.nact + 8.0 * A.n_scan;
+    int done = 0;
+    if (tot.nact == 0) done = 1;
+    else if (r >= A.max_rounds) done = 2;
+    ctl->done = done;
+    ctl->round = r;
+    int mode = 0;
+    if (A.policy == PR_MODE_PUSH && r >= 1) mode = 1;
+    else if (A.policy == PR_MODE_AUTO && r >= 1 && (double)tot.work < A.push_work) mode = 1;
+    ctl->mode = mode;
+    if (!done) {
+        if (mode) ctl->push_rounds += 1;
+        else ctl->pull_rounds += 1;
+    }
+    ctl->fsize[(r + 1) & 1] = 0;
+    ctl->blocks_done = 0;
+    __threadfence();
+    if (A.use_graph) {
+        cudaGraphSetConditional(A.h_loop, done ? 0u : 1u);
+        cudaGraphSetConditional(A.h_mode, (unsigned)mode);
+    }
+}
+
+// Publish this block's partial; the last block to arrive reduces all of
+// them in a fixed order (deterministic) and finalises row r.
+__device__ void finish_round(const RunArgs &A, Partial p, int64_t r, bool fast, bool with_consts, Partial cst) {
+    __shared__ bool is_last;
+    block_reduce(p);
+    if (with_consts) block_reduce(cst);
+    if (threadIdx.x == 0) {
+        A.partials[blockIdx.x] = p;
+        if (with_consts) A.partials[A.max_blocks + blockIdx.x] = cst;
+        __threadfence();
+        unsigned ticket = atomicAdd(&A.ctl->blocks_done, 1u);
+        is_last = ticket == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    Partial acc, cacc;
+    zero(acc);
+    zero(cacc);
+    for (int64_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+        add(acc, load_partial(A.partials + b));
+        if (with_consts) add(cacc, load_partial(A.partials + A.max_blocks + b));
+    }
+    block_reduce(acc);
+    if (with_consts) block_reduce(cacc);
+    if (threadIdx.x == 0) {
+        if (with_consts) {
+            A.ctl->c_l1 = cacc.l1;
+            A.ctl->c_above = cacc.above;
+            A.ctl->c_nd_above = cacc.nd_above;
+            A.ctl->c_conv_all = cacc.conv_all;
+            A.ctl->c_conv_scan = cacc.conv_scan;
+        }
+        finalize_row(A, acc, r, fast);
+    }
+}
+
+// ---------------------------------------------------------------- fast engine kernels
+
+__global__ void k_reset(RunArgs A) {
+    RunCtl *c = A.ctl;
+    c->round = 0;
+    c->rows = 0;
+    c->push_ops = c->push_ops_dangling = 0;
+    c->pull_rounds = c->push_rounds = 0;
+    c->fsize[0] = c->fsize[1] = 0;
+    c->mode = 0;
+    c->done = 0;
+    c->blocks_done = 0;
+    c->t0_ns = globaltimer();
+    c->bytes = 0.0;
+    c->c_l1 = c->c_above = c->c_nd_above = 0.0;
+    c->c_conv_all = c->c_conv_scan = 0;
+    c->mass_total = 0.0;
+    c->settled = 0;
+}
+
+// State 0 (h = 1 everywhere, MassState.fresh engines.py:51-54): trace row 0
+// and its drain.  Vertices in D go through the common epilogue; vertices
+// outside D never receive mass, so their post-drain value is constant for
+// every later row (recorded as constants) and their round-0 shares are
+// scattered once by k_seed_scatter.
+__global__ void __launch_bounds__(256) k_init(RunArgs A) {
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    Partial p, cst;
+    zero(p);
+    zero(cst);
+    if (v < A.n) {
+        A.reserved[v] = 0.0;
+        A.s[A.n + v] = 0.0;
+        if (A.in_d[v]) {
+            epilogue(A, v, 1.0, 0, p);
+        } else {
+            int32_t dv = A.deg[v];
+            bool scan = A.algo == PR_ALGO_FPFULL || dv > 0;
+            bool above = 1.0 > A.xi;
+            p.l1 += 1.0;
+            if (above) {
+                p.above += 1.0;
+                if (dv > 0) p.nd_above += 1.0;
+            } else {
+                p.conv_all += 1;
+                if (scan) p.conv_scan += 1;
+            }
+            bool active = above && scan;
+            double after = active ? 0.0 : 1.0;
+            if (active) {
+                A.reserved[v] = A.frac;
+                p.nact += 1;
+                p.work += (int64_t)dv + 1;
+                p.push_ops += A.row_len[v];
+                if (A.dtc) p.push_dang += A.dtc[v];
+            }
+            A.h[v] = after;
+            A.s[v] = 0.0;
+            cst.l1 += after;
+            if (after > A.xi) {
+                cst.above += after;
+                if (dv > 0) cst.nd_above += after;
+            } else {
+                cst.conv_all += 1;
+                if (scan) cst.conv_scan += 1;
+            }
+        }
+    }
+    finish_round(A, p, 0, true, true, cst);
+}
+
+// round-0 shares of active vertices outside D (in-degree 0): scatter once
+__global__ void __launch_bounds__(256) k_seed_scatter(RunArgs A) {
+    if (!(1.0 > A.xi)) return;
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < A.n_seed; i += nwarps) {
+        int32_t u = A.seeds[i];
+        int32_t du = A.deg[u];
+        if (du <= 0) continue;
+        double share = __ddiv_rn(__dmul_rn(A.c, 1.0), (double)du);
+        for (int64_t e = A.push_off[u] + lane; e < A.push_off[u + 1]; e += 32) atomicAdd(&A.h[A.push_tgt[e]], share);
+    }
+}
+
+// Dense round t: h(t+1)_v = h_drained(t)_v + sum_{u in in(v)} s(t)_u over D,
+// fused with the drain of state t+1.
+__global__ void __launch_bounds__(256) k_pull(RunArgs A) {
+    __shared__ double red[8];
+    int64_t t = A.ctl->round;
+    const double *__restrict__ s_in = A.s + (t & 1) * A.n;
+    int64_t r = t + 1;
+    Partial p;
+    zero(p);
+    int64_t b = blockIdx.x;
+    int tid = threadIdx.x;
+    if (b < A.blk_start[1]) {
+        // bin 0: thread per destination (in-degree <= 4), sequential sum
+        int64_t idx = A.bin_start[0] + b * 256 + tid;
+        if (idx < A.bin_start[1]) {
+            int32_t v = A.ids[idx];
+            double acc = 0.0;
+            for (int64_t e = A.in_off[v]; e < A.in_off[v + 1]; ++e) acc += __ldg(&s_in[A.in_src[e]]);
+            epilogue(A, v, A.h[v] + acc, r, p);
+        }
+    } else if (b < A.blk_start[2]) {
+        // bin 1: 8 lanes per destination (in-degree 5..64)
+        int g = tid >> 3, l = tid & 7;
+        int64_t idx = A.bin_start[1] + (b - A.blk_start[1]) * 32 + g;
+        bool ok = idx < A.bin_start[2];
+        int32_t v = ok ? A.ids[idx] : 0;
+        double acc = 0.0;
+        if (ok)
+            for (int64_t e = A.in_off[v] + l; e < A.in_off[v + 1]; e += 8) acc += __ldg(&s_in[A.in_src[e]]);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        if (ok && l == 0) epilogue(A, v, A.h[v] + acc, r, p);
+    } else if (b < A.blk_start[3]) {
+        // bin 2: warp per destination (in-degree 65..2048)
+        int w = tid >> 5, l = tid & 31;
+        int64_t idx = A.bin_start[2] + (b - A.blk_start[2]) * 8 + w;
+        bool ok = idx < A.bin_start[3];
+        int32_t v = ok ? A.ids[idx] : 0;
+        double acc = 0.0;
+        if (ok)
+            for (int64_t e = A.in_off[v] + l; e < A.in_off[v + 1]; e += 32) acc += __ldg(&s_in[A.in_src[e]]);
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (ok && l == 0) epilogue(A, v, A.h[v] + acc, r, p);
+    } else if (b < A.blk_start[4]) {
+        // bin 3: CTA per destination (hubs)
+        int64_t idx = A.bin_start[3] + (b - A.blk_start[3]);
+        int32_t v = A.ids[idx];
+        double acc = 0.0;
+        for (int64_t e = A.in_off[v] + tid; e < A.in_off[v + 1]; e += 256) acc += __ldg(&s_in[A.in_src[e]]);
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if ((tid & 31) == 0) red[tid >> 5] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            double tot = 0.0;
+            for (int k = 0; k < 8; ++k) tot += red[k];
+            epilogue(A, v, A.h[v] + tot, r, p);
+        }
+    }
+    finish_round(A, p, r, true, false, p);
+}
+
+// Sparse round t, step 1: scatter the frontier's shares (red.global.add.f64)
+__global__ void __launch_bounds__(256) k_push(RunArgs A) {
+    int64_t t = A.ctl->round;
+    const double *__restrict__ s_in = A.s + (t & 1) * A.n;
+    const int32_t *F = A.frontier + (t & 1) * A.fcap;
+    int64_t cnt = A.ctl->fsize[t & 1];
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < cnt; i += nwarps) {
+        int32_t u = F[i];
+        double sh = s_in[u];
+        int64_t lo = A.push_off[u], hi = A.push_off[u + 1];
+        for (int64_t e = lo + lane; e < hi; e += 32) atomicAdd(&A.h[A.push_tgt[e]], sh);
+    }
+}
+
+// Sparse round t, step 2: drain state t+1 over D
+__global__ void __launch_bounds__(256) k_scan(RunArgs A) {
+    int64_t t = A.ctl->round;
+    int64_t r = t + 1;
+    Partial p;
+    zero(p);
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < A.d_count) {
+        int32_t v = A.ids[i];
+        epilogue(A, v, A.h[v], r, p);
+    }
+    finish_round(A, p, r, true, false, p);
+}
+
+// ---------------------------------------------------------------- exact engine
+
+__global__ void k_ex_init(RunArgs A) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < A.n; v += (int64_t)gridDim.x * blockDim.x) {
+        A.h[v] = 1.0;
+        A.reserved[v] = 0.0;
+    }
+}
+
+// trace row of state t (engines.py:421-435) and its drain (engines.py:438-444)
+__global__ void __launch_bounds__(256) k_ex_prep(RunArgs A) {
+    int64_t t = A.ctl->rows;  // state index = rows produced so far
+    Partial p;
+    zero(p);
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v < A.n) {
+        double hv = A.h[v], rv = A.reserved[v];
+        p.digest = digest_term(v, rv, hv);
+        int32_t dv = A.deg[v];
+        bool scan = A.algo == PR_ALGO_FPFULL || dv > 0;
+        bool above = hv > A.xi;
+        p.l1 = hv;
+        if (above) {
+            p.above = hv;
+            if (dv > 0) p.nd_above = hv;
+        } else {
+            p.conv_all = 1;
+            if (scan) p.conv_scan = 1;
+        }
+        bool active = above && scan;
+        A.act[v] = active;
+        if (active) {
+            A.reserved[v] = __dadd_rn(rv, __dmul_rn(A.frac, hv));
+            int32_t len = A.row_len[v];
+            A.s[v] = len > 0 ? __ddiv_rn(__dmul_rn(A.c, hv), (double)dv) : 0.0;
+            p.nact = 1;
+            p.work = (int64_t)dv + 1;
+            p.push_ops = len;
+            if (A.dtc) p.push_dang = A.dtc[v];
+        } else {
+            A.s[v] = 0.0;
+        }
+    }
+    finish_round(A, p, t, false, false, p);
+}
+
+// h(t+1)_v = (active ? 0 : h_v) + sum over in-edges in ascending source order
+// (== the sequential np.bincount accumulation, engines.py:446-448)
+__global__ void k_ex_pull(RunArgs A) {
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= A.n) return;
+    double acc = 0.0;
+    bool receives = A.algo != PR_ALGO_IFP2 || A.deg[v] > 0;
+    if (receives)
+        for (int64_t e = A.in_off[v]; e < A.in_off[v + 1]; ++e) acc = __dadd_rn(acc, A.s[A.in_src[e]]);
+    double base = A.act[v] ? 0.0 : A.h[v];
+    A.h[v] = __dadd_rn(base, acc);
+}
+
+// ---------------------------------------------------------------- settle + normalise (K7)
+
+// engines.py:269-289: reserved[d] = h[d] + sum_{u in S(d)} (c*reserved[u])/deg[u]
+__global__ void k_settle(RunArgs A, const int32_t *dang_ids, int64_t nd, const int64_t *src_off,
+                         const int32_t *src_ids, int exact) {
+    if (exact) {
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd; i += (int64_t)gridDim.x * blockDim.x) {
+            double acc = 0.0;
+            for (int64_t e = src_off[i]; e < src_off[i + 1]; ++e) {
+                int32_t u = src_ids[e];
+                acc = __dadd_rn(acc, __ddiv_rn(__dmul_rn(A.c, A.reserved[u]), (double)A.deg[u]));
+            }
+            int32_t d = dang_ids[i];
+            A.reserved[d] = __dadd_rn(A.h[d], acc);
+            A.h[d] = 0.0;
+        }
+        return;
+    }
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < nd; i += nwarps) {
+        double acc = 0.0;
+        for (int64_t e = src_off[i] + lane; e < src_off[i + 1]; e += 32) {
+            int32_t u = src_ids[e];
+            acc += __ddiv_rn(__dmul_rn(A.c, A.reserved[u]), (double)A.deg[u]);
+        }
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+            int32_t d = dang_ids[i];
+            A.reserved[d] = A.h[d] + acc;
+            A.h[d] = 0.0;
+        }
+    }
+}
+
+// total mass (deterministic; x = reserved [+ h]) and, for IFP2, the
+// post-settle trace row (engines.py:331-335)
+__global__ void __launch_bounds__(256) k_total(RunArgs A, int include_h, int64_t settled, int write_row) {
+    __shared__ bool is_last;
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    Partial p, x;
+    zero(p);
+    zero(x);
+    if (v < A.n) {
+        double hv = A.h[v];
+        x.l1 = include_h ? A.reserved[v] + hv : A.reserved[v];
+        int32_t dv = A.deg[v];
+        bool scan = A.algo == PR_ALGO_FPFULL || dv > 0;
+        p.l1 = hv;
+        if (hv > A.xi) {
+            p.above = hv;
+            if (dv > 0) p.nd_above = hv;
+        } else {
+            p.conv_all = 1;
+            if (scan) p.conv_scan = 1;
+        }
+    }
+    block_reduce(p);
+    block_reduce(x);
+    if (threadIdx.x == 0) {
+        A.partials[blockIdx.x] = p;
+        A.partials[2 * A.max_blocks + blockIdx.x] = x;
+        __threadfence();
+        unsigned ticket = atomicAdd(&A.ctl->blocks_done, 1u);
+        is_last = ticket == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    Partial acc, xacc;
+    zero(acc);
+    zero(xacc);
+    for (int64_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+        add(acc, load_partial(A.partials + b));
+        add(xacc, load_partial(A.partials + 2 * A.max_blocks + b));
+    }
+    block_reduce(acc);
+    block_reduce(xacc);
+    if (threadIdx.x == 0) {
+        RunCtl *ctl = A.ctl;
+        ctl->mass_total = xacc.l1;
+        ctl->settled = settled;
+        ctl->blocks_done = 0;
+        if (write_row) {
+            int64_t r = ctl->rows;
+            ctl->push_ops += settled;
+            ctl->push_ops_dangling += settled;
+            if (r < A.rows_cap) {
+                pr_round_stats row;
+                row.h_l1 = acc.l1;
+                row.alpha = acc.above > 0.0 ? acc.nd_above / acc.above : 1.0;
+                row.active_mass = acc.above;
+                row.carry_mass = acc.l1 - acc.above;
+                row.converged = A.conv_all ? acc.conv_all : acc.conv_scan;
+                row.work = 0;
+                row.push_ops = ctl->push_ops;
+                row.push_ops_dangling = ctl->push_ops_dangling;
+                row.digest = 0;
+                row.wall_ms = (double)(globaltimer() - ctl->t0_ns) * 1e-6;
+                A.rows[r] = row;
+            }
+            ctl->rows = r + 1;
+        }
+    }
+}
+
+__global__ void k_scale(RunArgs A, int include_h, double *values) {
+    double tot = A.ctl->mass_total;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < A.n; v += (int64_t)gridDim.x * blockDim.x) {
+        double x = include_h ? A.reserved[v] + A.h[v] : A.reserved[v];
+        values[v] = x / tot;
+    }
+}
+
+__global__ void k_mark_d(const int32_t *ids, int64_t count, uint8_t *in_d) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        in_d[ids[i]] = 1;
+}
+
+// ---------------------------------------------------------------- host side
+
+static int add_kernel(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t *deps, size_t ndeps, void *func,
+                      unsigned grid, unsigned block, void **args) {
+    cudaKernelNodeParams kp;
+    memset(&kp, 0, sizeof(kp));
+    kp.func = func;
+    kp.gridDim = dim3(grid);
+    kp.blockDim = dim3(block);
+    kp.sharedMemBytes = 0;
+    kp.kernelParams = args;
+    PR_CUDA(cudaGraphAddKernelNode(node, g, deps, ndeps, &kp));
+    return PR_OK;
+}
+
+struct Plan {
+    RunArgs A;
+    bool exact;
+    unsigned g_all, g_pull, g_push, g_scan;
+};
+
+static bool same_key(const pr_run_params &a, const pr_run_params &b) {
+    return a.algorithm == b.algorithm && a.mode == b.mode && a.damping == b.damping && a.threshold == b.threshold &&
+           a.max_rounds == b.max_rounds && a.push_switch == b.push_switch && a.converged_scope == b.converged_scope;
+}
+
+void invalidate_cache(Graph &g) {
+    for (auto &c : g.cached) {
+        if (c.exec) cudaGraphExecDestroy(c.exec);
+        if (c.graph) cudaGraphDestroy(c.graph);
+        c.exec = nullptr;
+        c.graph = nullptr;
+        c.valid = false;
+    }
+}
+
+// One graph per parameter set:  reset -> init -> seeds -> WHILE(loop) {
+// SWITCH(mode) { 0: pull | 1: push -> scan } }   (exact: WHILE { pull -> prep }).
+static int build_graph(Plan &P, cudaGraph_t *out_g, cudaGraphExec_t *out_exec) {
+    cudaGraph_t G;
+    PR_CUDA(cudaGraphCreate(&G, 0));
+    RunArgs &A = P.A;
+    PR_CUDA(cudaGraphConditionalHandleCreate(&A.h_loop, G, 1, cudaGraphCondAssignDefault));
+    PR_CUDA(cudaGraphConditionalHandleCreate(&A.h_mode, G, 0, cudaGraphCondAssignDefault));
+    A.use_graph = 1;
+    void *args[] = {&A};
+    cudaGraphNode_t n_reset, n_init, n_seed, n_while, n_sw, n_a, n_b;
+    PR_TRY(add_kernel(G, &n_reset, nullptr, 0, (void *)k_reset, 1, 1, args));
+    if (P.exact) {
+        PR_TRY(add_kernel(G, &n_init, &n_reset, 1, (void *)k_ex_init, P.g_all, 256, args));
+        PR_TRY(add_kernel(G, &n_seed, &n_init, 1, (void *)k_ex_prep, P.g_all, 256, args));
+    } else {
+        PR_TRY(add_kernel(G, &n_init, &n_reset, 1, (void *)k_init, P.g_all, 256, args));
+        PR_TRY(add_kernel(G, &n_seed, &n_init, 1, (void *)k_seed_scatter, P.g_push, 256, args));
+    }
+    cudaGraphNodeParams wp = {};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = A.h_loop;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    PR_CUDA(cudaGraphAddNode(&n_while, G, &n_seed, 1, &wp));
+    cudaGraph_t body = wp.conditional.phGraph_out[0];
+    if (P.exact) {
+        PR_TRY(add_kernel(body, &n_a, nullptr, 0, (void *)k_ex_pull, P.g_all, 256, args));
+        PR_TRY(add_kernel(body, &n_b, &n_a, 1, (void *)k_ex_prep, P.g_all, 256, args));
+    } else {
+        cudaGraphNodeParams sp = {};
+        sp.type = cudaGraphNodeTypeConditional;
+        sp.conditional.handle = A.h_mode;
+        sp.conditional.type = cudaGraphCondTypeSwitch;
+        sp.conditional.size = 2;
+        PR_CUDA(cudaGraphAddNode(&n_sw, body, nullptr, 0, &sp));
+        cudaGraph_t b_pull = sp.conditional.phGraph_out[0], b_push = sp.conditional.phGraph_out[1];
+        PR_TRY(add_kernel(b_pull, &n_a, nullptr, 0, (void *)k_pull, P.g_pull, 256, args));
+        PR_TRY(add_kernel(b_push, &n_a, nullptr, 0, (void *)k_push, P.g_push, 256, args));
+        PR_TRY(add_kernel(b_push, &n_b, &n_a, 1, (void *)k_scan, P.g_scan, 256, args));
+    }
+    cudaGraphExec_t ex;
+    PR_CUDA(cudaGraphInstantiate(&ex, G, 0));
+    *out_g = G;
+    *out_exec = ex;
+    return PR_OK;
+}
+
+// Workspace sized once per graph; any reallocation invalidates the cached
+// executable graphs (they bake the pointers in).
+static int ws_alloc(Graph &g, int64_t need_blocks) {
+    int64_t n = g.n;
+    void *before[9] = {g.h.ptr, g.reserved.ptr, g.s2.ptr, g.act.ptr, g.in_d.ptr,
+                       g.frontier2.ptr, g.partials.ptr, g.ctl.ptr, g.rows.ptr};
+    PR_TRY(ensure(g.h, 8 * n));
+    PR_TRY(ensure(g.reserved, 8 * n));
+    PR_TRY(ensure(g.s2, 16 * n));
+    PR_TRY(ensure(g.act, n));
+    PR_TRY(ensure(g.in_d, n));
+    PR_TRY(ensure(g.frontier2, 8 * (n + 1)));
+    PR_TRY(ensure(g.ctl, sizeof(RunCtl)));
+    if (g.rows_cap == 0) g.rows_cap = 1 << 16;
+    PR_TRY(ensure(g.rows, sizeof(pr_round_stats) * g.rows_cap));
+    int64_t mb = (n + 255) / 256 + 8;
+    if (need_blocks + 8 > mb) mb = need_blocks + 8;
+    if (mb > g.max_blocks) {
+        PR_TRY(ensure(g.partials, sizeof(Partial) * 3 * mb));
+        g.max_blocks = mb;
+    }
+    void *after[9] = {g.h.ptr, g.reserved.ptr, g.s2.ptr, g.act.ptr, g.in_d.ptr,
+                      g.frontier2.ptr, g.partials.ptr, g.ctl.ptr, g.rows.ptr};
+    if (memcmp(before, after, sizeof(before)) != 0) invalidate_cache(g);
+    return PR_OK;
+}
+
+int run_rounds(Graph &g, const pr_run_params &p, double *d_values, pr_round_stats *rows, int64_t row_cap,
+               pr_run_result *res) {
+    Ctx &ctx = *g.ctx;
+    cudaStream_t st = ctx.stream;
+    const int algo = p.algorithm;
+    if (algo < 0 || algo > 2) return fail(PR_ERR_ARG, "unknown algorithm");
+    if (!(p.damping > 0.0 && p.damping < 1.0)) return fail(PR_ERR_ARG, "damping must be in (0,1)");
+    if (!(p.threshold > 0.0)) return fail(PR_ERR_ARG, "threshold must be positive");
+    if (p.mode < 0 || p.mode > 3) return fail(PR_ERR_ARG, "unknown mode");
+    if (p.max_rounds < 0) return fail(PR_ERR_ARG, "max_rounds must be non-negative");
+    const bool exact = p.mode == PR_MODE_EXACT;
+    if (p.on_round && !exact) return fail(PR_ERR_ARG, "on_round observers need PR_MODE_EXACT");
+    const bool host_loop = p.host_loop || p.on_round;
+    if (algo == PR_ALGO_IFP2) {
+        if (!g.has_ifp2) return fail(PR_ERR_STATE, "IFP2 needs pr_preprocess_ifp2 first");
+    } else {
+        PR_TRY(ensure_dtc(g));
+    }
+    PR_TRY(count_dangling(g));
+    const int which = algo == PR_ALGO_IFP2 ? 1 : 0;
+    PR_TRY(ensure_sched(g, which));
+    auto &S = g.sched[which];
+    int64_t n = g.n;
+    int64_t blk = 0;
+    for (int k = 0; k < 4; ++k) blk += S.blocks[k];
+    PR_TRY(ws_alloc(g, blk));
+
+    Plan P;
+    memset(&P, 0, sizeof(P));
+    RunArgs &A = P.A;
+    A.n = n;
+    A.in_off = g.in_off.as<int64_t>();
+    A.in_src = g.in_src.as<int32_t>();
+    if (algo == PR_ALGO_IFP2) {
+        A.push_off = g.live_off.as<int64_t>();
+        A.push_tgt = g.live_tgt.as<int32_t>();
+        A.row_len = g.live_deg.as<int32_t>();
+        A.dtc = nullptr;
+    } else {
+        A.push_off = g.out_off.as<int64_t>();
+        A.push_tgt = g.out_tgt.as<int32_t>();
+        A.row_len = g.out_deg.as<int32_t>();
+        A.dtc = g.dtc.as<int32_t>();
+    }
+    A.deg = g.out_deg.as<int32_t>();
+    A.ids = S.ids.as<int32_t>();
+    blk = 0;
+    for (int k = 0; k < 4; ++k) {
+        A.bin_start[k] = S.bin_start[k];
+        A.blk_start[k] = blk;
+        blk += S.blocks[k];
+    }
+    A.bin_start[4] = S.bin_start[4];
+    A.blk_start[4] = blk;
+    A.d_count = S.count;
+    A.seeds = S.seed_ids.as<int32_t>();
+    A.n_seed = S.n_seed;
+    A.in_d = g.in_d.as<uint8_t>();
+    A.h = g.h.as<double>();
+    A.reserved = g.reserved.as<double>();
+    A.s = g.s2.as<double>();
+    A.frontier = g.frontier2.as<int32_t>();
+    A.fcap = n;
+    A.act = g.act.as<uint8_t>();
+    A.partials = g.partials.as<Partial>();
+    A.max_blocks = g.max_blocks;
+    A.ctl = g.ctl.as<RunCtl>();
+    A.rows = g.rows.as<pr_round_stats>();
+    A.rows_cap = g.rows_cap;
+    A.c = p.damping;
+    A.xi = p.threshold;
+    A.frac = algo == PR_ALGO_FPFULL ? 1.0 - p.damping : 1.0;
+    A.algo = algo;
+    A.policy = p.mode;
+    A.conv_all = p.converged_scope == PR_CONV_ALL;
+    A.max_rounds = p.max_rounds;
+    int64_t pull_edges = algo == PR_ALGO_IFP2 ? g.ifp2.live_edges : g.m;
+    double sw = p.push_switch > 0.0 ? p.push_switch : 0.05;
+    A.push_work = sw * (double)(pull_edges + S.count);
+    A.n_scan = (double)(algo == PR_ALGO_FPFULL ? n : n - g.n_dangling);
+    P.exact = exact;
+    P.g_all = grid_for(n, 256);
+    P.g_pull = (unsigned)(blk > 0 ? blk : 1);
+    P.g_scan = grid_for(S.count, 256);
+    P.g_push = (unsigned)ctx.sm_count * 8;
+
+    PR_CUDA(cudaMemsetAsync(g.in_d.ptr, 0, n, st));
+    if (S.count) k_mark_d<<<grid_for(S.count, 256), 256, 0, st>>>(A.ids, S.count, g.in_d.as<uint8_t>());
+
+    cudaEvent_t e0, e1, e2;
+    PR_CUDA(cudaEventCreate(&e0));
+    PR_CUDA(cudaEventCreate(&e1));
+    PR_CUDA(cudaEventCreate(&e2));
+    PR_CUDA(cudaEventRecord(e0, st));
+    if (!host_loop) {
+        Graph::Cached *slot = nullptr;
+        for (auto &c : g.cached)
+            if (c.valid && same_key(c.key, p)) { slot = &c; break; }
+        if (!slot) {
+            slot = &g.cached[0];
+            for (auto &c : g.cached)
+                if (!c.valid) { slot = &c; break; }
+            if (slot->exec) cudaGraphExecDestroy(slot->exec);
+            if (slot->graph) cudaGraphDestroy(slot->graph);
+            slot->exec = nullptr;
+            slot->graph = nullptr;
+            slot->valid = false;
+            PR_TRY(build_graph(P, &slot->graph, &slot->exec));
+            slot->key = p;
+            slot->valid = true;
+        }
+        PR_CUDA(cudaGraphLaunch(slot->exec, st));
+    } else {
+        A.use_graph = 0;
+        RunCtl hc;
+        k_reset<<<1, 1, 0, st>>>(A);
+        if (exact) {
+            k_ex_init<<<P.g_all, 256, 0, st>>>(A);
+            k_ex_prep<<<P.g_all, 256, 0, st>>>(A);
+        } else {
+            k_init<<<P.g_all, 256, 0, st>>>(A);
+            k_seed_scatter<<<P.g_push, 256, 0, st>>>(A);
+        }
+        std::vector<double> obs_r, obs_h;
+        if (p.on_round) {
+            obs_r.resize((size_t)n);
+            obs_h.resize((size_t)n);
+        }
+        for (;;) {
+            PR_CUDA(cudaMemcpyAsync(&hc, A.ctl, sizeof(hc), cudaMemcpyDeviceToHost, st));
+            PR_CUDA(cudaStreamSynchronize(st));
+            if (hc.done) break;
+            if (exact) {
+                k_ex_pull<<<P.g_all, 256, 0, st>>>(A);
+                if (p.on_round) {
+                    // reference semantics: called after round t's update (engines.py:453-454)
+                    PR_CUDA(cudaMemcpyAsync(obs_r.data(), A.reserved, 8 * n, cudaMemcpyDeviceToHost, st));
+                    PR_CUDA(cudaMemcpyAsync(obs_h.data(), A.h, 8 * n, cudaMemcpyDeviceToHost, st));
+                    PR_CUDA(cudaStreamSynchronize(st));
+                    p.on_round(p.user, hc.rows - 1, obs_r.data(), obs_h.data());
+                }
+                k_ex_prep<<<P.g_all, 256, 0, st>>>(A);
+            } else if (hc.mode == 0) {
+                k_pull<<<P.g_pull, 256, 0, st>>>(A);
+            } else {
+                k_push<<<P.g_push, 256, 0, st>>>(A);
+                k_scan<<<P.g_scan, 256, 0, st>>>(A);
+            }
+            PR_CUDA(cudaGetLastError());
+        }
+    }
+    PR_CUDA(cudaEventRecord(e1, st));
+    int64_t settled = 0;
+    if (algo == PR_ALGO_IFP2) {
+        settled = g.ifp2.source_edges;
+        if (g.ifp2.dangling)
+            k_settle<<<exact ? grid_for(g.ifp2.dangling, 256) : grid_for(g.ifp2.dangling * 32, 256), 256, 0, st>>>(
+                A, g.dang_ids.as<int32_t>(), g.ifp2.dangling, g.src_off.as<int64_t>(), g.src_ids.as<int32_t>(),
+                exact ? 1 : 0);
+    }
+    int include_h = algo == PR_ALGO_IFP1 ? 1 : 0;
+    k_total<<<P.g_all, 256, 0, st>>>(A, include_h, settled, algo == PR_ALGO_IFP2 ? 1 : 0);
+    if (d_values) {
+        unsigned gs = grid_for(n, 256);
+        if (gs > 4096) gs = 4096;
+        k_scale<<<gs, 256, 0, st>>>(A, include_h, d_values);
+    }
+    PR_CUDA(cudaEventRecord(e2, st));
+    PR_CUDA(cudaEventSynchronize(e2));
+    PR_CUDA(cudaGetLastError());
+    float ms_loop = 0.f, ms_all = 0.f;
+    PR_CUDA(cudaEventElapsedTime(&ms_loop, e0, e1));
+    PR_CUDA(cudaEventElapsedTime(&ms_all, e0, e2));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    RunCtl hc;
+    PR_CUDA(cudaMemcpy(&hc, A.ctl, sizeof(hc), cudaMemcpyDeviceToHost));
+    int64_t nrows = hc.rows;
+    if (rows && row_cap > 0) {
+        int64_t k = nrows < row_cap ? nrows : row_cap;
+        if (k > g.rows_cap) k = g.rows_cap;
+        PR_CUDA(cudaMemcpy(rows, A.rows, sizeof(pr_round_stats) * k, cudaMemcpyDeviceToHost));
+    }
+    if (res) {
+        res->rounds = hc.pull_rounds + hc.push_rounds;
+        res->rows = nrows;
+        res->push_ops = hc.push_ops;
+        res->push_ops_dangling = hc.push_ops_dangling;
+        res->settled = settled;
+        res->pull_rounds = hc.pull_rounds;
+        res->push_rounds = hc.push_rounds;
+        res->mass_total = hc.mass_total;
+        res->push_ms = ms_all;
+        res->round_ms = ms_loop;
+        res->bytes_moved = hc.bytes;
+    }
+    if (hc.done == 2)
+        return fail(PR_ERR_NOT_SETTLED,
+                    "sync simulation did not settle in " + std::to_string(p.max_rounds) + " iterations");
+    return PR_OK;
+}
+
+}  // namespace pr

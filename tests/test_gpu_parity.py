@@ -1,0 +1,297 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle and the
+reference's golden vectors.
+
+Bars (BASELINE.json north_star): integer preprocessing bit-exact; exact
+(sync) rounds bit-identical state; fast engines within L1 <= 1e-9 of the
+reference vectors with identical top-100 under (-score, id).
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import corpus_graph
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2302_03245_b200")
+from paper_2302_03245_b200 import synthetic  # noqa: E402
+
+XI = 1e-12
+INT_KEYS = ("out_offsets", "out_targets", "in_offsets", "in_sources")
+CLS_KEYS = ("dangling", "unreferenced", "weak_dangling", "weak_unreferenced")
+IFP2_KEYS = ("live_offsets", "live_targets", "live_degree", "dangling_ids", "source_offsets", "source_ids")
+MODES = ("auto", "pull", "push")
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.int64).tobytes()).hexdigest()
+
+
+def top100(values):
+    order = np.lexsort((np.arange(values.size), -values))   # (-score, id), serialize.py:16
+    return order[:100]
+
+
+def cfg(xi=XI):
+    return P.SolverConfig(threshold=xi)
+
+
+# ------------------------------------------------------------ graph core
+
+def test_corpus_preprocessing_bit_exact(golden_corpus):
+    for i in range(int(golden_corpus["count"])):
+        n, src, dst = corpus_graph(golden_corpus, i)
+        g = P.from_edges(n, src, dst)
+        for k in INT_KEYS:
+            assert np.array_equal(getattr(g, k), golden_corpus[f"g{i}_{k}"]), (i, k)
+        cls = P.classify(g)
+        for k in CLS_KEYS:
+            assert np.array_equal(getattr(cls, k), golden_corpus[f"g{i}_{k}"]), (i, k)
+        assert cls.dangling_edge_count == int(golden_corpus[f"g{i}_m_d"])
+        assert np.array_equal(P.dangling_target_counts(g, cls), golden_corpus[f"g{i}_dtc"])
+        pg = P.preprocess_ifp2(g, cls)
+        for k in IFP2_KEYS:
+            assert np.array_equal(getattr(pg, k), golden_corpus[f"g{i}_{k}"]), (i, k)
+
+
+@pytest.mark.parametrize("config", ["c1", "c2", "c4"])
+def test_config_preprocessing_bit_exact(config, golden_c1):
+    n, src, dst = synthetic.make(config, seed=0)
+    g = P.from_edges(n, src, dst)
+    ref = oracle.from_edges(n, src, dst)
+    for k in INT_KEYS:
+        assert np.array_equal(getattr(g, k), getattr(ref, k)), k
+    cls = P.classify(g)
+    rc = oracle.classify(ref)
+    for k in CLS_KEYS:
+        assert np.array_equal(getattr(cls, k), getattr(rc, k)), k
+    assert cls.dangling_edge_count == rc.dangling_edge_count
+    pg = P.preprocess_ifp2(g, cls)
+    rp = oracle.preprocess_ifp2(ref, rc.dangling)
+    for k in IFP2_KEYS:
+        assert np.array_equal(getattr(pg, k), getattr(rp, k)), k
+    if config == "c1":
+        for k in INT_KEYS + CLS_KEYS + IFP2_KEYS:
+            gold = golden_c1[f"{k}_sha256"]
+            obj = pg if k in IFP2_KEYS else (cls if k in CLS_KEYS else g)
+            assert sha(getattr(obj, k)) == str(gold), k
+
+
+def test_upload_roundtrip_and_errors():
+    n, src, dst = synthetic.make("c1", seed=1)
+    ref = oracle.from_edges(n, src, dst)
+    dev = P.graph.DeviceGraph.upload(ref)
+    out = dev.export()
+    for k in INT_KEYS:
+        assert np.array_equal(out[k], getattr(ref, k)), k
+    with pytest.raises(ValueError, match="range"):
+        P.from_edges(2, [0], [2])
+    with pytest.raises(ValueError):
+        P.from_edges(0, [], [])
+
+
+def test_rmat_device_generator_matches_numpy():
+    from paper_2302_03245_b200 import _lib
+    import ctypes
+    ctx = _lib.context()
+    L = _lib.load()
+    count = 200_000
+    ps, pd = ctypes.c_void_p(), ctypes.c_void_p()
+    _lib.check(L.pr_device_alloc(ctx.handle, 8 * count, ctypes.byref(ps)))
+    _lib.check(L.pr_device_alloc(ctx.handle, 8 * count, ctypes.byref(pd)))
+    _lib.check(L.pr_rmat_generate(ctx.handle, 20, 5, 0.57, 0.19, 0.19, 7, 12345, count, ps, pd))
+    hs, hd = np.empty(count, np.int64), np.empty(count, np.int64)
+    _lib.check(L.pr_memcpy_d2h(ctx.handle, _lib.ptr(hs), ps, 8 * count))
+    _lib.check(L.pr_memcpy_d2h(ctx.handle, _lib.ptr(hd), pd, 8 * count))
+    L.pr_device_free(ctx.handle, ps)
+    L.pr_device_free(ctx.handle, pd)
+    _, s, d = synthetic.rmat_edges(20, 5, seed=7, first=12345, count=count)
+    assert np.array_equal(hs, s) and np.array_equal(hd, d)
+
+
+# ------------------------------------------------------------ exact (sync) rounds
+
+def _sync_check(gold, key, vec, tr):
+    for col in ("converged", "work", "push_ops", "push_ops_dangling"):
+        assert np.array_equal(np.asarray(tr.column(col)), gold[key + col]), (key, col)
+    scale = max(1.0, float(gold[key + "h_l1"][0]))
+    for col in ("h_l1", "alpha", "active_mass", "carry_mass"):
+        np.testing.assert_allclose(tr.column(col), gold[key + col], rtol=1e-12, atol=1e-14 * scale)
+    np.testing.assert_allclose(vec.values, gold[key + "values"], rtol=1e-13, atol=1e-17)
+
+
+def test_corpus_sync_exact_state_bit_identical(golden_corpus):
+    for i in range(int(golden_corpus["count"])):
+        n, src, dst = corpus_graph(golden_corpus, i)
+        g = P.from_edges(n, src, dst)
+        cls = P.classify(g)
+        pg = P.preprocess_ifp2(g, cls)
+        for variant in ("ifp1", "ifp2", "fp-full"):
+            key = f"g{i}_sync_{variant.replace('-', '_')}_"
+            last = {}
+
+            def cb(t, r, h, last=last):
+                last["r"], last["h"] = r.copy(), h.copy()
+
+            subject = pg if variant == "ifp2" else g
+            vec, tr = P.sync_simulate(subject, cfg(), variant=variant, cls=cls, on_iteration=cb)
+            _sync_check(golden_corpus, key, vec, tr)
+            if key + "reserved_pre_settle" in golden_corpus:
+                assert np.array_equal(last["r"], golden_corpus[key + "reserved_pre_settle"]), key
+                assert np.array_equal(last["h"], golden_corpus[key + "h_pre_settle"]), key
+
+
+@pytest.mark.parametrize("config", ["c1", "c2"])
+def test_sync_exact_per_round_digest_matches_oracle(config):
+    """Every round's (reserved, pending) state bit-identical to the oracle's
+    restatement of sync_simulate, via the per-row state digest (device graph
+    loop, no host round trips)."""
+    n, src, dst = synthetic.make(config, seed=0)
+    g = P.from_edges(n, src, dst)
+    ref = oracle.from_edges(n, src, dst)
+    for variant in ("ifp1", "ifp2"):
+        o = oracle.sync_simulate(ref, variant, threshold=1e-10)
+        dev = P.graph.device_graph(g)
+        if variant == "ifp2":
+            dev.preprocess_ifp2()
+        values, rows, res, reserved, pending = dev.run(variant, "exact", 0.85, 1e-10, 1_000_000,
+                                                       1, want_state=True)
+        k = len(o.rows) - (1 if variant == "ifp2" else 0)
+        assert res.rounds == o.iterations
+        assert np.array_equal(rows["digest"][:k], o.rows["digest"][:k]), variant
+        for col in ("converged", "work", "push_ops", "push_ops_dangling"):
+            assert np.array_equal(rows[col], o.rows[col]), (variant, col)
+        if variant == "ifp1":
+            assert np.array_equal(reserved, o.reserved) and np.array_equal(pending, o.h)
+        np.testing.assert_allclose(values, o.values, rtol=1e-12, atol=0)
+
+
+# ------------------------------------------------------------ fast engines vs reference
+
+@pytest.mark.parametrize("mode", MODES)
+def test_corpus_engines_match_reference(golden_corpus, mode):
+    for i in range(int(golden_corpus["count"])):
+        n, src, dst = corpus_graph(golden_corpus, i)
+        g = P.from_edges(n, src, dst)
+        cls = P.classify(g)
+        pg = P.preprocess_ifp2(g, cls)
+        v1, t1 = P.ifp1_run(g, cls, cfg(), workers=4, mode=mode)
+        v2, t2 = P.ifp2_run(pg, cfg(), workers=4, mode=mode)
+        tol = max(1e-10, 10 * XI * n)
+        assert np.max(np.abs(v1.values - golden_corpus[f"g{i}_ifp1_values"])) <= tol, i
+        assert np.max(np.abs(v2.values - golden_corpus[f"g{i}_ifp2_values"])) <= tol, i
+        assert t2.final.push_ops_dangling == cls.dangling_edge_count
+        assert t1.final.push_ops_dangling >= cls.dangling_edge_count
+        if f"g{i}_dense_values" in golden_corpus:
+            d = golden_corpus[f"g{i}_dense_values"]
+            assert np.max(np.abs(v1.values - d) / d) <= max(1e-8, 10 * XI * n)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_c1_engines_parity(golden_c1, mode):
+    n, src, dst = synthetic.make("c1", seed=0)
+    g = P.from_edges(n, src, dst)
+    cls = P.classify(g)
+    pg = P.preprocess_ifp2(g, cls)
+    for algo, run in (("ifp1", lambda: P.ifp1_run(g, cls, cfg(), mode=mode)),
+                      ("ifp2", lambda: P.ifp2_run(pg, cfg(), mode=mode))):
+        vec, tr = run()
+        ref = golden_c1[f"{algo}_values"]
+        assert np.abs(vec.values - ref).sum() <= 1e-9, algo
+        assert np.array_equal(top100(vec.values), top100(ref)), algo
+        assert abs(vec.values.sum() - 1.0) <= 1e-12
+    assert tr.final.push_ops_dangling == int(golden_c1["ifp2_push_ops_dangling"])
+    # the phase-1 final row precedes the settle row (engines.py:331-335)
+    assert tr.samples[-2].push_ops_dangling == 0
+
+
+@pytest.mark.parametrize("xi", [1e-10, 1e-12])
+def test_c2_full_size_parity(xi):
+    """C2 at full size: fast engine vs the oracle sync twin (L1 <= 1e-9,
+    identical top-100) and mass conservation."""
+    n, src, dst = synthetic.make("c2", seed=0)
+    g = P.from_edges(n, src, dst)
+    ref = oracle.from_edges(n, src, dst)
+    cls = P.classify(g)
+    pg = P.preprocess_ifp2(g, cls)
+    for algo in ("ifp1", "ifp2"):
+        o = oracle.sync_simulate(ref, algo, threshold=xi)
+        for mode in MODES:
+            if algo == "ifp1":
+                vec, tr = P.ifp1_run(g, cls, cfg(xi), mode=mode)
+            else:
+                vec, tr = P.ifp2_run(pg, cfg(xi), mode=mode)
+            assert np.abs(vec.values - o.values).sum() <= 1e-9, (algo, mode)
+            assert np.array_equal(top100(vec.values), top100(o.values)), (algo, mode)
+            if algo == "ifp2":
+                assert tr.final.push_ops_dangling == cls.dangling_edge_count
+
+
+# ------------------------------------------------------------ known answers (reference tests)
+
+def test_known_answers():
+    c = P.SolverConfig()
+    chain = P.from_edges(3, [0, 1], [1, 2])
+    exact = np.array([1.0, 1.85, 2.5725]) / 5.4225                  # test_solvers.py:16-18
+    v, _ = P.ifp1_run(chain, P.classify(chain), cfg())
+    assert np.max(np.abs(v.values - exact)) <= 1e-10
+    pv, _ = P.power_method(chain, c)
+    assert np.max(np.abs(pv.values - exact)) < 1e-12               # test_solvers.py:58-61
+    fanin = P.from_edges(3, [0, 1], [2, 2])
+    cls = P.classify(fanin)
+    v2, t2 = P.ifp2_run(P.preprocess_ifp2(fanin, cls), cfg(), workers=2)
+    assert np.max(np.abs(v2.values - np.array([1.0, 1.0, 2.7]) / 4.7)) <= 1e-12  # test_engines.py:246-257
+    assert t2.samples[-2].push_ops == 0
+    cyc = P.from_edges(2, [0, 1], [1, 0])
+    v, _ = P.ifp1_run(cyc, P.classify(cyc), cfg())
+    assert v.values == pytest.approx([0.5, 0.5], abs=1e-10)
+    empty = P.from_edges(3, [], [])
+    ce = P.classify(empty)
+    v, _ = P.ifp1_run(empty, ce, cfg(), workers=2)
+    assert v.values == pytest.approx([1 / 3] * 3, abs=1e-12)       # test_engines.py:278-286
+    v, _ = P.ifp2_run(P.preprocess_ifp2(empty, ce), cfg(), workers=2)
+    assert v.values == pytest.approx([1 / 3] * 3, abs=1e-12)
+    chain_cls = P.classify(chain)
+    assert chain_cls.weak_dangling.tolist() == [1] and chain_cls.weak_unreferenced.tolist() == [1]
+    single = P.from_edges(1, [], [])
+    v, _ = P.ifp1_run(single, P.classify(single), cfg())
+    assert v.values.tolist() == [1.0]
+
+
+def test_power_matches_reference(golden_corpus, golden_c1):
+    for i in range(int(golden_corpus["count"])):
+        n, src, dst = corpus_graph(golden_corpus, i)
+        g = P.from_edges(n, src, dst)
+        vec, tr = P.power_method(g, P.SolverConfig(max_iterations=210))
+        np.testing.assert_allclose(vec.values, golden_corpus[f"g{i}_power_values"], rtol=0, atol=1e-14)
+        np.testing.assert_allclose(tr.column("h_l1"), golden_corpus[f"g{i}_power_deltas"], rtol=1e-9, atol=1e-15)
+    n, src, dst = synthetic.make("c1", seed=0)
+    vec, _ = P.power_method(P.from_edges(n, src, dst), P.SolverConfig(max_iterations=210))
+    np.testing.assert_allclose(vec.values, golden_c1["power_values"], rtol=1e-12, atol=0)
+    sums = []
+    P.power_method(P.from_edges(n, src, dst), P.SolverConfig(max_iterations=20),
+                   on_iterate=lambda k, pi: sums.append(float(pi.sum())))
+    assert len(sums) == 20 and all(abs(s - 1.0) <= 1e-12 for s in sums)
+
+
+def test_validation_errors():
+    chain = P.from_edges(3, [0, 1], [1, 2])
+    cls = P.classify(chain)
+    with pytest.raises(ValueError, match="damping"):
+        P.ifp1_run(chain, cls, P.SolverConfig(damping=1.5))
+    with pytest.raises(ValueError, match="threshold"):
+        P.ifp1_run(chain, cls, P.SolverConfig(threshold=0.0))
+    with pytest.raises(ValueError, match=">= 1"):
+        P.ifp1_run(chain, cls, cfg(), workers=0)
+    with pytest.raises(ValueError, match="strategy"):
+        P.ifp1_run(chain, cls, cfg(), strategy="zigzag")
+    with pytest.raises(ValueError, match="variant"):
+        P.sync_simulate(chain, cfg(), variant="both")
+    with pytest.raises(ValueError, match="backend"):
+        P.ifp1_run(chain, cls, cfg(), backend="fortran")
+    cyc = P.from_edges(2, [0, 1], [1, 0])
+    with pytest.raises(RuntimeError, match="settle"):
+        P.sync_simulate(cyc, cfg(), variant="ifp1", max_iterations=3)

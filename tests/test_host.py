@@ -1,0 +1,102 @@
+"""CPU-only checks of the host layer and the C-ABI library (no compute)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2302_03245_b200 as P
+from paper_2302_03245_b200 import _lib, synthetic
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    names = []
+    for fn in os.listdir(os.path.join(REPO, "include")):
+        if fn.endswith(".h"):
+            text = open(os.path.join(REPO, "include", fn)).read()
+            names += re.findall(r"^\s*(?:int|const char \*|void)\s*\**\s*(pr_\w+)\s*\(", text, re.M)
+    return sorted(set(names))
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.load()
+    names = header_functions()
+    assert len(names) >= 25
+    missing = [n for n in names if not hasattr(L, n)]
+    assert not missing, missing
+    assert set(names) <= set(_lib.SIGNATURES), set(names) - set(_lib.SIGNATURES)
+    assert L.pr_abi_version() == 1
+
+
+def test_struct_layouts_match_header():
+    assert ctypes.sizeof(_lib.RoundStats) == 80
+    assert _lib.ROUND_DTYPE.itemsize == 80
+    assert ctypes.sizeof(_lib.RunResult) == 11 * 8
+
+
+def test_library_is_sm100a_only():
+    out = os.popen(f"cuobjdump --list-elf {_lib.LIB_PATH} 2>/dev/null").read()
+    if not out:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out), out
+
+
+def test_no_cpu_fallback_without_device():
+    if _lib.device_count() > 0:
+        pytest.skip("a CUDA device is present")
+    assert P.available_backends() == []
+    with pytest.raises(RuntimeError):
+        P.from_edges(3, [0, 1], [1, 2])
+
+
+def test_solver_config_validation_messages():
+    with pytest.raises(ValueError, match="damping"):
+        P.SolverConfig(damping=1.0).validate(3)
+    with pytest.raises(ValueError, match="threshold"):
+        P.SolverConfig(threshold=-1).validate(3)
+    with pytest.raises(ValueError, match="personalization"):
+        P.SolverConfig(personalization=np.ones(2)).validate(3)
+    with pytest.raises(ValueError, match="non-negative"):
+        P.SolverConfig(max_iterations=-1).validate(3)
+    P.SolverConfig().validate(3)
+    assert P.SolverConfig().restart_vector(4).tolist() == [0.25] * 4
+
+
+def test_backend_resolution():
+    assert P.resolve_backend("cuda").NAME == "cuda"
+    assert P.resolve_backend("auto").NAME == "cuda"
+    with pytest.raises(ValueError, match="backend"):
+        P.resolve_backend("python")
+
+
+def test_from_edges_argument_errors_before_device():
+    with pytest.raises(ValueError, match="equal length"):
+        P.from_edges(3, [0, 1], [1])
+    with pytest.raises(ValueError, match="at least one"):
+        P.from_edges(0, [], [])
+    with pytest.raises(ValueError, match="range"):
+        P.from_edges(2, [0], [2])
+
+
+def test_trace_csv(tmp_path):
+    tr = P.RunTrace(samples=[P.TraceSample(0, 1.5, 2, 1.0, 3, 4, 5, 6.0)])
+    path = tmp_path / "t.csv"
+    tr.write_csv(path)
+    lines = path.read_text().splitlines()
+    assert lines[0] == "t,h_l1,converged,alpha,work,push_ops,push_ops_dangling,wall_ms"
+    assert lines[1] == "0,1.5,2,1.0,3,4,5,6.000"
+    assert tr.final.push_ops == 4
+
+
+def test_rmat_numpy_generator_is_deterministic_and_sane():
+    n, s1, d1 = synthetic.rmat_edges(12, 4, seed=3)
+    _, s2, d2 = synthetic.rmat_edges(12, 4, seed=3, first=100, count=50)
+    assert np.array_equal(s1[100:150], s2) and np.array_equal(d1[100:150], d2)
+    assert n == 4096 and s1.max() < n and d1.max() < n
+    # quadrant a dominates: the low half of the id range holds ~76% of sources
+    assert 0.70 < np.mean(s1 < n // 2) < 0.82
