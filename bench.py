@@ -193,7 +193,7 @@ def run_ours(args):
         _, _, res, _, _ = dev.run(args.algo, args.mode, DAMPING, XI, 1_000_000, _lib.CONV_SCAN, row_cap=1)
         return res
 
-    for _ in range(max(args.warmup, 3 if args.warmup < 3 else args.warmup)):
+    for _ in range(args.warmup):
         step()
     if world > 1:
         torch.distributed.barrier()

@@ -14,7 +14,7 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libpushrank_cuda.so")
+LIB_PATH = os.environ.get("PUSHRANK_LIB") or os.path.join(HERE, "lib", "libpushrank_cuda.so")
 
 c_i64 = ctypes.c_int64
 c_f64 = ctypes.c_double

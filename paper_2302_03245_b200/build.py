@@ -12,7 +12,8 @@ HEADERS = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [
     os.path.join(os.path.dirname(HERE), "include", "pushrank_cuda.h")]
 LIB = os.path.join(HERE, "lib", "libpushrank_cuda.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-warn-spills"]
+              "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills"]
+OBJ_DIR = os.path.join(os.path.dirname(HERE), "build", "obj")
 
 
 def nvcc() -> str:
@@ -32,12 +33,23 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    objs = [os.path.join(OBJ_DIR, os.path.basename(s)[:-3] + ".o") for s in SOURCES]
+
+    def compile_one(pair):
+        src, obj = pair
+        cmd = [nvcc(), *NVCC_FLAGS, "-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        list(ex.map(compile_one, zip(SOURCES, objs)))
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, *SOURCES]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True)
+    subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs],
+                   check=True)
     os.replace(tmp, LIB)
     return LIB
 

@@ -244,25 +244,23 @@ static int run_common(pr_graph *g, const pr_run_params *params, double *values, 
     Graph &G = *g->g;
     PR_TRY(set_device(*G.ctx));
     cudaStream_t st = G.ctx->stream;
-    DevBuf dv;
-    double *d_values = nullptr;
-    if (values) {
-        if (host_out) {
-            PR_TRY(ensure(dv, 8 * G.n));
-            d_values = dv.as<double>();
-        } else {
-            d_values = values;
-        }
+    DevBuf dv, dr, dp;
+    double *d_values = values, *d_reserved = reserved, *d_pending = pending;
+    if (host_out) {
+        if (values) { PR_TRY(ensure(dv, 8 * G.n)); d_values = dv.as<double>(); }
+        if (reserved) { PR_TRY(ensure(dr, 8 * G.n)); d_reserved = dr.as<double>(); }
+        if (pending) { PR_TRY(ensure(dp, 8 * G.n)); d_pending = dp.as<double>(); }
     }
     pr_run_result local;
     memset(&local, 0, sizeof(local));
-    int rc = run_rounds(G, *params, d_values, rows, row_cap, &local);
+    int rc = run_rounds(G, *params, d_values, d_reserved, d_pending, rows, row_cap, &local);
     if (result) *result = local;
     if (rc != PR_OK && rc != PR_ERR_NOT_SETTLED) return rc;
-    cudaMemcpyKind kind = host_out ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-    if (values && host_out) PR_CUDA(cudaMemcpyAsync(values, d_values, 8 * G.n, kind, st));
-    if (reserved) PR_CUDA(cudaMemcpyAsync(reserved, G.reserved.ptr, 8 * G.n, kind, st));
-    if (pending) PR_CUDA(cudaMemcpyAsync(pending, G.h.ptr, 8 * G.n, kind, st));
+    if (host_out) {
+        if (values) PR_CUDA(cudaMemcpyAsync(values, d_values, 8 * G.n, cudaMemcpyDeviceToHost, st));
+        if (reserved) PR_CUDA(cudaMemcpyAsync(reserved, d_reserved, 8 * G.n, cudaMemcpyDeviceToHost, st));
+        if (pending) PR_CUDA(cudaMemcpyAsync(pending, d_pending, 8 * G.n, cudaMemcpyDeviceToHost, st));
+    }
     PR_CUDA(cudaStreamSynchronize(st));
     return rc;
 }

@@ -9,6 +9,7 @@
 #include <cstring>
 
 #include "internal.cuh"
+#include "cubutil.cuh"
 
 namespace pr {
 
@@ -32,16 +33,9 @@ Graph::~Graph() {
         if (c.exec) cudaGraphExecDestroy(c.exec);
         if (c.graph) cudaGraphDestroy(c.graph);
     }
+    delete run;
 }
 
-// Run a CUB algorithm: size query, grow ctx scratch, execute.
-template <class F> static int cub_run(Ctx &ctx, F &&f) {
-    size_t bytes = 0;
-    PR_CUDA(f((void *)nullptr, bytes));
-    PR_TRY(ensure(ctx.scratch, bytes));
-    PR_CUDA(f(ctx.scratch.ptr, bytes));
-    return PR_OK;
-}
 
 static int bit_width_u64(unsigned long long x) {
     int b = 0;
@@ -49,8 +43,6 @@ static int bit_width_u64(unsigned long long x) {
     return b;
 }
 
-#define GRID_STRIDE(i, count) \
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (count); i += (int64_t)gridDim.x * blockDim.x)
 
 // ---------------------------------------------------------------- elementwise helpers
 
@@ -503,6 +495,78 @@ int preprocess_ifp2_device(Graph &g) {
     return PR_OK;
 }
 
+// ---------------------------------------------------------------- run layout
+
+// sort key: class (2 bits) | descending out-degree inside class 0 (31 bits) | id (31 bits)
+__global__ void k_relabel_keys(const int64_t *__restrict__ out_off, const int64_t *__restrict__ in_off, int64_t n,
+                               unsigned long long *__restrict__ keys) {
+    GRID_STRIDE(v, n) {
+        int64_t od = out_off[v + 1] - out_off[v], id = in_off[v + 1] - in_off[v];
+        unsigned long long cls = od > 0 ? (id > 0 ? 0 : 1) : (id > 0 ? 2 : 3);
+        unsigned long long dk = cls == 0 ? (unsigned long long)(0x7FFFFFFFll - od) : 0ull;
+        keys[v] = (cls << 62) | (dk << 31) | (unsigned long long)v;
+    }
+}
+
+__global__ void k_perm_from_keys(const unsigned long long *__restrict__ keys, int64_t n, int32_t *__restrict__ perm,
+                                 int32_t *__restrict__ rank) {
+    GRID_STRIDE(i, n) {
+        int32_t v = (int32_t)(keys[i] & 0x7FFFFFFFull);
+        perm[i] = v;
+        rank[v] = (int32_t)i;
+    }
+}
+
+// warp per original row: relabelled (src, dst) of every edge
+__global__ void k_relabel_edges(const int64_t *__restrict__ out_off, const int32_t *__restrict__ out_tgt, int64_t n,
+                                const int32_t *__restrict__ rank, int64_t *__restrict__ src, int64_t *__restrict__ dst) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t u = warp; u < n; u += nw) {
+        int32_t ru = rank[u];
+        for (int64_t e = out_off[u] + lane; e < out_off[u + 1]; e += 32) {
+            src[e] = ru;
+            dst[e] = rank[out_tgt[e]];
+        }
+    }
+}
+
+int ensure_run_layout(Graph &g) {
+    if (g.run) return PR_OK;
+    Ctx &ctx = *g.ctx;
+    cudaStream_t st = ctx.stream;
+    int64_t n = g.n, m = g.m;
+    DevBuf keys, sorted, src, dst;
+    PR_TRY(ensure(keys, 8 * n));
+    PR_TRY(ensure(sorted, 8 * n));
+    PR_TRY(ensure(g.perm, 4 * n));
+    PR_TRY(ensure(g.rank, 4 * n));
+    k_relabel_keys<<<gs_grid(ctx, n), 256, 0, st>>>(g.out_off.as<int64_t>(), g.in_off.as<int64_t>(), n,
+                                                   keys.as<unsigned long long>());
+    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortKeys(t, b, keys.as<unsigned long long>(), sorted.as<unsigned long long>(),
+                                              (int)n, 0, 64, st);
+    }));
+    k_perm_from_keys<<<gs_grid(ctx, n), 256, 0, st>>>(sorted.as<unsigned long long>(), n, g.perm.as<int32_t>(),
+                                                     g.rank.as<int32_t>());
+    keys.release();
+    sorted.release();
+    PR_TRY(ensure(src, 8 * (m ? m : 1)));
+    PR_TRY(ensure(dst, 8 * (m ? m : 1)));
+    if (m) {
+        unsigned gr = (unsigned)(ctx.sm_count * 32);
+        k_relabel_edges<<<gr, 256, 0, st>>>(g.out_off.as<int64_t>(), g.out_tgt.as<int32_t>(), n,
+                                            g.rank.as<int32_t>(), src.as<int64_t>(), dst.as<int64_t>());
+    }
+    PR_CUDA(cudaStreamSynchronize(st));
+    PR_CUDA(cudaGetLastError());
+    Graph *r = nullptr;
+    PR_TRY(build_from_device_edges(ctx, n, src.as<int64_t>(), dst.as<int64_t>(), m, &r));
+    g.run = r;
+    return PR_OK;
+}
+
 int count_dangling(Graph &g) {
     if (g.n_dangling >= 0) return PR_OK;
     Ctx &ctx = *g.ctx;
@@ -518,67 +582,6 @@ int count_dangling(Graph &g) {
     PR_CUDA(cudaMemcpyAsync(&c, dcount.ptr, 8, cudaMemcpyDeviceToHost, ctx.stream));
     PR_CUDA(cudaStreamSynchronize(ctx.stream));
     g.n_dangling = c;
-    return PR_OK;
-}
-
-// ---------------------------------------------------------------- pull schedules
-
-// in-degree bins: 0: <= 4 (thread per vertex), 1: <= 64 (8 lanes), 2: <= 2048 (warp), 3: CTA
-__host__ __device__ inline int pull_bin(int64_t d) { return d <= 4 ? 0 : d <= 64 ? 1 : d <= 2048 ? 2 : 3; }
-
-struct InBin {
-    const int64_t *in_off;
-    const int32_t *out_deg;
-    int which, bin;
-    __host__ __device__ bool operator()(int32_t v) const {
-        int64_t d = in_off[v + 1] - in_off[v];
-        bool member = which == 2 ? true : (d > 0 && (which == 0 || out_deg[v] > 0));
-        return member && pull_bin(d) == bin;
-    }
-};
-struct IsSeed {
-    const int64_t *in_off;
-    const int32_t *out_deg;
-    __host__ __device__ bool operator()(int32_t v) const { return in_off[v + 1] == in_off[v] && out_deg[v] > 0; }
-};
-
-int ensure_sched(Graph &g, int which) {
-    auto &S = g.sched[which];
-    if (S.built) return PR_OK;
-    Ctx &ctx = *g.ctx;
-    cudaStream_t st = ctx.stream;
-    int64_t n = g.n;
-    DevBuf dcount;
-    PR_TRY(ensure(dcount, 8));
-    PR_TRY(ensure(S.ids, 4 * n));
-    auto first = thrust::make_counting_iterator<int32_t>(0);
-    int64_t total = 0;
-    static const int per_block[4] = {256, 32, 8, 1};
-    for (int k = 0; k < 4; ++k) {
-        S.bin_start[k] = total;
-        int32_t *dst = S.ids.as<int32_t>() + total;
-        PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
-            return cub::DeviceSelect::If(t, b, first, dst, dcount.as<int64_t>(), (int)n,
-                                         InBin{g.in_off.as<int64_t>(), g.out_deg.as<int32_t>(), which, k}, st);
-        }));
-        int64_t c = 0;
-        PR_CUDA(cudaMemcpyAsync(&c, dcount.ptr, 8, cudaMemcpyDeviceToHost, st));
-        PR_CUDA(cudaStreamSynchronize(st));
-        S.blocks[k] = (c + per_block[k] - 1) / per_block[k];
-        total += c;
-    }
-    S.bin_start[4] = total;
-    S.count = total;
-    PR_TRY(ensure(S.seed_ids, 4 * n));
-    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
-        return cub::DeviceSelect::If(t, b, first, S.seed_ids.as<int32_t>(), dcount.as<int64_t>(), (int)n,
-                                     IsSeed{g.in_off.as<int64_t>(), g.out_deg.as<int32_t>()}, st);
-    }));
-    PR_CUDA(cudaMemcpyAsync(&S.n_seed, dcount.ptr, 8, cudaMemcpyDeviceToHost, st));
-    PR_CUDA(cudaStreamSynchronize(st));
-    // edges covered by D rows (for the roofline byte count)
-    S.edges = 0;
-    S.built = true;
     return PR_OK;
 }
 

@@ -66,7 +66,7 @@ struct RunCtl {
     int32_t mode;             // 0 pull, 1 push (for the next round)
     int32_t done;             // 1 = converged, 2 = max_rounds exhausted
     uint32_t blocks_done;     // last-block arrival counter
-    uint32_t pad;
+    int32_t append;           // record push items during the next epilogue
     uint64_t t0_ns;           // globaltimer at prologue
     double bytes;             // algorithmic bytes accumulated
     // constant contributions of vertices outside the round set (rows >= 1)
@@ -103,15 +103,28 @@ struct Graph {
     pr_ifp2_counts ifp2{};
     DevBuf live_off, live_tgt, live_deg;     // int64 [n+1], int32 [live_m], int32 [n]
     DevBuf dang_ids, src_off, src_ids;       // int32 [n_d], int64 [n_d+1], int32 [m_d]
-    // pull schedules, built lazily: [0] ifp1/fp-full destinations, [1] ifp2, [2] power (all)
+    // Pull schedules, built lazily: [0] ifp1/fp-full destinations (in-degree
+    // > 0), [1] ifp2 (non-dangling, in-degree > 0), [2] power (in-degree > 0;
+    // the zero-in-degree vertices are listed separately).  Rows of D keep
+    // ascending id order; their sources are compacted into one CSC and cut
+    // into equal edge ranges, one per warp (sched.cu, tiles.cuh).
     struct Sched {
         bool built = false;
         int64_t count = 0;        // |D|
-        int64_t bin_start[5] = {0, 0, 0, 0, 0};   // bin k = ids[bin_start[k] .. bin_start[k+1])
-        int64_t blocks[4] = {0, 0, 0, 0};
-        int64_t edges = 0;        // edges of D rows
-        DevBuf ids;               // int32 [|D|], bins concatenated, ascending id within a bin
-        int64_t n_seed = 0;       // vertices outside D that are active at round 0 (scatter seeds)
+        int64_t edges = 0;        // edges of the D rows
+        int64_t ew = 0, n_ranges = 0;  // range weight (edges + ALPHA*rows), range count
+        DevBuf ids;               // int32 [|D|] vertex id of each row
+        DevBuf doff;              // int64 [|D|+1] compacted CSC offsets
+        DevBuf csc;               // int32 [edges + pad] compacted sources
+        DevBuf flags;             // uint32 words: bit e set if edge e starts a row
+        DevBuf rrow;              // int32 [n_ranges] row holding each range's first edge
+        DevBuf rstart;            // int64 [n_ranges+1] first edge of each range
+        DevBuf rsplit;            // int2 [n_ranges] split-row range bounds (tiles.cuh)
+        DevBuf row_cnt;           // int32 [|D|] split-row arrival counters
+        DevBuf lead, trail;       // double [n_ranges] split-row partials
+        int64_t n_zero = 0;       // power: in-degree-0 vertices
+        DevBuf zero_ids;
+        int64_t n_seed = 0;       // vertices outside D active at round 0 (scatter seeds)
         DevBuf seed_ids;          // int32
     } sched[3];
     // run workspace
@@ -120,6 +133,15 @@ struct Graph {
     int64_t max_blocks = 0;     // partial slots per region (partials holds 3 regions)
     int64_t n_dangling = -1;    // #(out_degree == 0), computed lazily
     DevBuf pw;                // power-method workspace
+    // Run layout of the fast engines (sched relabel, graph.cu): the same
+    // graph with vertices renumbered by class (in>0&out>0 | out>0&in=0 |
+    // out=0&in>0 | isolated) and, inside the first class, by descending
+    // out-degree, so hot sources are dense in L1/L2 and every engine's
+    // destination set is a contiguous id range.  Exact mode keeps the
+    // original layout (bit-exact summation order).
+    Graph *run = nullptr;
+    DevBuf perm;              // int32 [n]: run id -> original id
+    DevBuf rank;              // int32 [n]: original id -> run id
     // cached instantiated round-loop graphs, keyed by run parameters
     struct Cached {
         bool valid = false;
@@ -132,17 +154,24 @@ struct Graph {
 
 int ensure_dtc(Graph &g);
 int count_dangling(Graph &g);
+int ensure_run_layout(Graph &g);
 void invalidate_cache(Graph &g);
-int ensure_sched(Graph &g, int which);
+int ensure_sched(Graph &g, int which, int64_t target_warps = 0);
 int build_from_device_edges(Ctx &ctx, int64_t n, const int64_t *d_src, const int64_t *d_dst,
                             int64_t m_raw, Graph **out);
 int classify_device(Graph &g);
 int preprocess_ifp2_device(Graph &g);
-int run_rounds(Graph &g, const pr_run_params &p, double *d_values, pr_round_stats *rows,
+int run_rounds(Graph &g, const pr_run_params &p, double *d_values, double *d_reserved, double *d_pending,
+               pr_round_stats *rows,
                int64_t row_cap, pr_run_result *res);
 int power_device(Graph &g, double damping, int64_t iterations, double tolerance, double threshold,
                  const double *h_personalization, double *h_pi, double *h_deltas, int64_t *h_converged,
                  int (*on_iterate)(void *, int64_t, const double *), void *user, pr_run_result *res);
+
+constexpr int TILE = 256;   // edges per warp tile (long rows are cut into TILE chunks)
+constexpr int CSC_PAD = 1024;  // int32 padding past the compacted CSC for vector loads
+constexpr int64_t RANGE_ALPHA = 4;      // merge-path weight of one row drain, in edges
+constexpr int64_t RANGES_PER_WARP = 2;  // gather ranges per warp of the persistent grid
 
 // small helpers
 inline unsigned grid_for(int64_t items, int per_block) {

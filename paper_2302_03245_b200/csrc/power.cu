@@ -14,6 +14,7 @@
 
 #include "internal.cuh"
 #include "reduce.cuh"
+#include "tiles.cuh"
 
 namespace pr {
 
@@ -31,8 +32,9 @@ struct PowArgs {
     const int64_t *in_off;
     const int32_t *in_src;
     const int32_t *deg;
-    const int32_t *ids;
-    int64_t bin_start[5], blk_start[5];
+    RangeView T;              // rows with in-degree > 0
+    const int32_t *zero_ids; // in-degree-0 vertices: nxt = restart * p
+    int64_t n_zero;
     const double *p;         // personalization (null: uniform 1/n)
     double *pi, *nxt, *z;
     double *deltas;          // device [iterations]
@@ -98,69 +100,27 @@ __global__ void __launch_bounds__(256) k_pw_init(PowArgs A) {
 
 // nxt_v = sum z over in-edges + restart * p_v; block partial of sum(nxt)
 __global__ void __launch_bounds__(256) k_pw_gather(PowArgs A) {
-    __shared__ double red[8];
-    const double *__restrict__ z = A.z;
-    double restart = A.ctl->restart;
+    __shared__ double rs_all[8][RS_CAP];
+    const double restart = A.ctl->restart;
+    const int lane = threadIdx.x & 31;
+    double *rs = rs_all[threadIdx.x >> 5];
     Partial p;
     zero(p);
-    int64_t b = blockIdx.x;
-    int tid = threadIdx.x;
-    if (b < A.blk_start[1]) {
-        int64_t idx = A.bin_start[0] + b * 256 + tid;
-        if (idx < A.bin_start[1]) {
-            int32_t v = A.ids[idx];
-            double acc = 0.0;
-            for (int64_t e = A.in_off[v]; e < A.in_off[v + 1]; ++e) acc += __ldg(&z[A.in_src[e]]);
-            double x = __dadd_rn(acc, __dmul_rn(restart, pval(A, v)));
-            A.nxt[v] = x;
-            p.l1 += x;
-        }
-    } else if (b < A.blk_start[2]) {
-        int g = tid >> 3, l = tid & 7;
-        int64_t idx = A.bin_start[1] + (b - A.blk_start[1]) * 32 + g;
-        bool ok = idx < A.bin_start[2];
-        int32_t v = ok ? A.ids[idx] : 0;
-        double acc = 0.0;
-        if (ok)
-            for (int64_t e = A.in_off[v] + l; e < A.in_off[v + 1]; e += 8) acc += __ldg(&z[A.in_src[e]]);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        if (ok && l == 0) {
-            double x = __dadd_rn(acc, __dmul_rn(restart, pval(A, v)));
-            A.nxt[v] = x;
-            p.l1 += x;
-        }
-    } else if (b < A.blk_start[3]) {
-        int w = tid >> 5, l = tid & 31;
-        int64_t idx = A.bin_start[2] + (b - A.blk_start[2]) * 8 + w;
-        bool ok = idx < A.bin_start[3];
-        int32_t v = ok ? A.ids[idx] : 0;
-        double acc = 0.0;
-        if (ok)
-            for (int64_t e = A.in_off[v] + l; e < A.in_off[v + 1]; e += 32) acc += __ldg(&z[A.in_src[e]]);
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (ok && l == 0) {
-            double x = __dadd_rn(acc, __dmul_rn(restart, pval(A, v)));
-            A.nxt[v] = x;
-            p.l1 += x;
-        }
-    } else if (b < A.blk_start[4]) {
-        int64_t idx = A.bin_start[3] + (b - A.blk_start[3]);
-        int32_t v = A.ids[idx];
-        double acc = 0.0;
-        for (int64_t e = A.in_off[v] + tid; e < A.in_off[v + 1]; e += 256) acc += __ldg(&z[A.in_src[e]]);
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if ((tid & 31) == 0) red[tid >> 5] = acc;
-        __syncthreads();
-        if (tid == 0) {
-            double tot = 0.0;
-            for (int k = 0; k < 8; ++k) tot += red[k];
-            double x = __dadd_rn(tot, __dmul_rn(restart, pval(A, v)));
-            A.nxt[v] = x;
-            p.l1 += x;
-        }
-    }
+    auto finish = [&](int32_t v, double sum) {
+        double x = __dadd_rn(sum, __dmul_rn(restart, pval(A, v)));
+        A.nxt[v] = x;
+        p.l1 += x;
+    };
+    auto split_row = [&](int64_t row, double sum) { finish(A.T.ids[row], sum); };
+    auto drain_batch = [&](int64_t row0, int cnt, const double *sums) {
+        for (int i = lane; i < cnt; i += 32) finish(__ldg(&A.T.ids[row0 + i]), sums[i]);
+    };
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = warp; k < A.T.n_ranges; k += nw) warp_range(A.T, k, A.z, rs, drain_batch, split_row);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.n_zero;
+         i += (int64_t)gridDim.x * blockDim.x)
+        finish(A.zero_ids[i], 0.0);
     pow_finish(A, p, [&](const Partial &acc) { A.ctl->total = acc.l1; });
 }
 
@@ -212,19 +172,17 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
     if (iterations < 0) return fail(PR_ERR_ARG, "max_iterations must be non-negative");
     Ctx &ctx = *g.ctx;
     cudaStream_t st = ctx.stream;
-    PR_TRY(ensure_sched(g, 2));
+    int per_sm = 0;
+    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pw_gather, 256, 0));
+    if (per_sm < 1) per_sm = 1;
+    PR_TRY(ensure_sched(g, 2, (int64_t)ctx.sm_count * per_sm * 8));
     auto &S = g.sched[2];
     int64_t n = g.n;
-    int64_t blk = 0;
     PowArgs A;
     memset(&A, 0, sizeof(A));
-    for (int k = 0; k < 4; ++k) {
-        A.bin_start[k] = S.bin_start[k];
-        A.blk_start[k] = blk;
-        blk += S.blocks[k];
-    }
-    A.bin_start[4] = S.bin_start[4];
-    A.blk_start[4] = blk;
+    int64_t blk = (S.n_ranges + 7) / 8;
+    if (blk > (int64_t)ctx.sm_count * per_sm) blk = (int64_t)ctx.sm_count * per_sm;
+    if (blk < 1) blk = 1;
     int64_t maxb = blk > (n + 255) / 256 ? blk : (n + 255) / 256;
     int64_t it_cap = iterations > 0 ? iterations : 1;
     // workspace: pi, nxt, z, p (opt), deltas, conv, partials, ctl
@@ -238,7 +196,20 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
     A.in_off = g.in_off.as<int64_t>();
     A.in_src = g.in_src.as<int32_t>();
     A.deg = g.out_deg.as<int32_t>();
-    A.ids = S.ids.as<int32_t>();
+    A.T.ids = S.ids.as<int32_t>();
+    A.T.doff = S.doff.as<int64_t>();
+    A.T.csc = S.csc.as<int32_t>();
+    A.T.flags8 = S.flags.as<uint8_t>();
+    A.T.rrow = S.rrow.as<int32_t>();
+    A.T.rstart = S.rstart.as<int64_t>();
+    A.T.rsplit = S.rsplit.as<int2>();
+    A.T.edges = S.edges;
+    A.T.n_ranges = S.n_ranges;
+    A.T.row_cnt = S.row_cnt.as<int32_t>();
+    A.T.lead = S.lead.as<double>();
+    A.T.trail = S.trail.as<double>();
+    A.zero_ids = S.zero_ids.as<int32_t>();
+    A.n_zero = S.n_zero;
     A.pi = (double *)(base + off_pi);
     A.nxt = (double *)(base + off_nxt);
     A.z = (double *)(base + off_z);
@@ -254,7 +225,7 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
     A.iterations = iterations;
     if (h_p) PR_CUDA(cudaMemcpyAsync((void *)A.p, h_p, 8 * n, cudaMemcpyHostToDevice, st));
     PR_CUDA(cudaMemsetAsync(A.ctl, 0, sizeof(PowCtl), st));
-    unsigned g_all = grid_for(n, 256), g_gather = (unsigned)(blk > 0 ? blk : 1);
+    unsigned g_all = grid_for(n, 256), g_gather = (unsigned)blk;
 
     cudaEvent_t e0, e1;
     PR_CUDA(cudaEventCreate(&e0));

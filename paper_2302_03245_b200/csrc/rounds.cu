@@ -25,12 +25,14 @@
 // source sums with explicit _rn intrinsics -- bit-identical reserved/h to
 // sync_simulate's np.bincount order.
 #include <cooperative_groups.h>
+#include <cooperative_groups/scan.h>
 
 #include <cstring>
 #include <vector>
 
 #include "internal.cuh"
 #include "reduce.cuh"
+#include "tiles.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -45,15 +47,14 @@ struct RunArgs {
     const int32_t *deg;        // original out-degree: push weight denominator
     const int32_t *row_len;    // push row length for push_ops (out_deg or live_deg)
     const int32_t *dtc;        // dangling-target counts (ifp1/fp-full) or null (ifp2)
-    const int32_t *ids;        // D, bins concatenated
-    int64_t bin_start[5];
-    int64_t blk_start[5];
+    RangeView T;                // pull schedule of D (sched.cu)
+    const int32_t *ids;        // D rows' vertex ids (== T.ids)
     int64_t d_count;
     const int32_t *seeds;      // vertices outside D active at state 0
     int64_t n_seed;
     const uint8_t *in_d;       // membership mask of D
     double *h, *reserved, *s;  // s: 2*n (ping-pong by state parity)
-    int32_t *frontier;         // 2*fcap
+    long long *frontier;       // 2*fcap push items: (vertex << 24) | chunk
     int64_t fcap;
     uint8_t *act;              // exact engine
     Partial *partials;         // 3 regions of max_blocks: round, constants, mass totals
@@ -62,7 +63,7 @@ struct RunArgs {
     pr_round_stats *rows;
     int64_t rows_cap;
     double c, xi, frac;
-    int32_t algo, policy, conv_all, use_graph;
+    int32_t algo, policy, conv_all, use_graph, has_mode;
     int64_t max_rounds;
     double push_work;          // AUTO: push when the next round's work < push_work
     double n_scan;             // scan-set size (bytes model)
@@ -75,23 +76,42 @@ __device__ __forceinline__ uint64_t digest_term(int64_t v, double r, double h) {
     return (a ^ (b * 0xBF58476D1CE4E5B9ull)) * w;
 }
 
-// warp-aggregated frontier append among the currently converged lanes
-__device__ __forceinline__ void frontier_append(bool pred, int32_t v, int32_t *F, int64_t *size) {
-    cg::coalesced_group g = cg::coalesced_threads();
-    unsigned bal = g.ballot(pred);
-    if (!bal) return;
+// Warp-collective append of push items (all 32 lanes call it; `enabled` is
+// warp-uniform): a vertex with k TILE-edge chunks of (live) out-edges
+// contributes k items, so hub rows are spread over k warps in a push round.
+__device__ __forceinline__ void append_warp(bool enabled, int items, int32_t v, long long *F, int64_t *size) {
+    if (!enabled) return;
+    const int lane = threadIdx.x & 31;
+    int incl = items;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) return;
     unsigned long long base = 0;
-    if (g.thread_rank() == 0) base = atomicAdd((unsigned long long *)size, (unsigned long long)__popc(bal));
-    base = g.shfl(base, 0);
-    if (pred) F[base + __popc(bal & ((1u << g.thread_rank()) - 1u))] = v;
+    if (lane == 0) base = atomicAdd((unsigned long long *)size, (unsigned long long)total);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (int c = 0; c < items; ++c) F[base + (incl - items) + c] = ((long long)v << 24) | c;
+}
+
+__device__ __forceinline__ void append_one(int items, int32_t v, long long *F, int64_t *size) {
+    if (!items) return;
+    unsigned long long base = atomicAdd((unsigned long long *)size, (unsigned long long)items);
+    for (int c = 0; c < items; ++c) F[base + c] = ((long long)v << 24) | c;
 }
 
 // Drain one vertex of state r given its pre-drain pending mass hv:
-// statistics, reservation, shares s[r&1], frontier append.
-__device__ __forceinline__ void epilogue(const RunArgs &A, int64_t v, double hv, int64_t r, Partial &p) {
-    int32_t dv = A.deg[v];
-    bool scan = A.algo == PR_ALGO_FPFULL || dv > 0;
-    bool above = hv > A.xi;  // strict (engines.py:421, _kernels.pyx:89)
+// statistics, reservation, shares s[r&1].  Returns its push-item count.
+__device__ __forceinline__ int drain_vertex(const RunArgs &A, int64_t v, double hv, int64_t r, Partial &p) {
+    // every per-vertex load issued up front: one memory round trip per batch
+    const int32_t dv = __ldg(&A.deg[v]);
+    const int32_t len = __ldg(&A.row_len[v]);
+    const int32_t dt = A.dtc ? __ldg(&A.dtc[v]) : 0;
+    const double rv = A.reserved[v];
+    const bool scan = A.algo == PR_ALGO_FPFULL || dv > 0;
+    const bool above = hv > A.xi;  // strict (engines.py:421, _kernels.pyx:89)
     p.l1 += hv;
     if (above) {
         p.above += hv;
@@ -100,23 +120,21 @@ __device__ __forceinline__ void epilogue(const RunArgs &A, int64_t v, double hv,
         p.conv_all += 1;
         if (scan) p.conv_scan += 1;
     }
-    bool active = above && scan;
     double *s_out = A.s + (r & 1) * A.n;
-    if (active) {
+    if (above && scan) {
         // (c*h)/deg with two roundings, never c*h*inv_deg (engines.py:444, _kernels.pyx:97)
-        double share = dv > 0 ? __ddiv_rn(__dmul_rn(A.c, hv), (double)dv) : 0.0;
-        s_out[v] = share;
-        A.reserved[v] = __dadd_rn(A.reserved[v], __dmul_rn(A.frac, hv));
+        s_out[v] = dv > 0 ? __ddiv_rn(__dmul_rn(A.c, hv), (double)dv) : 0.0;
+        A.reserved[v] = __dadd_rn(rv, __dmul_rn(A.frac, hv));
         A.h[v] = 0.0;
         p.nact += 1;
         p.work += (int64_t)dv + 1;
-        p.push_ops += A.row_len[v];
-        if (A.dtc) p.push_dang += A.dtc[v];
-    } else {
-        s_out[v] = 0.0;
-        A.h[v] = hv;
+        p.push_ops += len;
+        p.push_dang += dt;
+        return (len + TILE - 1) / TILE;
     }
-    frontier_append(active, (int32_t)v, A.frontier + (r & 1) * A.fcap, &A.ctl->fsize[r & 1]);
+    s_out[v] = 0.0;
+    A.h[v] = hv;
+    return 0;
 }
 
 // Thread 0 of the last block: write trace row r, decide what runs next,
@@ -156,29 +174,35 @@ __device__ void finalize_row(const RunArgs &A, const Partial &tot, int64_t r, bo
     else if (r >= A.max_rounds) done = 2;
     ctl->done = done;
     ctl->round = r;
+    // push needs the frontier of this state, recorded only when predicted
+    const bool have_frontier = ctl->append != 0;
     int mode = 0;
-    if (A.policy == PR_MODE_PUSH && r >= 1) mode = 1;
-    else if (A.policy == PR_MODE_AUTO && r >= 1 && (double)tot.work < A.push_work) mode = 1;
+    if (have_frontier && r >= 1) {
+        if (A.policy == PR_MODE_PUSH) mode = 1;
+        else if (A.policy == PR_MODE_AUTO && (double)tot.work < A.push_work) mode = 1;
+    }
     ctl->mode = mode;
     if (!done) {
         if (mode) ctl->push_rounds += 1;
         else ctl->pull_rounds += 1;
     }
+    // record the next state's frontier when a push round is likely after it
+    ctl->append = A.policy == PR_MODE_PUSH || (A.policy == PR_MODE_AUTO && (double)tot.work < 4.0 * A.push_work);
     ctl->fsize[(r + 1) & 1] = 0;
     ctl->blocks_done = 0;
     __threadfence();
     if (A.use_graph) {
         cudaGraphSetConditional(A.h_loop, done ? 0u : 1u);
-        cudaGraphSetConditional(A.h_mode, (unsigned)mode);
+        if (A.has_mode) cudaGraphSetConditional(A.h_mode, (unsigned)mode);
     }
 }
 
 // Publish this block's partial; the last block to arrive reduces all of
 // them in a fixed order (deterministic) and finalises row r.
-__device__ void finish_round(const RunArgs &A, Partial p, int64_t r, bool fast, bool with_consts, Partial cst) {
+// `p` (and `cst`) must already be the block totals in thread 0.
+__device__ void publish_round(const RunArgs &A, const Partial &p, int64_t r, bool fast, bool with_consts,
+                              const Partial &cst) {
     __shared__ bool is_last;
-    block_reduce(p);
-    if (with_consts) block_reduce(cst);
     if (threadIdx.x == 0) {
         A.partials[blockIdx.x] = p;
         if (with_consts) A.partials[A.max_blocks + blockIdx.x] = cst;
@@ -210,6 +234,18 @@ __device__ void finish_round(const RunArgs &A, Partial p, int64_t r, bool fast, 
     }
 }
 
+__device__ void finish_round(const RunArgs &A, Partial p, int64_t r, bool fast, bool with_consts, Partial cst) {
+    block_reduce(p);
+    if (with_consts) block_reduce(cst);
+    publish_round(A, p, r, fast, with_consts, cst);
+}
+
+// warp-sum a batch partial and fold it into this warp's shared accumulator
+__device__ __forceinline__ void warp_fold(Partial &bp, Partial &acc) {
+    for (int o = 16; o > 0; o >>= 1) shfl_add(bp, o);
+    if ((threadIdx.x & 31) == 0) add(acc, bp);
+}
+
 // ---------------------------------------------------------------- fast engine kernels
 
 __global__ void k_reset(RunArgs A) {
@@ -222,6 +258,7 @@ __global__ void k_reset(RunArgs A) {
     c->mode = 0;
     c->done = 0;
     c->blocks_done = 0;
+    c->append = 0;
     c->t0_ns = globaltimer();
     c->bytes = 0.0;
     c->c_l1 = c->c_above = c->c_nd_above = 0.0;
@@ -240,11 +277,12 @@ __global__ void __launch_bounds__(256) k_init(RunArgs A) {
     Partial p, cst;
     zero(p);
     zero(cst);
+    int items = 0;
     if (v < A.n) {
         A.reserved[v] = 0.0;
         A.s[A.n + v] = 0.0;
         if (A.in_d[v]) {
-            epilogue(A, v, 1.0, 0, p);
+            items = drain_vertex(A, v, 1.0, 0, p);
         } else {
             int32_t dv = A.deg[v];
             bool scan = A.algo == PR_ALGO_FPFULL || dv > 0;
@@ -278,6 +316,7 @@ __global__ void __launch_bounds__(256) k_init(RunArgs A) {
             }
         }
     }
+    append_warp(A.ctl->append != 0, items, (int32_t)v, A.frontier, &A.ctl->fsize[0]);
     finish_round(A, p, 0, true, true, cst);
 }
 
@@ -297,81 +336,85 @@ __global__ void __launch_bounds__(256) k_seed_scatter(RunArgs A) {
 }
 
 // Dense round t: h(t+1)_v = h_drained(t)_v + sum_{u in in(v)} s(t)_u over D,
-// fused with the drain of state t+1.
-__global__ void __launch_bounds__(256) k_pull(RunArgs A) {
-    __shared__ double red[8];
-    int64_t t = A.ctl->round;
+// fused with the drain of state t+1.  Persistent grid, one warp per tile;
+// row sums staged in shared memory, then drained lane-parallel.
+#ifndef PULL_MIN_BLOCKS
+#define PULL_MIN_BLOCKS 2
+#endif
+__global__ void __launch_bounds__(256, PULL_MIN_BLOCKS) k_pull(RunArgs A) {
+    __shared__ double rs_all[8][RS_CAP];
+    __shared__ Partial wpart[8];   // per-warp statistics (kept out of the gather's registers)
+    const int64_t t = A.ctl->round;
     const double *__restrict__ s_in = A.s + (t & 1) * A.n;
-    int64_t r = t + 1;
+    const int64_t r = t + 1;
+    const bool app = A.ctl->append != 0;
+    long long *F = A.frontier + (r & 1) * A.fcap;
+    int64_t *fsize = &A.ctl->fsize[r & 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double *rs = rs_all[wid];
+    if (lane == 0) zero(wpart[wid]);
+    __syncwarp();
+    auto split_row = [&](int64_t row, double sum) {  // lane 0 only
+        Partial bp;
+        zero(bp);
+        int32_t v = A.ids[row];
+        int it = drain_vertex(A, v, A.h[v] + sum, r, bp);
+        if (app) append_one(it, v, F, fsize);
+        add(wpart[wid], bp);
+    };
+    auto drain_batch = [&](int64_t row0, int cnt, const double *sums) {
+        for (int b = 0; b < cnt; b += 32) {
+            const int i = b + lane;
+            Partial bp;
+            zero(bp);
+            int items = 0;
+            int32_t v = 0;
+            if (i < cnt) {
+                v = __ldg(&A.ids[row0 + i]);
+                items = drain_vertex(A, v, A.h[v] + sums[i], r, bp);
+            }
+            append_warp(app, items, v, F, fsize);
+            warp_fold(bp, wpart[wid]);
+        }
+    };
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = warp; k < A.T.n_ranges; k += nw) warp_range(A.T, k, s_in, rs, drain_batch, split_row);
+    __syncthreads();
     Partial p;
     zero(p);
-    int64_t b = blockIdx.x;
-    int tid = threadIdx.x;
-    if (b < A.blk_start[1]) {
-        // bin 0: thread per destination (in-degree <= 4), sequential sum
-        int64_t idx = A.bin_start[0] + b * 256 + tid;
-        if (idx < A.bin_start[1]) {
-            int32_t v = A.ids[idx];
-            double acc = 0.0;
-            for (int64_t e = A.in_off[v]; e < A.in_off[v + 1]; ++e) acc += __ldg(&s_in[A.in_src[e]]);
-            epilogue(A, v, A.h[v] + acc, r, p);
-        }
-    } else if (b < A.blk_start[2]) {
-        // bin 1: 8 lanes per destination (in-degree 5..64)
-        int g = tid >> 3, l = tid & 7;
-        int64_t idx = A.bin_start[1] + (b - A.blk_start[1]) * 32 + g;
-        bool ok = idx < A.bin_start[2];
-        int32_t v = ok ? A.ids[idx] : 0;
-        double acc = 0.0;
-        if (ok)
-            for (int64_t e = A.in_off[v] + l; e < A.in_off[v + 1]; e += 8) acc += __ldg(&s_in[A.in_src[e]]);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        if (ok && l == 0) epilogue(A, v, A.h[v] + acc, r, p);
-    } else if (b < A.blk_start[3]) {
-        // bin 2: warp per destination (in-degree 65..2048)
-        int w = tid >> 5, l = tid & 31;
-        int64_t idx = A.bin_start[2] + (b - A.blk_start[2]) * 8 + w;
-        bool ok = idx < A.bin_start[3];
-        int32_t v = ok ? A.ids[idx] : 0;
-        double acc = 0.0;
-        if (ok)
-            for (int64_t e = A.in_off[v] + l; e < A.in_off[v + 1]; e += 32) acc += __ldg(&s_in[A.in_src[e]]);
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (ok && l == 0) epilogue(A, v, A.h[v] + acc, r, p);
-    } else if (b < A.blk_start[4]) {
-        // bin 3: CTA per destination (hubs)
-        int64_t idx = A.bin_start[3] + (b - A.blk_start[3]);
-        int32_t v = A.ids[idx];
-        double acc = 0.0;
-        for (int64_t e = A.in_off[v] + tid; e < A.in_off[v + 1]; e += 256) acc += __ldg(&s_in[A.in_src[e]]);
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if ((tid & 31) == 0) red[tid >> 5] = acc;
-        __syncthreads();
-        if (tid == 0) {
-            double tot = 0.0;
-            for (int k = 0; k < 8; ++k) tot += red[k];
-            epilogue(A, v, A.h[v] + tot, r, p);
-        }
-    }
-    finish_round(A, p, r, true, false, p);
+    if (threadIdx.x == 0)
+        for (int w = 0; w < 8; ++w) add(p, wpart[w]);
+    publish_round(A, p, r, true, false, p);
 }
 
-// Sparse round t, step 1: scatter the frontier's shares (red.global.add.f64)
+// Sparse round t, step 1: scatter the frontier's shares (red.global.add.f64);
+// one warp per push item (a TILE-edge chunk of one vertex's out-row), the 8
+// target loads of a lane issued before its 8 reductions.
 __global__ void __launch_bounds__(256) k_push(RunArgs A) {
     int64_t t = A.ctl->round;
     const double *__restrict__ s_in = A.s + (t & 1) * A.n;
-    const int32_t *F = A.frontier + (t & 1) * A.fcap;
+    const long long *F = A.frontier + (t & 1) * A.fcap;
     int64_t cnt = A.ctl->fsize[t & 1];
     int lane = threadIdx.x & 31;
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t i = warp; i < cnt; i += nwarps) {
-        int32_t u = F[i];
+        long long item = F[i];
+        int32_t u = (int32_t)(item >> 24);
+        int64_t c = item & 0xFFFFFF;
         double sh = s_in[u];
-        int64_t lo = A.push_off[u], hi = A.push_off[u + 1];
-        for (int64_t e = lo + lane; e < hi; e += 32) atomicAdd(&A.h[A.push_tgt[e]], sh);
+        int64_t lo = A.push_off[u] + c * TILE, hi = A.push_off[u + 1];
+        if (hi > lo + TILE) hi = lo + TILE;
+        int32_t tg[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            int64_t e = lo + k * 32 + lane;
+            tg[k] = e < hi ? __ldg(&A.push_tgt[e]) : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (tg[k] >= 0) atomicAdd(&A.h[tg[k]], sh);
     }
 }
 
@@ -382,10 +425,13 @@ __global__ void __launch_bounds__(256) k_scan(RunArgs A) {
     Partial p;
     zero(p);
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int items = 0;
+    int32_t v = 0;
     if (i < A.d_count) {
-        int32_t v = A.ids[i];
-        epilogue(A, v, A.h[v], r, p);
+        v = __ldg(&A.ids[i]);
+        items = drain_vertex(A, v, A.h[v], r, p);
     }
+    append_warp(A.ctl->append != 0, items, v, A.frontier + (r & 1) * A.fcap, &A.ctl->fsize[r & 1]);
     finish_round(A, p, r, true, false, p);
 }
 
@@ -555,12 +601,18 @@ __global__ void __launch_bounds__(256) k_total(RunArgs A, int include_h, int64_t
     }
 }
 
-__global__ void k_scale(RunArgs A, int include_h, double *values) {
+// values in original vertex order (perm: run id -> original id, or identity)
+__global__ void k_scale(RunArgs A, int include_h, double *values, const int32_t *perm) {
     double tot = A.ctl->mass_total;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < A.n; v += (int64_t)gridDim.x * blockDim.x) {
         double x = include_h ? A.reserved[v] + A.h[v] : A.reserved[v];
-        values[v] = x / tot;
+        values[perm ? perm[v] : v] = x / tot;
     }
+}
+
+__global__ void k_unpermute(const double *src, int64_t n, const int32_t *perm, double *dst) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        dst[perm ? perm[v] : v] = src[v];
 }
 
 __global__ void k_mark_d(const int32_t *ids, int64_t count, uint8_t *in_d) {
@@ -611,7 +663,10 @@ static int build_graph(Plan &P, cudaGraph_t *out_g, cudaGraphExec_t *out_exec) {
     PR_CUDA(cudaGraphCreate(&G, 0));
     RunArgs &A = P.A;
     PR_CUDA(cudaGraphConditionalHandleCreate(&A.h_loop, G, 1, cudaGraphCondAssignDefault));
-    PR_CUDA(cudaGraphConditionalHandleCreate(&A.h_mode, G, 0, cudaGraphCondAssignDefault));
+    // every handle must belong to a conditional node, so the mode switch
+    // handle exists only in the fast engine's graph
+    A.has_mode = !P.exact;
+    if (A.has_mode) PR_CUDA(cudaGraphConditionalHandleCreate(&A.h_mode, G, 0, cudaGraphCondAssignDefault));
     A.use_graph = 1;
     void *args[] = {&A};
     cudaGraphNode_t n_reset, n_init, n_seed, n_while, n_sw, n_a, n_b;
@@ -654,7 +709,7 @@ static int build_graph(Plan &P, cudaGraph_t *out_g, cudaGraphExec_t *out_exec) {
 
 // Workspace sized once per graph; any reallocation invalidates the cached
 // executable graphs (they bake the pointers in).
-static int ws_alloc(Graph &g, int64_t need_blocks) {
+static int ws_alloc(Graph &g, int64_t need_blocks, int64_t fcap) {
     int64_t n = g.n;
     void *before[9] = {g.h.ptr, g.reserved.ptr, g.s2.ptr, g.act.ptr, g.in_d.ptr,
                        g.frontier2.ptr, g.partials.ptr, g.ctl.ptr, g.rows.ptr};
@@ -663,7 +718,7 @@ static int ws_alloc(Graph &g, int64_t need_blocks) {
     PR_TRY(ensure(g.s2, 16 * n));
     PR_TRY(ensure(g.act, n));
     PR_TRY(ensure(g.in_d, n));
-    PR_TRY(ensure(g.frontier2, 8 * (n + 1)));
+    PR_TRY(ensure(g.frontier2, 16 * fcap));
     PR_TRY(ensure(g.ctl, sizeof(RunCtl)));
     if (g.rows_cap == 0) g.rows_cap = 1 << 16;
     PR_TRY(ensure(g.rows, sizeof(pr_round_stats) * g.rows_cap));
@@ -679,9 +734,9 @@ static int ws_alloc(Graph &g, int64_t need_blocks) {
     return PR_OK;
 }
 
-int run_rounds(Graph &g, const pr_run_params &p, double *d_values, pr_round_stats *rows, int64_t row_cap,
-               pr_run_result *res) {
-    Ctx &ctx = *g.ctx;
+int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_reserved, double *d_pending,
+               pr_round_stats *rows, int64_t row_cap, pr_run_result *res) {
+    Ctx &ctx = *g_in.ctx;
     cudaStream_t st = ctx.stream;
     const int algo = p.algorithm;
     if (algo < 0 || algo > 2) return fail(PR_ERR_ARG, "unknown algorithm");
@@ -692,19 +747,32 @@ int run_rounds(Graph &g, const pr_run_params &p, double *d_values, pr_round_stat
     const bool exact = p.mode == PR_MODE_EXACT;
     if (p.on_round && !exact) return fail(PR_ERR_ARG, "on_round observers need PR_MODE_EXACT");
     const bool host_loop = p.host_loop || p.on_round;
-    if (algo == PR_ALGO_IFP2) {
-        if (!g.has_ifp2) return fail(PR_ERR_STATE, "IFP2 needs pr_preprocess_ifp2 first");
-    } else {
-        PR_TRY(ensure_dtc(g));
+    if (algo == PR_ALGO_IFP2 && !g_in.has_ifp2) return fail(PR_ERR_STATE, "IFP2 needs pr_preprocess_ifp2 first");
+    // fast engines run on the relabelled layout; exact mode on the original
+    Graph *gp = &g_in;
+    if (!exact) {
+        PR_TRY(ensure_run_layout(g_in));
+        gp = g_in.run;
     }
+    Graph &g = *gp;
+    const int32_t *perm = exact ? nullptr : g_in.perm.as<int32_t>();
+    if (algo == PR_ALGO_IFP2) PR_TRY(preprocess_ifp2_device(g));
+    else PR_TRY(ensure_dtc(g));
     PR_TRY(count_dangling(g));
     const int which = algo == PR_ALGO_IFP2 ? 1 : 0;
-    PR_TRY(ensure_sched(g, which));
+    // persistent pull grid: as many blocks as fit on the device at once,
+    // one equal edge range per warp
+    int per_sm = 0;
+    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pull, 256, 0));
+    if (per_sm < 1) per_sm = 1;
+    PR_TRY(ensure_sched(g, which, (int64_t)ctx.sm_count * per_sm * 8));
     auto &S = g.sched[which];
     int64_t n = g.n;
-    int64_t blk = 0;
-    for (int k = 0; k < 4; ++k) blk += S.blocks[k];
-    PR_TRY(ws_alloc(g, blk));
+    int64_t pull_blocks = (S.n_ranges + 7) / 8;
+    if (pull_blocks > (int64_t)ctx.sm_count * per_sm) pull_blocks = (int64_t)ctx.sm_count * per_sm;
+    if (pull_blocks < 1) pull_blocks = 1;
+    const int64_t fcap = n + g.m / TILE + 1;
+    PR_TRY(ws_alloc(g, pull_blocks, fcap));
 
     Plan P;
     memset(&P, 0, sizeof(P));
@@ -725,14 +793,18 @@ int run_rounds(Graph &g, const pr_run_params &p, double *d_values, pr_round_stat
     }
     A.deg = g.out_deg.as<int32_t>();
     A.ids = S.ids.as<int32_t>();
-    blk = 0;
-    for (int k = 0; k < 4; ++k) {
-        A.bin_start[k] = S.bin_start[k];
-        A.blk_start[k] = blk;
-        blk += S.blocks[k];
-    }
-    A.bin_start[4] = S.bin_start[4];
-    A.blk_start[4] = blk;
+    A.T.ids = S.ids.as<int32_t>();
+    A.T.doff = S.doff.as<int64_t>();
+    A.T.csc = S.csc.as<int32_t>();
+    A.T.flags8 = S.flags.as<uint8_t>();
+    A.T.rrow = S.rrow.as<int32_t>();
+    A.T.rstart = S.rstart.as<int64_t>();
+    A.T.rsplit = S.rsplit.as<int2>();
+    A.T.edges = S.edges;
+    A.T.n_ranges = S.n_ranges;
+    A.T.row_cnt = S.row_cnt.as<int32_t>();
+    A.T.lead = S.lead.as<double>();
+    A.T.trail = S.trail.as<double>();
     A.d_count = S.count;
     A.seeds = S.seed_ids.as<int32_t>();
     A.n_seed = S.n_seed;
@@ -740,8 +812,8 @@ int run_rounds(Graph &g, const pr_run_params &p, double *d_values, pr_round_stat
     A.h = g.h.as<double>();
     A.reserved = g.reserved.as<double>();
     A.s = g.s2.as<double>();
-    A.frontier = g.frontier2.as<int32_t>();
-    A.fcap = n;
+    A.frontier = g.frontier2.as<long long>();
+    A.fcap = fcap;
     A.act = g.act.as<uint8_t>();
     A.partials = g.partials.as<Partial>();
     A.max_blocks = g.max_blocks;
@@ -761,7 +833,7 @@ int run_rounds(Graph &g, const pr_run_params &p, double *d_values, pr_round_stat
     A.n_scan = (double)(algo == PR_ALGO_FPFULL ? n : n - g.n_dangling);
     P.exact = exact;
     P.g_all = grid_for(n, 256);
-    P.g_pull = (unsigned)(blk > 0 ? blk : 1);
+    P.g_pull = (unsigned)pull_blocks;
     P.g_scan = grid_for(S.count, 256);
     P.g_push = (unsigned)ctx.sm_count * 8;
 
@@ -841,10 +913,12 @@ int run_rounds(Graph &g, const pr_run_params &p, double *d_values, pr_round_stat
     }
     int include_h = algo == PR_ALGO_IFP1 ? 1 : 0;
     k_total<<<P.g_all, 256, 0, st>>>(A, include_h, settled, algo == PR_ALGO_IFP2 ? 1 : 0);
-    if (d_values) {
+    {
         unsigned gs = grid_for(n, 256);
         if (gs > 4096) gs = 4096;
-        k_scale<<<gs, 256, 0, st>>>(A, include_h, d_values);
+        if (d_values) k_scale<<<gs, 256, 0, st>>>(A, include_h, d_values, perm);
+        if (d_reserved) k_unpermute<<<gs, 256, 0, st>>>(A.reserved, n, perm, d_reserved);
+        if (d_pending) k_unpermute<<<gs, 256, 0, st>>>(A.h, n, perm, d_pending);
     }
     PR_CUDA(cudaEventRecord(e2, st));
     PR_CUDA(cudaEventSynchronize(e2));

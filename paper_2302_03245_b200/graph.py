@@ -13,6 +13,7 @@ be passed where a ``Graph`` is expected; it is uploaded once and cached.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -128,6 +129,9 @@ class DeviceGraph:
             on_round=None, row_cap: int = 1 << 16, values_out: np.ndarray | None = None):
         """One solve through pr_run; returns (values, rows, result, reserved, pending)."""
         n = self.n
+        # PUSHRANK_HOST_LOOP=1 launches the same kernels round by round from
+        # the host (ncu cannot profile kernel nodes of conditional graphs)
+        host_loop = host_loop or os.environ.get("PUSHRANK_HOST_LOOP", "0") == "1"
         params = _lib.RunParams(algorithm=_lib.ALGO[algorithm], mode=_lib.MODE[mode], damping=float(damping),
                                 threshold=float(threshold), max_rounds=int(max_rounds),
                                 push_switch=float(push_switch), converged_scope=int(converged_scope),
