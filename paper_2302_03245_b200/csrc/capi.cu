@@ -1,4 +1,7 @@
 // capi.cu -- extern "C" boundary of libpushrank_cuda (include/pushrank_cuda.h).
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -7,6 +10,20 @@
 namespace pr {
 
 static thread_local std::string g_last_error;
+
+void phase_mark(cudaStream_t st, const char *what) {
+    static const bool on = [] {
+        const char *e = getenv("PUSHRANK_TIMING");
+        return e && e[0] == '1';
+    }();
+    if (!on) return;
+    static thread_local std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+    cudaStreamSynchronize(st);
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[pushrank] %-28s %9.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+}
 
 void set_error(const std::string &msg) { g_last_error = msg; }
 
@@ -27,6 +44,7 @@ int export_i64(Ctx &ctx, const DevBuf &src, int64_t count, int64_t *host);
 
 static int set_device(Ctx &ctx) {
     PR_CUDA(cudaSetDevice(ctx.device));
+    alloc_stream() = ctx.stream;
     return PR_OK;
 }
 
@@ -76,6 +94,14 @@ int pr_ctx_create(int device, pr_ctx **out) {
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) {
+        // keep freed pool memory cached: graph builds reuse it without driver calls
+        cudaMemPool_t pool;
+        e = cudaDeviceGetDefaultMemPool(&pool, device);
+        uint64_t keep = UINT64_MAX;
+        if (e == cudaSuccess) e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    alloc_stream() = c->c.stream;
+    if (e == cudaSuccess) {
         cudaDeviceProp prop;
         e = cudaGetDeviceProperties(&prop, device);
         if (e == cudaSuccess) {
@@ -101,6 +127,7 @@ int pr_ctx_create(int device, pr_ctx **out) {
 int pr_ctx_destroy(pr_ctx *ctx) {
     if (!ctx) return PR_OK;
     cudaSetDevice(ctx->c.device);
+    alloc_stream() = ctx->c.stream;
     cudaStreamSynchronize(ctx->c.stream);
     ctx->c.scratch.release();
     ctx->c.flush.release();
@@ -169,6 +196,7 @@ int pr_graph_upload(pr_ctx *ctx, int64_t n, int64_t m, const int64_t *out_offset
 int pr_graph_destroy(pr_graph *g) {
     if (!g) return PR_OK;
     cudaSetDevice(g->g->ctx->device);
+    alloc_stream() = g->g->ctx->stream;
     cudaStreamSynchronize(g->g->ctx->stream);
     delete g->g;
     delete g;

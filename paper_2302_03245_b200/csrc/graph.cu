@@ -13,15 +13,20 @@
 
 namespace pr {
 
+cudaStream_t &alloc_stream() {
+    static thread_local cudaStream_t s = nullptr;
+    return s;
+}
+
 int ensure(DevBuf &b, size_t bytes) {
     if (bytes == 0) bytes = 16;
     if (b.bytes >= bytes) return PR_OK;
     b.release();
-    cudaError_t e = cudaMalloc(&b.ptr, bytes);
+    cudaError_t e = cudaMallocAsync(&b.ptr, bytes, alloc_stream());
     if (e != cudaSuccess) {
         b.ptr = nullptr;
         cudaGetLastError();
-        return fail(PR_ERR_NOMEM, "cudaMalloc(" + std::to_string(bytes) + " B) failed: " +
+        return fail(PR_ERR_NOMEM, "cudaMallocAsync(" + std::to_string(bytes) + " B) failed: " +
                                       cudaGetErrorString(e));
     }
     b.bytes = bytes;
@@ -517,19 +522,49 @@ __global__ void k_perm_from_keys(const unsigned long long *__restrict__ keys, in
     }
 }
 
-// warp per original row: relabelled (src, dst) of every edge
-__global__ void k_relabel_edges(const int64_t *__restrict__ out_off, const int32_t *__restrict__ out_tgt, int64_t n,
-                                const int32_t *__restrict__ rank, int64_t *__restrict__ src, int64_t *__restrict__ dst) {
+// degree of new row i = degree of old row perm[i]
+__global__ void k_perm_len(const int64_t *__restrict__ off, const int32_t *__restrict__ perm, int64_t n,
+                           int64_t *__restrict__ len) {
+    GRID_STRIDE(i, n + 1) {
+        if (i == n) { len[n] = 0; continue; }
+        int32_t v = perm[i];
+        len[i] = off[v + 1] - off[v];
+    }
+}
+
+// warp per new row: copy the old row, renaming its column ids through rank
+__global__ void k_perm_rows(const int64_t *__restrict__ off, const int32_t *__restrict__ col,
+                            const int32_t *__restrict__ perm, const int32_t *__restrict__ rank, int64_t n,
+                            const int64_t *__restrict__ noff, int32_t *__restrict__ ncol) {
     int lane = threadIdx.x & 31;
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t u = warp; u < n; u += nw) {
-        int32_t ru = rank[u];
-        for (int64_t e = out_off[u] + lane; e < out_off[u + 1]; e += 32) {
-            src[e] = ru;
-            dst[e] = rank[out_tgt[e]];
-        }
+    for (int64_t i = warp; i < n; i += nw) {
+        int32_t v = perm[i];
+        int64_t lo = off[v], len = off[v + 1] - lo, o = noff[i];
+        for (int64_t k = lane; k < len; k += 32) ncol[o + k] = rank[col[lo + k]];
     }
+}
+
+// Permuted copy of one adjacency direction (no sort: a relabelling only
+// moves rows and renames columns; row-internal order is irrelevant to the
+// fast engines, whose summation order is fixed by their own schedule).
+static int permute_adjacency(Ctx &ctx, const DevBuf &off, const DevBuf &col, const DevBuf &perm, const DevBuf &rank,
+                             int64_t n, int64_t m, DevBuf &noff, DevBuf &ncol) {
+    cudaStream_t st = ctx.stream;
+    DevBuf len;
+    PR_TRY(ensure(len, 8 * (n + 1)));
+    PR_TRY(ensure(noff, 8 * (n + 1)));
+    PR_TRY(ensure(ncol, 4 * (m ? m : 1)));
+    k_perm_len<<<gs_grid(ctx, n + 1), 256, 0, st>>>(off.as<int64_t>(), perm.as<int32_t>(), n, len.as<int64_t>());
+    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, len.as<int64_t>(), noff.as<int64_t>(), (int)(n + 1), st);
+    }));
+    if (m)
+        k_perm_rows<<<(unsigned)(ctx.sm_count * 32), 256, 0, st>>>(off.as<int64_t>(), col.as<int32_t>(),
+                                                                 perm.as<int32_t>(), rank.as<int32_t>(), n,
+                                                                 noff.as<int64_t>(), ncol.as<int32_t>());
+    return PR_OK;
 }
 
 int ensure_run_layout(Graph &g) {
@@ -537,7 +572,7 @@ int ensure_run_layout(Graph &g) {
     Ctx &ctx = *g.ctx;
     cudaStream_t st = ctx.stream;
     int64_t n = g.n, m = g.m;
-    DevBuf keys, sorted, src, dst;
+    DevBuf keys, sorted;
     PR_TRY(ensure(keys, 8 * n));
     PR_TRY(ensure(sorted, 8 * n));
     PR_TRY(ensure(g.perm, 4 * n));
@@ -550,19 +585,18 @@ int ensure_run_layout(Graph &g) {
     }));
     k_perm_from_keys<<<gs_grid(ctx, n), 256, 0, st>>>(sorted.as<unsigned long long>(), n, g.perm.as<int32_t>(),
                                                      g.rank.as<int32_t>());
-    keys.release();
-    sorted.release();
-    PR_TRY(ensure(src, 8 * (m ? m : 1)));
-    PR_TRY(ensure(dst, 8 * (m ? m : 1)));
-    if (m) {
-        unsigned gr = (unsigned)(ctx.sm_count * 32);
-        k_relabel_edges<<<gr, 256, 0, st>>>(g.out_off.as<int64_t>(), g.out_tgt.as<int32_t>(), n,
-                                            g.rank.as<int32_t>(), src.as<int64_t>(), dst.as<int64_t>());
-    }
-    PR_CUDA(cudaStreamSynchronize(st));
-    PR_CUDA(cudaGetLastError());
-    Graph *r = nullptr;
-    PR_TRY(build_from_device_edges(ctx, n, src.as<int64_t>(), dst.as<int64_t>(), m, &r));
+    Graph *r = new Graph();
+    r->ctx = &ctx;
+    r->n = n;
+    r->m = m;
+    r->raw = g.raw;
+    int rc = permute_adjacency(ctx, g.out_off, g.out_tgt, g.perm, g.rank, n, m, r->out_off, r->out_tgt);
+    if (!rc) rc = permute_adjacency(ctx, g.in_off, g.in_src, g.perm, g.rank, n, m, r->in_off, r->in_src);
+    if (!rc) rc = ensure(r->out_deg, 4 * n);
+    if (!rc) k_degree<<<gs_grid(ctx, n), 256, 0, st>>>(r->out_off.as<int64_t>(), n, r->out_deg.as<int32_t>());
+    if (!rc && (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess))
+        rc = fail(PR_ERR_CUDA, "run layout build failed");
+    if (rc) { delete r; return rc; }
     g.run = r;
     return PR_OK;
 }

@@ -30,6 +30,12 @@ int fail(int code, const std::string &msg);
     } while (0)
 
 // ---------------------------------------------------------------- device buffers
+// Buffers come from the device's stream-ordered memory pool (cudaMallocAsync
+// on the context stream, release threshold kept at "never"), so building a
+// graph, its schedules and workspaces costs no cudaMalloc/cudaFree syncs.
+// alloc_stream() is the stream of the context the current C-ABI call runs on.
+cudaStream_t &alloc_stream();
+
 struct DevBuf {
     void *ptr = nullptr;
     size_t bytes = 0;
@@ -38,7 +44,7 @@ struct DevBuf {
     DevBuf &operator=(const DevBuf &) = delete;
     ~DevBuf() { release(); }
     void release() {
-        if (ptr) cudaFree(ptr);
+        if (ptr) cudaFreeAsync(ptr, alloc_stream());
         ptr = nullptr;
         bytes = 0;
     }
@@ -172,6 +178,9 @@ constexpr int TILE = 256;   // edges per warp tile (long rows are cut into TILE 
 constexpr int CSC_PAD = 1024;  // int32 padding past the compacted CSC for vector loads
 constexpr int64_t RANGE_ALPHA = 4;      // merge-path weight of one row drain, in edges
 constexpr int64_t RANGES_PER_WARP = 2;  // gather ranges per warp of the persistent grid
+
+// PUSHRANK_TIMING=1: host-side phase timings (synchronising) on stderr
+void phase_mark(cudaStream_t st, const char *what);
 
 // small helpers
 inline unsigned grid_for(int64_t items, int per_block) {

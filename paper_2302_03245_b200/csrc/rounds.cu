@@ -750,15 +750,18 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     if (algo == PR_ALGO_IFP2 && !g_in.has_ifp2) return fail(PR_ERR_STATE, "IFP2 needs pr_preprocess_ifp2 first");
     // fast engines run on the relabelled layout; exact mode on the original
     Graph *gp = &g_in;
+    phase_mark(ctx.stream, "run: enter");
     if (!exact) {
         PR_TRY(ensure_run_layout(g_in));
         gp = g_in.run;
+        phase_mark(ctx.stream, "run: layout");
     }
     Graph &g = *gp;
     const int32_t *perm = exact ? nullptr : g_in.perm.as<int32_t>();
     if (algo == PR_ALGO_IFP2) PR_TRY(preprocess_ifp2_device(g));
     else PR_TRY(ensure_dtc(g));
     PR_TRY(count_dangling(g));
+    phase_mark(ctx.stream, "run: ifp2 split/dtc");
     const int which = algo == PR_ALGO_IFP2 ? 1 : 0;
     // persistent pull grid: as many blocks as fit on the device at once,
     // one equal edge range per warp
@@ -772,7 +775,9 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     if (pull_blocks > (int64_t)ctx.sm_count * per_sm) pull_blocks = (int64_t)ctx.sm_count * per_sm;
     if (pull_blocks < 1) pull_blocks = 1;
     const int64_t fcap = n + g.m / TILE + 1;
+    phase_mark(ctx.stream, "run: schedule");
     PR_TRY(ws_alloc(g, pull_blocks, fcap));
+    phase_mark(ctx.stream, "run: workspace");
 
     Plan P;
     memset(&P, 0, sizeof(P));
@@ -861,6 +866,7 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
             PR_TRY(build_graph(P, &slot->graph, &slot->exec));
             slot->key = p;
             slot->valid = true;
+            phase_mark(ctx.stream, "run: graph instantiate");
         }
         PR_CUDA(cudaGraphLaunch(slot->exec, st));
     } else {
@@ -922,6 +928,7 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     }
     PR_CUDA(cudaEventRecord(e2, st));
     PR_CUDA(cudaEventSynchronize(e2));
+    phase_mark(ctx.stream, "run: solve");
     PR_CUDA(cudaGetLastError());
     float ms_loop = 0.f, ms_all = 0.f;
     PR_CUDA(cudaEventElapsedTime(&ms_loop, e0, e1));
