@@ -1,0 +1,140 @@
+// bins.cuh -- degree-binned CSC gather over the pull schedule (sched.cu).
+//
+// Rows are sorted by descending in-degree and cut into block work units of
+// near-equal cost (edges + ROW_COST * rows); a unit never mixes bins:
+//   * hub unit    -- HUB_CHUNK edges of one row with > HUB_DEG edges, 16
+//                    coalesced gathers per thread; the last chunk of a row to
+//                    arrive adds the chunk sums in chunk order;
+//   * warp unit   -- rows with THREAD_DEG < d <= HUB_DEG; warp w takes rows
+//                    w, w+8, ...; lanes stride a row with 8 gathers in flight;
+//   * thread unit -- rows with d <= THREAD_DEG; thread t takes rows t, t+256,
+//                    ... (coalesced drains), 8 index loads then 8 gathers.
+// Rows of a unit have near-equal degree (sorted), so warps carry uniform
+// work; units are dealt round-robin to a persistent grid.  Every summation
+// order is fixed by the schedule: results are run-to-run deterministic.
+#pragma once
+
+#include "internal.cuh"
+
+namespace pr {
+
+struct BinView {
+    const int32_t *ids;      // row -> vertex id
+    const int64_t *doff;     // row offsets in csc
+    const int32_t *csc;      // compacted sources (padded)
+    int64_t count, n_hub, n_warp;
+    const int64_t *chunk_base;   // first chunk unit of each hub row
+    const int2 *units;           // (row_begin, row_end) or hub chunk (row, -(chunk+1))
+    int64_t n_units;
+    int32_t *row_cnt;
+    double *chunk_part;          // per hub chunk unit
+};
+
+__device__ __forceinline__ double row_sum_thread(const int32_t *__restrict__ csc, int64_t lo, int64_t hi,
+                                                 const double *__restrict__ x) {
+    double acc = 0.0;
+    for (int64_t e = lo; e < hi; e += 8) {
+        int idx[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) idx[q] = e + q < hi ? __ldg(&csc[e + q]) : -1;
+        double t[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t[q] = idx[q] >= 0 ? __ldg(&x[idx[q]]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc += t[q];
+    }
+    return acc;
+}
+
+// lanes stride [lo, hi) with 8 gathers in flight; warp-reduced (fixed tree)
+__device__ __forceinline__ double span_sum_warp(const int32_t *__restrict__ csc, int64_t lo, int64_t hi,
+                                                const double *__restrict__ x) {
+    const int lane = threadIdx.x & 31;
+    double acc = 0.0;
+    for (int64_t e = lo + lane; e < hi; e += 256) {
+        int idx[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) idx[q] = e + 32 * q < hi ? __ldg(&csc[e + 32 * q]) : -1;
+        double t[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t[q] = idx[q] >= 0 ? __ldg(&x[idx[q]]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc += t[q];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    return acc;
+}
+
+// thread_row(valid, row, sum): all 32 lanes of a warp (warp-collective safe)
+// single_row(row, sum): one thread
+template <class ThreadRow, class SingleRow>
+__device__ __forceinline__ void bins_run(const BinView &B, const double *__restrict__ x, ThreadRow &thread_row,
+                                         SingleRow &single_row) {
+    __shared__ double red[8];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int64_t warp_rows = B.n_hub + B.n_warp;
+    for (int64_t u = blockIdx.x; u < B.n_units; u += gridDim.x) {
+        const int2 d = B.units[u];
+        if (d.y < 0) {
+            // ---- HUB_CHUNK edges of one hub row, whole block
+            const int64_t r = d.x, c = -(int64_t)d.y - 1;
+            const int64_t rb = B.doff[r], re = B.doff[r + 1];
+            const int64_t c0 = rb + c * HUB_CHUNK;
+            const int64_t c1 = c0 + HUB_CHUNK < re ? c0 + HUB_CHUNK : re;
+            int idx[HUB_CHUNK / 256];
+#pragma unroll
+            for (int q = 0; q < HUB_CHUNK / 256; ++q) {
+                const int64_t e = c0 + tid + 256 * q;
+                idx[q] = e < c1 ? __ldg(&B.csc[e]) : -1;
+            }
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < HUB_CHUNK / 256; ++q) acc += idx[q] >= 0 ? __ldg(&x[idx[q]]) : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            __syncthreads();
+            if (lane == 0) red[wid] = acc;
+            __syncthreads();
+            if (tid == 0) {
+                double s = 0.0;
+                for (int k = 0; k < 8; ++k) s += red[k];
+                const int nch = (int)((re - rb + HUB_CHUNK - 1) / HUB_CHUNK);
+                B.chunk_part[u] = s;
+                __threadfence();
+                if (atomicAdd(&B.row_cnt[r], 1) == nch - 1) {
+                    __threadfence();
+                    const int64_t first = B.chunk_base[r];
+                    double tot = 0.0;
+                    for (int k = 0; k < nch; ++k) tot += __ldcg(&B.chunk_part[first + k]);
+                    B.row_cnt[r] = 0;
+                    single_row(r, tot);
+                }
+            }
+        } else if (d.x < warp_rows) {
+            // ---- warp rows: warp w takes rows w, w+8, ...; sums of 32 rows
+            // collected (lane j holds row j's) and drained lane-parallel
+            for (int64_t base = d.x + wid; base < d.y; base += 8 * 32) {
+                double mine = 0.0;
+                for (int j = 0; j < 32; ++j) {
+                    const int64_t row = base + 8 * j;
+                    if (row >= d.y) break;
+                    const double s = span_sum_warp(B.csc, B.doff[row], B.doff[row + 1], x);
+                    if (lane == j) mine = s;
+                }
+                const int64_t row = base + 8 * lane;
+                thread_row(row < d.y, row, mine);
+            }
+        } else {
+            // ---- thread rows: thread t takes rows t, t+256, ... (whole warps iterate together)
+            for (int64_t base = d.x; base < d.y; base += 256) {
+                const int64_t row = base + tid;
+                const bool valid = row < d.y;
+                const double s = valid ? row_sum_thread(B.csc, B.doff[row], B.doff[row + 1], x) : 0.0;
+                thread_row(valid, row, s);
+            }
+        }
+    }
+}
+
+}  // namespace pr

@@ -41,6 +41,7 @@ int upload_graph(Ctx &ctx, int64_t n, int64_t m, const int64_t *out_off, const i
 int export_graph(Graph &g, int64_t *out_off, int64_t *out_tgt, int64_t *in_off, int64_t *in_src);
 int export_i32(Ctx &ctx, const DevBuf &src, int64_t count, int64_t *host);
 int export_i64(Ctx &ctx, const DevBuf &src, int64_t count, int64_t *host);
+int debug_gather(Graph &g0, int variant, int iters, int blocks_per_sm, double *ms_out);
 
 static int set_device(Ctx &ctx) {
     PR_CUDA(cudaSetDevice(ctx.device));
@@ -372,6 +373,13 @@ int pr_memcpy_d2h(pr_ctx *ctx, void *h_dst, const void *d_src, int64_t bytes) {
     PR_CUDA(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, ctx->c.stream));
     PR_CUDA(cudaStreamSynchronize(ctx->c.stream));
     return PR_OK;
+}
+
+// diagnostics (not part of the documented ABI): gather microbenchmarks
+int pr_debug_gather(pr_graph *g, int variant, int iters, int blocks_per_sm, double *ms_out) {
+    CHECK_PTR(g, "graph");
+    PR_TRY(set_device(*g->g->ctx));
+    return debug_gather(*g->g, variant, iters, blocks_per_sm, ms_out);
 }
 
 }  // extern "C"

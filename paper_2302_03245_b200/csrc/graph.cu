@@ -502,13 +502,14 @@ int preprocess_ifp2_device(Graph &g) {
 
 // ---------------------------------------------------------------- run layout
 
-// sort key: class (2 bits) | descending out-degree inside class 0 (31 bits) | id (31 bits)
+// sort key: class (2 bits) | descending in-degree inside the receiving
+// classes 0 and 2 (31 bits) | id (31 bits)
 __global__ void k_relabel_keys(const int64_t *__restrict__ out_off, const int64_t *__restrict__ in_off, int64_t n,
                                unsigned long long *__restrict__ keys) {
     GRID_STRIDE(v, n) {
         int64_t od = out_off[v + 1] - out_off[v], id = in_off[v + 1] - in_off[v];
         unsigned long long cls = od > 0 ? (id > 0 ? 0 : 1) : (id > 0 ? 2 : 3);
-        unsigned long long dk = cls == 0 ? (unsigned long long)(0x7FFFFFFFll - od) : 0ull;
+        unsigned long long dk = (cls == 0 || cls == 2) ? (unsigned long long)(0x7FFFFFFFll - id) : 0ull;
         keys[v] = (cls << 62) | (dk << 31) | (unsigned long long)v;
     }
 }

@@ -111,23 +111,26 @@ struct Graph {
     DevBuf dang_ids, src_off, src_ids;       // int32 [n_d], int64 [n_d+1], int32 [m_d]
     // Pull schedules, built lazily: [0] ifp1/fp-full destinations (in-degree
     // > 0), [1] ifp2 (non-dangling, in-degree > 0), [2] power (in-degree > 0;
-    // the zero-in-degree vertices are listed separately).  Rows of D keep
-    // ascending id order; their sources are compacted into one CSC and cut
-    // into equal edge ranges, one per warp (sched.cu, tiles.cuh).
+    // the zero-in-degree vertices are listed separately).  Rows are ordered by
+    // descending in-degree and cut into block units of near-equal cost --
+    // hub-row chunks (rows > HUB_DEG), warp-row ranges (> THREAD_DEG),
+    // thread-row ranges -- dealt round-robin to a persistent grid (bins.cuh).
     struct Sched {
         bool built = false;
         int64_t count = 0;        // |D|
         int64_t edges = 0;        // edges of the D rows
-        int64_t ew = 0, n_ranges = 0;  // range weight (edges + ALPHA*rows), range count
-        DevBuf ids;               // int32 [|D|] vertex id of each row
+        int64_t n_hub = 0, n_warp = 0;    // rows [0,n_hub) hubs, [n_hub, n_hub+n_warp) warp rows
+        int64_t n_chunks = 0;     // CHUNK-edge units of the hub rows
+        DevBuf ids;               // int32 [|D|] vertex id of each row (descending in-degree)
         DevBuf doff;              // int64 [|D|+1] compacted CSC offsets
         DevBuf csc;               // int32 [edges + pad] compacted sources
-        DevBuf flags;             // uint32 words: bit e set if edge e starts a row
-        DevBuf rrow;              // int32 [n_ranges] row holding each range's first edge
-        DevBuf rstart;            // int64 [n_ranges+1] first edge of each range
-        DevBuf rsplit;            // int2 [n_ranges] split-row range bounds (tiles.cuh)
-        DevBuf row_cnt;           // int32 [|D|] split-row arrival counters
-        DevBuf lead, trail;       // double [n_ranges] split-row partials
+        DevBuf chunk_base;        // int64 [n_hub+1] first chunk of each hub row
+        DevBuf row_cum;           // int64 [|D|+1] exclusive prefix of row costs (edges + ROW_COST)
+        int64_t unit_blocks = 0;  // grid size the units below were cut for
+        int64_t n_units = 0;
+        DevBuf units;             // int2 [n_units]: (row_begin, row_end) or hub chunk (row, -(chunk+1))
+        DevBuf row_cnt;           // int32 [n_hub] chunk arrival counters
+        DevBuf chunk_part;        // double [n_chunks] chunk partial sums
         int64_t n_zero = 0;       // power: in-degree-0 vertices
         DevBuf zero_ids;
         int64_t n_seed = 0;       // vertices outside D active at round 0 (scatter seeds)
@@ -139,12 +142,13 @@ struct Graph {
     int64_t max_blocks = 0;     // partial slots per region (partials holds 3 regions)
     int64_t n_dangling = -1;    // #(out_degree == 0), computed lazily
     DevBuf pw;                // power-method workspace
-    // Run layout of the fast engines (sched relabel, graph.cu): the same
-    // graph with vertices renumbered by class (in>0&out>0 | out>0&in=0 |
-    // out=0&in>0 | isolated) and, inside the first class, by descending
-    // out-degree, so hot sources are dense in L1/L2 and every engine's
-    // destination set is a contiguous id range.  Exact mode keeps the
-    // original layout (bit-exact summation order).
+    // Run layout of the fast engines (graph.cu): the same graph with
+    // vertices renumbered by class (in>0&out>0 | out>0&in=0 | out=0&in>0 |
+    // isolated) and, inside the receiving classes, by descending in-degree:
+    // pull rows of similar degree are adjacent (uniform warps), hot sources
+    // (in/out degrees correlate on power-law graphs) are dense in L1/L2, and
+    // the IFP2 destination set is a contiguous id range.  Exact mode keeps
+    // the original layout (bit-exact summation order).
     Graph *run = nullptr;
     DevBuf perm;              // int32 [n]: run id -> original id
     DevBuf rank;              // int32 [n]: original id -> run id
@@ -162,7 +166,8 @@ int ensure_dtc(Graph &g);
 int count_dangling(Graph &g);
 int ensure_run_layout(Graph &g);
 void invalidate_cache(Graph &g);
-int ensure_sched(Graph &g, int which, int64_t target_warps = 0);
+int ensure_sched(Graph &g, int which);
+int ensure_units(Graph &g, int which, int64_t blocks);
 int build_from_device_edges(Ctx &ctx, int64_t n, const int64_t *d_src, const int64_t *d_dst,
                             int64_t m_raw, Graph **out);
 int classify_device(Graph &g);
@@ -176,8 +181,11 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
 
 constexpr int TILE = 256;   // edges per warp tile (long rows are cut into TILE chunks)
 constexpr int CSC_PAD = 1024;  // int32 padding past the compacted CSC for vector loads
-constexpr int64_t RANGE_ALPHA = 4;      // merge-path weight of one row drain, in edges
-constexpr int64_t RANGES_PER_WARP = 2;  // gather ranges per warp of the persistent grid
+constexpr int64_t THREAD_DEG = 32;   // rows up to this in-degree: one thread each
+constexpr int64_t HUB_DEG = 4096;    // rows above: cut into HUB_CHUNK-edge block units
+constexpr int64_t HUB_CHUNK = 4096;  // edges per hub unit (256 threads x 16)
+constexpr int64_t ROW_COST = 8;      // per-row drain cost in edge units (unit sizing)
+constexpr int64_t UNITS_PER_BLOCK = 4;  // target work units per block of the persistent grid
 
 // PUSHRANK_TIMING=1: host-side phase timings (synchronising) on stderr
 void phase_mark(cudaStream_t st, const char *what);

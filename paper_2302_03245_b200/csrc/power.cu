@@ -14,7 +14,7 @@
 
 #include "internal.cuh"
 #include "reduce.cuh"
-#include "tiles.cuh"
+#include "bins.cuh"
 
 namespace pr {
 
@@ -32,7 +32,7 @@ struct PowArgs {
     const int64_t *in_off;
     const int32_t *in_src;
     const int32_t *deg;
-    RangeView T;              // rows with in-degree > 0
+    BinView T;               // rows with in-degree > 0
     const int32_t *zero_ids; // in-degree-0 vertices: nxt = restart * p
     int64_t n_zero;
     const double *p;         // personalization (null: uniform 1/n)
@@ -99,11 +99,8 @@ __global__ void __launch_bounds__(256) k_pw_init(PowArgs A) {
 }
 
 // nxt_v = sum z over in-edges + restart * p_v; block partial of sum(nxt)
-__global__ void __launch_bounds__(256) k_pw_gather(PowArgs A) {
-    __shared__ double rs_all[8][RS_CAP];
+__global__ void __launch_bounds__(256, 4) k_pw_gather(PowArgs A) {
     const double restart = A.ctl->restart;
-    const int lane = threadIdx.x & 31;
-    double *rs = rs_all[threadIdx.x >> 5];
     Partial p;
     zero(p);
     auto finish = [&](int32_t v, double sum) {
@@ -111,13 +108,11 @@ __global__ void __launch_bounds__(256) k_pw_gather(PowArgs A) {
         A.nxt[v] = x;
         p.l1 += x;
     };
-    auto split_row = [&](int64_t row, double sum) { finish(A.T.ids[row], sum); };
-    auto drain_batch = [&](int64_t row0, int cnt, const double *sums) {
-        for (int i = lane; i < cnt; i += 32) finish(__ldg(&A.T.ids[row0 + i]), sums[i]);
+    auto thread_row = [&](bool valid, int64_t row, double sum) {
+        if (valid) finish(__ldg(&A.T.ids[row]), sum);
     };
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t k = warp; k < A.T.n_ranges; k += nw) warp_range(A.T, k, A.z, rs, drain_batch, split_row);
+    auto single_row = [&](int64_t row, double sum) { finish(__ldg(&A.T.ids[row]), sum); };
+    bins_run(A.T, A.z, thread_row, single_row);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.n_zero;
          i += (int64_t)gridDim.x * blockDim.x)
         finish(A.zero_ids[i], 0.0);
@@ -154,12 +149,13 @@ __global__ void __launch_bounds__(256) k_pw_norm(PowArgs A) {
 }
 
 static int add_node(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t *deps, size_t nd, void *f,
-                    unsigned grid, void **args) {
+                    unsigned grid, void **args, size_t smem = 0) {
     cudaKernelNodeParams kp;
     memset(&kp, 0, sizeof(kp));
     kp.func = f;
     kp.gridDim = dim3(grid);
     kp.blockDim = dim3(256);
+    kp.sharedMemBytes = (unsigned)smem;
     kp.kernelParams = args;
     PR_CUDA(cudaGraphAddKernelNode(node, g, deps, nd, &kp));
     return PR_OK;
@@ -175,14 +171,13 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
     int per_sm = 0;
     PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pw_gather, 256, 0));
     if (per_sm < 1) per_sm = 1;
-    PR_TRY(ensure_sched(g, 2, (int64_t)ctx.sm_count * per_sm * 8));
+    PR_TRY(ensure_sched(g, 2));
     auto &S = g.sched[2];
     int64_t n = g.n;
     PowArgs A;
     memset(&A, 0, sizeof(A));
-    int64_t blk = (S.n_ranges + 7) / 8;
-    if (blk > (int64_t)ctx.sm_count * per_sm) blk = (int64_t)ctx.sm_count * per_sm;
-    if (blk < 1) blk = 1;
+    const int64_t blk = (int64_t)ctx.sm_count * per_sm;
+    PR_TRY(ensure_units(g, 2, blk));
     int64_t maxb = blk > (n + 255) / 256 ? blk : (n + 255) / 256;
     int64_t it_cap = iterations > 0 ? iterations : 1;
     // workspace: pi, nxt, z, p (opt), deltas, conv, partials, ctl
@@ -199,15 +194,14 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
     A.T.ids = S.ids.as<int32_t>();
     A.T.doff = S.doff.as<int64_t>();
     A.T.csc = S.csc.as<int32_t>();
-    A.T.flags8 = S.flags.as<uint8_t>();
-    A.T.rrow = S.rrow.as<int32_t>();
-    A.T.rstart = S.rstart.as<int64_t>();
-    A.T.rsplit = S.rsplit.as<int2>();
-    A.T.edges = S.edges;
-    A.T.n_ranges = S.n_ranges;
+    A.T.count = S.count;
+    A.T.n_hub = S.n_hub;
+    A.T.n_warp = S.n_warp;
+    A.T.chunk_base = S.chunk_base.as<int64_t>();
     A.T.row_cnt = S.row_cnt.as<int32_t>();
-    A.T.lead = S.lead.as<double>();
-    A.T.trail = S.trail.as<double>();
+    A.T.chunk_part = S.chunk_part.as<double>();
+    A.T.units = S.units.as<int2>();
+    A.T.n_units = S.n_units;
     A.zero_ids = S.zero_ids.as<int32_t>();
     A.n_zero = S.n_zero;
     A.pi = (double *)(base + off_pi);

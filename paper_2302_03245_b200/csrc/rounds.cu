@@ -32,7 +32,7 @@
 
 #include "internal.cuh"
 #include "reduce.cuh"
-#include "tiles.cuh"
+#include "bins.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -47,7 +47,7 @@ struct RunArgs {
     const int32_t *deg;        // original out-degree: push weight denominator
     const int32_t *row_len;    // push row length for push_ops (out_deg or live_deg)
     const int32_t *dtc;        // dangling-target counts (ifp1/fp-full) or null (ifp2)
-    RangeView T;                // pull schedule of D (sched.cu)
+    BinView T;                  // pull schedule of D (sched.cu, bins.cuh)
     const int32_t *ids;        // D rows' vertex ids (== T.ids)
     int64_t d_count;
     const int32_t *seeds;      // vertices outside D active at state 0
@@ -336,56 +336,37 @@ __global__ void __launch_bounds__(256) k_seed_scatter(RunArgs A) {
 }
 
 // Dense round t: h(t+1)_v = h_drained(t)_v + sum_{u in in(v)} s(t)_u over D,
-// fused with the drain of state t+1.  Persistent grid, one warp per tile;
-// row sums staged in shared memory, then drained lane-parallel.
+// fused with the drain of state t+1.  Persistent grid over degree bins
+// (bins.cuh): thread rows drain lane-parallel (coalesced vertex loads,
+// warp-aggregated frontier append), warp and hub rows on one lane.
 #ifndef PULL_MIN_BLOCKS
-#define PULL_MIN_BLOCKS 2
+#define PULL_MIN_BLOCKS 4
 #endif
 __global__ void __launch_bounds__(256, PULL_MIN_BLOCKS) k_pull(RunArgs A) {
-    __shared__ double rs_all[8][RS_CAP];
-    __shared__ Partial wpart[8];   // per-warp statistics (kept out of the gather's registers)
     const int64_t t = A.ctl->round;
     const double *__restrict__ s_in = A.s + (t & 1) * A.n;
     const int64_t r = t + 1;
     const bool app = A.ctl->append != 0;
     long long *F = A.frontier + (r & 1) * A.fcap;
     int64_t *fsize = &A.ctl->fsize[r & 1];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    double *rs = rs_all[wid];
-    if (lane == 0) zero(wpart[wid]);
-    __syncwarp();
-    auto split_row = [&](int64_t row, double sum) {  // lane 0 only
-        Partial bp;
-        zero(bp);
-        int32_t v = A.ids[row];
-        int it = drain_vertex(A, v, A.h[v] + sum, r, bp);
-        if (app) append_one(it, v, F, fsize);
-        add(wpart[wid], bp);
-    };
-    auto drain_batch = [&](int64_t row0, int cnt, const double *sums) {
-        for (int b = 0; b < cnt; b += 32) {
-            const int i = b + lane;
-            Partial bp;
-            zero(bp);
-            int items = 0;
-            int32_t v = 0;
-            if (i < cnt) {
-                v = __ldg(&A.ids[row0 + i]);
-                items = drain_vertex(A, v, A.h[v] + sums[i], r, bp);
-            }
-            append_warp(app, items, v, F, fsize);
-            warp_fold(bp, wpart[wid]);
-        }
-    };
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t k = warp; k < A.T.n_ranges; k += nw) warp_range(A.T, k, s_in, rs, drain_batch, split_row);
-    __syncthreads();
     Partial p;
     zero(p);
-    if (threadIdx.x == 0)
-        for (int w = 0; w < 8; ++w) add(p, wpart[w]);
-    publish_round(A, p, r, true, false, p);
+    auto thread_row = [&](bool valid, int64_t row, double sum) {
+        int items = 0;
+        int32_t v = 0;
+        if (valid) {
+            v = __ldg(&A.ids[row]);
+            items = drain_vertex(A, v, A.h[v] + sum, r, p);
+        }
+        append_warp(app, items, v, F, fsize);
+    };
+    auto single_row = [&](int64_t row, double sum) {
+        int32_t v = __ldg(&A.ids[row]);
+        int it = drain_vertex(A, v, A.h[v] + sum, r, p);
+        if (app) append_one(it, v, F, fsize);
+    };
+    bins_run(A.T, s_in, thread_row, single_row);
+    finish_round(A, p, r, true, false, p);
 }
 
 // Sparse round t, step 1: scatter the frontier's shares (red.global.add.f64);
@@ -623,13 +604,13 @@ __global__ void k_mark_d(const int32_t *ids, int64_t count, uint8_t *in_d) {
 // ---------------------------------------------------------------- host side
 
 static int add_kernel(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t *deps, size_t ndeps, void *func,
-                      unsigned grid, unsigned block, void **args) {
+                      unsigned grid, unsigned block, void **args, size_t smem = 0) {
     cudaKernelNodeParams kp;
     memset(&kp, 0, sizeof(kp));
     kp.func = func;
     kp.gridDim = dim3(grid);
     kp.blockDim = dim3(block);
-    kp.sharedMemBytes = 0;
+    kp.sharedMemBytes = (unsigned)smem;
     kp.kernelParams = args;
     PR_CUDA(cudaGraphAddKernelNode(node, g, deps, ndeps, &kp));
     return PR_OK;
@@ -764,16 +745,15 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     phase_mark(ctx.stream, "run: ifp2 split/dtc");
     const int which = algo == PR_ALGO_IFP2 ? 1 : 0;
     // persistent pull grid: as many blocks as fit on the device at once,
-    // one equal edge range per warp
     int per_sm = 0;
     PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pull, 256, 0));
     if (per_sm < 1) per_sm = 1;
-    PR_TRY(ensure_sched(g, which, (int64_t)ctx.sm_count * per_sm * 8));
+    PR_TRY(ensure_sched(g, which));
     auto &S = g.sched[which];
     int64_t n = g.n;
-    int64_t pull_blocks = (S.n_ranges + 7) / 8;
-    if (pull_blocks > (int64_t)ctx.sm_count * per_sm) pull_blocks = (int64_t)ctx.sm_count * per_sm;
-    if (pull_blocks < 1) pull_blocks = 1;
+    // persistent pull grid, ~UNITS_PER_BLOCK equal-cost units per block
+    const int64_t pull_blocks = (int64_t)ctx.sm_count * per_sm;
+    PR_TRY(ensure_units(g, which, pull_blocks));
     const int64_t fcap = n + g.m / TILE + 1;
     phase_mark(ctx.stream, "run: schedule");
     PR_TRY(ws_alloc(g, pull_blocks, fcap));
@@ -801,15 +781,14 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     A.T.ids = S.ids.as<int32_t>();
     A.T.doff = S.doff.as<int64_t>();
     A.T.csc = S.csc.as<int32_t>();
-    A.T.flags8 = S.flags.as<uint8_t>();
-    A.T.rrow = S.rrow.as<int32_t>();
-    A.T.rstart = S.rstart.as<int64_t>();
-    A.T.rsplit = S.rsplit.as<int2>();
-    A.T.edges = S.edges;
-    A.T.n_ranges = S.n_ranges;
+    A.T.count = S.count;
+    A.T.n_hub = S.n_hub;
+    A.T.n_warp = S.n_warp;
+    A.T.chunk_base = S.chunk_base.as<int64_t>();
     A.T.row_cnt = S.row_cnt.as<int32_t>();
-    A.T.lead = S.lead.as<double>();
-    A.T.trail = S.trail.as<double>();
+    A.T.chunk_part = S.chunk_part.as<double>();
+    A.T.units = S.units.as<int2>();
+    A.T.n_units = S.n_units;
     A.d_count = S.count;
     A.seeds = S.seed_ids.as<int32_t>();
     A.n_seed = S.n_seed;

@@ -1,13 +1,17 @@
 // sched.cu -- pull schedules: the destination set D, its compacted CSC and
-// the row-aligned warp tiles the gather kernels walk.
+// the degree bins the gather kernels walk.
 //
 // Layout (built once per graph and engine, all on the device):
-//   ids[i]     vertex id of row i (ascending)
+//   ids[i]     vertex id of row i; rows sorted by descending in-degree
+//              (stable, so ties keep ascending id)
 //   doff[i]    offsets of row i's sources in csc (in-edges, ascending source)
-//   flags      1 bit per edge: set on the first edge of every row
-//   ranges     equal runs of ew edges (ew a multiple of 256), one per warp of
-//              the persistent gather grid; rrow[k] = row holding edge k*ew
-//              (tiles.cuh streams them and fixes up rows cut by a boundary)
+//   bins       rows [0, n_hub): > HUB_DEG edges; [n_hub, n_hub + n_warp):
+//              > THREAD_DEG edges (warp per row); the rest thread per row
+//   units      per grid size: hub rows cut into HUB_CHUNK-edge block units
+//              (combined by the last arriving chunk in chunk order); each
+//              other bin cut into contiguous row ranges of near-equal cost
+//              (edges + ROW_COST * rows, by a prefix sum), ~UNITS_PER_BLOCK
+//              per block of the persistent grid.
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -35,19 +39,28 @@ struct SeedPred {
     __host__ __device__ bool operator()(int32_t v) const { return in_off[v + 1] == in_off[v] && out_deg[v] > 0; }
 };
 
+// descending-degree sort key (ascending radix sort of ~degree)
+__global__ void k_deg_keys(const int32_t *__restrict__ ids, int64_t cnt, const int64_t *__restrict__ in_off,
+                           unsigned *__restrict__ keys) {
+    GRID_STRIDE(i, cnt) {
+        int32_t v = ids[i];
+        keys[i] = ~(unsigned)(in_off[v + 1] - in_off[v]);
+    }
+}
+
 __global__ void k_row_len(const int32_t *__restrict__ ids, int64_t cnt, const int64_t *__restrict__ in_off,
                           int64_t *__restrict__ len) {
-    GRID_STRIDE(i, cnt) {
+    GRID_STRIDE(i, cnt + 1) {
+        if (i == cnt) { len[cnt] = 0; continue; }
         int32_t v = ids[i];
         len[i] = in_off[v + 1] - in_off[v];
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) len[cnt] = 0;
 }
 
-// warp per row: copy the row's sources and set its start bit
+// warp per row: copy the row's sources into the compacted CSC
 __global__ void k_fill_csc(const int32_t *__restrict__ ids, int64_t cnt, const int64_t *__restrict__ in_off,
                            const int32_t *__restrict__ in_src, const int64_t *__restrict__ doff,
-                           int32_t *__restrict__ csc, unsigned *__restrict__ flags) {
+                           int32_t *__restrict__ csc) {
     int lane = threadIdx.x & 31;
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -55,95 +68,122 @@ __global__ void k_fill_csc(const int32_t *__restrict__ ids, int64_t cnt, const i
         int32_t v = ids[i];
         int64_t lo = in_off[v], len = in_off[v + 1] - lo, o = doff[i];
         for (int64_t k = lane; k < len; k += 32) csc[o + k] = in_src[lo + k];
-        if (lane == 0) atomicOr(&flags[o >> 5], 1u << (o & 31));
     }
 }
 
-// Merge-path split: range k starts at weight k*W on the axis where row i
-// occupies ALPHA units (its drain) followed by its edges.  The start is
-// snapped down to a multiple of 8 edges; rrow[k] = row holding that edge.
-__global__ void k_range_split(const int64_t *__restrict__ doff, int64_t cnt, int64_t edges, int64_t W,
-                              int64_t n_ranges, int64_t *__restrict__ rstart, int32_t *__restrict__ rrow) {
-    GRID_STRIDE(k, n_ranges + 1) {
-        if (k == n_ranges) { rstart[k] = edges; continue; }
-        const int64_t p = k * W;
-        int64_t lo = 0, hi = cnt - 1;  // last row i with doff[i] + ALPHA*i <= p
-        while (lo < hi) {
-            int64_t mid = (lo + hi + 1) >> 1;
-            if (doff[mid] + RANGE_ALPHA * mid <= p) lo = mid;
-            else hi = mid - 1;
-        }
-        int64_t e = p - RANGE_ALPHA * lo;
-        if (e < doff[lo]) e = doff[lo];
-        if (e > doff[lo + 1]) e = doff[lo + 1];
-        e &= ~7ll;
-        if (k == 0) e = 0;
-        rstart[k] = e;
-        // row holding edge e (doff strictly increasing: every D row has an edge)
-        int64_t a = 0, b = cnt - 1;
-        while (a < b) {
-            int64_t mid = (a + b + 1) >> 1;
-            if (doff[mid] <= e) a = mid;
-            else b = mid - 1;
-        }
-        rrow[k] = (int32_t)a;
+// numbers of rows with degree > t1 and > t2 (rows sorted by descending degree)
+__global__ void k_count_above(const int64_t *__restrict__ doff, int64_t cnt, int64_t t1, int64_t t2,
+                              unsigned long long *__restrict__ out) {
+    GRID_STRIDE(i, cnt) {
+        int64_t d = doff[i + 1] - doff[i];
+        if (d > t1) atomicAdd(&out[0], 1ull);
+        if (d > t2) atomicAdd(&out[1], 1ull);
     }
 }
 
-__device__ __forceinline__ int64_t range_holding(const int64_t *rstart, int64_t n_ranges, int64_t e) {
-    int64_t lo = 0, hi = n_ranges - 1;
-    while (lo < hi) {
-        int64_t mid = (lo + hi + 1) >> 1;
-        if (rstart[mid] <= e) lo = mid;
-        else hi = mid - 1;
-    }
-    return lo;
+__global__ void k_chunks_of(const int64_t *__restrict__ doff, int64_t n_hub, int64_t *__restrict__ nch) {
+    GRID_STRIDE(i, n_hub + 1) { nch[i] = i < n_hub ? (doff[i + 1] - doff[i] + HUB_CHUNK - 1) / HUB_CHUNK : 0; }
 }
 
-// per range: (range where its first row starts, range where the row holding
-// its last edge ends) -- the split-row fix-up bounds used by tiles.cuh
-__global__ void k_range_bounds(const int64_t *__restrict__ doff, const int64_t *__restrict__ rstart,
-                               const int32_t *__restrict__ rrow, int64_t cnt, int64_t n_ranges,
-                               int2 *__restrict__ rsplit) {
-    GRID_STRIDE(k, n_ranges) {
-        int64_t r0 = rrow[k];
-        int64_t b1 = rstart[k + 1];
-        int64_t lo = 0, hi = cnt - 1;  // row holding edge b1-1
-        while (lo < hi) {
-            int64_t mid = (lo + hi + 1) >> 1;
-            if (doff[mid] <= b1 - 1) lo = mid;
-            else hi = mid - 1;
-        }
-        int64_t k1 = range_holding(rstart, n_ranges, doff[r0]);
-        int64_t k2 = range_holding(rstart, n_ranges, doff[lo + 1] - 1);
-        rsplit[k] = make_int2((int)k1, (int)k2);
+
+__global__ void k_row_cost(const int64_t *__restrict__ doff, int64_t cnt, int64_t *__restrict__ cost) {
+    GRID_STRIDE(i, cnt + 1) { cost[i] = i < cnt ? doff[i + 1] - doff[i] + ROW_COST : 0; }
+}
+
+// hub chunk units (row, -(chunk+1)) in row/chunk order
+__global__ void k_hub_units(const int64_t *__restrict__ base, int64_t n_hub, int2 *__restrict__ units) {
+    GRID_STRIDE(i, n_hub) {
+        for (int64_t c = base[i]; c < base[i + 1]; ++c) units[c] = make_int2((int)i, (int)(-(c - base[i] + 1)));
     }
 }
 
-int ensure_sched(Graph &g, int which, int64_t target_warps) {
+// k equal-cost row ranges over rows [r0, r1): unit j = [first row with
+// cum >= j*C/k, first row with cum >= (j+1)*C/k)
+__global__ void k_range_units(const int64_t *__restrict__ cum, int64_t r0, int64_t r1, int64_t k,
+                              int2 *__restrict__ units) {
+    GRID_STRIDE(j, k) {
+        const int64_t base = cum[r0], total = cum[r1] - base;
+        auto find = [&](int64_t target) {
+            int64_t lo = r0, hi = r1;
+            while (lo < hi) {
+                int64_t mid = (lo + hi) >> 1;
+                if (cum[mid] - base >= target) hi = mid;
+                else lo = mid + 1;
+            }
+            return lo;
+        };
+        const int64_t a = j == 0 ? r0 : find((int64_t)((__int128)total * j / k));
+        const int64_t b = j == k - 1 ? r1 : find((int64_t)((__int128)total * (j + 1) / k));
+        units[j] = make_int2((int)a, (int)b);
+    }
+}
+
+int ensure_units(Graph &g, int which, int64_t blocks) {
+    auto &S = g.sched[which];
+    if (S.unit_blocks == blocks) return PR_OK;
+    Ctx &ctx = *g.ctx;
+    cudaStream_t st = ctx.stream;
+    int64_t cum[4];
+    const int64_t marks[4] = {S.n_hub, S.n_hub + S.n_warp, S.count, 0};
+    for (int i = 0; i < 3; ++i)
+        PR_CUDA(cudaMemcpyAsync(&cum[i], S.row_cum.as<int64_t>() + marks[i], 8, cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaStreamSynchronize(st));
+    const int64_t cw = cum[1] - cum[0], ct = cum[2] - cum[1];
+    int64_t T = (cw + ct) / (blocks * UNITS_PER_BLOCK);
+    if (T < 256 * ROW_COST) T = 256 * ROW_COST;
+    const int64_t kw = S.n_warp ? (cw + T - 1) / T : 0, kt = (S.count - S.n_hub - S.n_warp) ? (ct + T - 1) / T : 0;
+    S.n_units = S.n_chunks + kw + kt;
+    PR_TRY(ensure(S.units, 8 * (S.n_units + 1)));
+    int2 *U = S.units.as<int2>();
+    if (S.n_hub)
+        k_hub_units<<<grid_for(S.n_hub, 256), 256, 0, st>>>(S.chunk_base.as<int64_t>(), S.n_hub, U);
+    if (kw)
+        k_range_units<<<grid_for(kw, 256), 256, 0, st>>>(S.row_cum.as<int64_t>(), S.n_hub, S.n_hub + S.n_warp, kw,
+                                                        U + S.n_chunks);
+    if (kt)
+        k_range_units<<<grid_for(kt, 256), 256, 0, st>>>(S.row_cum.as<int64_t>(), S.n_hub + S.n_warp, S.count, kt,
+                                                        U + S.n_chunks + kw);
+    PR_CUDA(cudaGetLastError());
+    S.unit_blocks = blocks;
+    return PR_OK;
+}
+
+int ensure_sched(Graph &g, int which) {
     auto &S = g.sched[which];
     if (S.built) return PR_OK;
     Ctx &ctx = *g.ctx;
     cudaStream_t st = ctx.stream;
     int64_t n = g.n;
-    DevBuf dcount, len;
-    PR_TRY(ensure(dcount, 8));
+    DevBuf dcount, len, unsorted, keys, keys2;
+    PR_TRY(ensure(dcount, 16));
+    PR_TRY(ensure(unsorted, 4 * n));
     PR_TRY(ensure(S.ids, 4 * n));
     auto first = thrust::make_counting_iterator<int32_t>(0);
     int mode = which;
     PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
-        return cub::DeviceSelect::If(t, b, first, S.ids.as<int32_t>(), dcount.as<int64_t>(), (int)n,
+        return cub::DeviceSelect::If(t, b, first, unsorted.as<int32_t>(), dcount.as<int64_t>(), (int)n,
                                      RowMember{g.in_off.as<int64_t>(), g.out_deg.as<int32_t>(), mode}, st);
     }));
     int64_t cnt = 0;
     PR_CUDA(cudaMemcpyAsync(&cnt, dcount.ptr, 8, cudaMemcpyDeviceToHost, st));
     PR_CUDA(cudaStreamSynchronize(st));
     S.count = cnt;
-    // compacted CSC offsets
+    // rows by descending in-degree (stable)
+    PR_TRY(ensure(keys, 4 * (cnt ? cnt : 1)));
+    PR_TRY(ensure(keys2, 4 * (cnt ? cnt : 1)));
+    if (cnt) {
+        k_deg_keys<<<grid_for(cnt, 256) > 4096 ? 4096 : grid_for(cnt, 256), 256, 0, st>>>(
+            unsorted.as<int32_t>(), cnt, g.in_off.as<int64_t>(), keys.as<unsigned>());
+        PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, keys.as<unsigned>(), keys2.as<unsigned>(),
+                                                   unsorted.as<int32_t>(), S.ids.as<int32_t>(), (int)cnt, 0, 32, st);
+        }));
+    }
+    // compacted CSC in row order
     PR_TRY(ensure(len, 8 * (cnt + 1)));
     PR_TRY(ensure(S.doff, 8 * (cnt + 1)));
-    k_row_len<<<grid_for(cnt + 1, 256) > 4096 ? 4096 : grid_for(cnt + 1, 256), 256, 0, st>>>(
-        S.ids.as<int32_t>(), cnt, g.in_off.as<int64_t>(), len.as<int64_t>());
+    unsigned gc = grid_for(cnt + 1, 256) > 4096 ? 4096 : grid_for(cnt + 1, 256);
+    k_row_len<<<gc, 256, 0, st>>>(S.ids.as<int32_t>(), cnt, g.in_off.as<int64_t>(), len.as<int64_t>());
     PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
         return cub::DeviceScan::ExclusiveSum(t, b, len.as<int64_t>(), S.doff.as<int64_t>(), (int)(cnt + 1), st);
     }));
@@ -152,39 +192,45 @@ int ensure_sched(Graph &g, int which, int64_t target_warps) {
     PR_CUDA(cudaStreamSynchronize(st));
     S.edges = edges;
     PR_TRY(ensure(S.csc, 4 * (edges + CSC_PAD)));
-    size_t flag_words = (size_t)((edges + CSC_PAD) / 32 + 2);
-    PR_TRY(ensure(S.flags, 4 * flag_words));
     PR_CUDA(cudaMemsetAsync(S.csc.ptr, 0, 4 * (edges + CSC_PAD), st));
-    PR_CUDA(cudaMemsetAsync(S.flags.ptr, 0, 4 * flag_words, st));
     if (cnt) {
         unsigned gr = grid_for(cnt * 32, 256);
         if (gr > (unsigned)ctx.sm_count * 32) gr = ctx.sm_count * 32;
         k_fill_csc<<<gr, 256, 0, st>>>(S.ids.as<int32_t>(), cnt, g.in_off.as<int64_t>(), g.in_src.as<int32_t>(),
-                                       S.doff.as<int64_t>(), S.csc.as<int32_t>(), S.flags.as<unsigned>());
+                                       S.doff.as<int64_t>(), S.csc.as<int32_t>());
     }
-    // merge-path ranges of equal weight, ~RANGES_PER_WARP per warp of the gather grid
-    int64_t target = (target_warps > 0 ? target_warps : (int64_t)ctx.sm_count * 24) * RANGES_PER_WARP;
-    const int64_t weight = edges + RANGE_ALPHA * cnt;
-    int64_t W = (weight + target - 1) / target;
-    if (W < 64 * (RANGE_ALPHA + 1)) W = 64 * (RANGE_ALPHA + 1);
-    S.ew = W;
-    S.n_ranges = edges ? (weight + W - 1) / W : 0;
-    PR_TRY(ensure(S.rrow, 4 * (S.n_ranges + 1)));
-    PR_TRY(ensure(S.rstart, 8 * (S.n_ranges + 1)));
-    if (cnt) {
-        unsigned gc = grid_for(S.n_ranges + 1, 256);
-        k_range_split<<<gc, 256, 0, st>>>(S.doff.as<int64_t>(), cnt, edges, W, S.n_ranges, S.rstart.as<int64_t>(),
-                                          S.rrow.as<int32_t>());
-    }
-    PR_TRY(ensure(S.rsplit, 8 * (S.n_ranges + 1)));
-    if (cnt && S.n_ranges)
-        k_range_bounds<<<grid_for(S.n_ranges, 256), 256, 0, st>>>(S.doff.as<int64_t>(), S.rstart.as<int64_t>(),
-                                                                   S.rrow.as<int32_t>(), cnt, S.n_ranges,
-                                                                   S.rsplit.as<int2>());
-    PR_TRY(ensure(S.row_cnt, 4 * (cnt ? cnt : 1)));
-    PR_CUDA(cudaMemsetAsync(S.row_cnt.ptr, 0, 4 * (cnt ? cnt : 1), st));
-    PR_TRY(ensure(S.lead, 8 * (S.n_ranges ? S.n_ranges : 1)));
-    PR_TRY(ensure(S.trail, 8 * (S.n_ranges ? S.n_ranges : 1)));
+    // bins
+    PR_CUDA(cudaMemsetAsync(dcount.ptr, 0, 16, st));
+    if (cnt)
+        k_count_above<<<gc, 256, 0, st>>>(S.doff.as<int64_t>(), cnt, THREAD_DEG, HUB_DEG,
+                                          dcount.as<unsigned long long>());
+    unsigned long long above[2] = {0, 0};
+    PR_CUDA(cudaMemcpyAsync(above, dcount.ptr, 16, cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaStreamSynchronize(st));
+    S.n_hub = (int64_t)above[1];
+    S.n_warp = (int64_t)above[0] - S.n_hub;
+    DevBuf nch;
+    DevBuf &cbase = S.chunk_base;
+    PR_TRY(ensure(nch, 8 * (S.n_hub + 1)));
+    PR_TRY(ensure(cbase, 8 * (S.n_hub + 1)));
+    k_chunks_of<<<grid_for(S.n_hub + 1, 256), 256, 0, st>>>(S.doff.as<int64_t>(), S.n_hub, nch.as<int64_t>());
+    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, nch.as<int64_t>(), cbase.as<int64_t>(), (int)(S.n_hub + 1), st);
+    }));
+    PR_CUDA(cudaMemcpyAsync(&S.n_chunks, cbase.as<int64_t>() + S.n_hub, 8, cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaStreamSynchronize(st));
+    PR_TRY(ensure(S.chunk_part, 8 * (S.n_chunks + 1)));
+    PR_TRY(ensure(S.row_cnt, 4 * (S.n_hub + 1)));
+    PR_CUDA(cudaMemsetAsync(S.row_cnt.ptr, 0, 4 * (S.n_hub + 1), st));
+    // row cost prefix (unit sizing, ensure_units)
+    DevBuf rcost;
+    PR_TRY(ensure(rcost, 8 * (cnt + 1)));
+    PR_TRY(ensure(S.row_cum, 8 * (cnt + 1)));
+    k_row_cost<<<gc, 256, 0, st>>>(S.doff.as<int64_t>(), cnt, rcost.as<int64_t>());
+    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, rcost.as<int64_t>(), S.row_cum.as<int64_t>(), (int)(cnt + 1), st);
+    }));
+    S.unit_blocks = 0;
     // power: in-degree-0 vertices; engines: round-0 scatter seeds
     PR_TRY(ensure(S.zero_ids, 4 * n));
     if (which == 2) {

@@ -1,0 +1,113 @@
+// ubench.cu -- microbenchmarks of the gather pattern (diagnostics only; not
+// part of the engine).  pr_debug_gather runs variants of a pure gather-sum
+// over the run layout's compacted CSC (IFP2 schedule) to separate the
+// memory system's limit from the segmented-reduction overhead.
+#include <cstring>
+
+#include "internal.cuh"
+
+namespace pr {
+
+// v0: thread-contiguous 8 edges, 16B index loads, 8 independent gathers
+__global__ void ub_gather8(const int32_t *__restrict__ csc, int64_t edges, const double *__restrict__ x,
+                           double *__restrict__ out) {
+    double acc = 0.0;
+    for (int64_t e0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 8; e0 < edges;
+         e0 += (int64_t)gridDim.x * blockDim.x * 8) {
+        const int4 *p = reinterpret_cast<const int4 *>(csc + e0);
+        int4 a = __ldg(p), b = __ldg(p + 1);
+        int idx[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (e0 + q < edges) acc += __ldg(&x[idx[q]]);
+    }
+    if (acc == 123.456) out[0] = acc;
+}
+
+// v1: as v0 but 16 edges per thread per step (16 gathers in flight)
+__global__ void ub_gather16(const int32_t *__restrict__ csc, int64_t edges, const double *__restrict__ x,
+                            double *__restrict__ out) {
+    double acc = 0.0;
+    for (int64_t e0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 16; e0 < edges;
+         e0 += (int64_t)gridDim.x * blockDim.x * 16) {
+        const int4 *p = reinterpret_cast<const int4 *>(csc + e0);
+        int4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2), d = __ldg(p + 3);
+        int idx[16] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w, d.x, d.y, d.z, d.w};
+        double t[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) t[q] = e0 + q < edges ? __ldg(&x[idx[q]]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc += t[q];
+    }
+    if (acc == 123.456) out[0] = acc;
+}
+
+// v2: coalesced lane-interleaved (e = base + lane + 32q), 8 per lane
+__global__ void ub_gather_lanes(const int32_t *__restrict__ csc, int64_t edges, const double *__restrict__ x,
+                                double *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    double acc = 0.0;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = warp * 256; base < edges; base += nw * 256) {
+        int idx[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) idx[q] = base + lane + 32 * q < edges ? __ldg(&csc[base + lane + 32 * q]) : -1;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (idx[q] >= 0) acc += __ldg(&x[idx[q]]);
+    }
+    if (acc == 123.456) out[0] = acc;
+}
+
+// v3: index stream only (no gathers): the CSC read bound
+__global__ void ub_stream(const int32_t *__restrict__ csc, int64_t edges, double *__restrict__ out) {
+    int acc = 0;
+    for (int64_t e0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 8; e0 < edges;
+         e0 += (int64_t)gridDim.x * blockDim.x * 8) {
+        const int4 *p = reinterpret_cast<const int4 *>(csc + e0);
+        int4 a = __ldg(p), b = __ldg(p + 1);
+        acc += a.x ^ a.y ^ a.z ^ a.w ^ b.x ^ b.y ^ b.z ^ b.w;
+    }
+    if (acc == 123456789) out[0] = acc;
+}
+
+int debug_gather(Graph &g0, int variant, int iters, int blocks_per_sm, double *ms_out) {
+    PR_TRY(ensure_run_layout(g0));
+    Graph &g = *g0.run;
+    PR_TRY(preprocess_ifp2_device(g));
+    PR_TRY(ensure_sched(g, 1));
+    auto &S = g.sched[1];
+    Ctx &ctx = *g.ctx;
+    cudaStream_t st = ctx.stream;
+    DevBuf x, out;
+    PR_TRY(ensure(x, 8 * g.n));
+    PR_TRY(ensure(out, 8));
+    PR_CUDA(cudaMemsetAsync(x.ptr, 0, 8 * g.n, st));
+    unsigned grid = (unsigned)(ctx.sm_count * (blocks_per_sm > 0 ? blocks_per_sm : 8));
+    cudaEvent_t e0, e1;
+    PR_CUDA(cudaEventCreate(&e0));
+    PR_CUDA(cudaEventCreate(&e1));
+    for (int rep = 0; rep < 2; ++rep) {
+        PR_CUDA(cudaEventRecord(e0, st));
+        for (int it = 0; it < iters; ++it) {
+            switch (variant) {
+            case 0: ub_gather8<<<grid, 256, 0, st>>>(S.csc.as<int32_t>(), S.edges, x.as<double>(), out.as<double>()); break;
+            case 1: ub_gather16<<<grid, 256, 0, st>>>(S.csc.as<int32_t>(), S.edges, x.as<double>(), out.as<double>()); break;
+            case 2: ub_gather_lanes<<<grid, 256, 0, st>>>(S.csc.as<int32_t>(), S.edges, x.as<double>(), out.as<double>()); break;
+            default: ub_stream<<<grid, 256, 0, st>>>(S.csc.as<int32_t>(), S.edges, out.as<double>()); break;
+            }
+        }
+        PR_CUDA(cudaEventRecord(e1, st));
+        PR_CUDA(cudaEventSynchronize(e1));
+    }
+    float ms = 0.f;
+    PR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms_out = ms / iters;
+    return PR_OK;
+}
+
+}  // namespace pr
+
