@@ -141,6 +141,7 @@ struct Graph {
     int64_t rows_cap = 0;
     int64_t max_blocks = 0;     // partial slots per region (partials holds 3 regions)
     int64_t n_dangling = -1;    // #(out_degree == 0), computed lazily
+    int64_t settle_big = -1;    // leading dangling vertices with > 32 sources (run layout)
     DevBuf pw;                // power-method workspace
     // Run layout of the fast engines (graph.cu): the same graph with
     // vertices renumbered by class (in>0&out>0 | out>0&in=0 | out=0&in>0 |
@@ -182,10 +183,16 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
 constexpr int TILE = 256;   // edges per warp tile (long rows are cut into TILE chunks)
 constexpr int CSC_PAD = 1024;  // int32 padding past the compacted CSC for vector loads
 constexpr int64_t THREAD_DEG = 32;   // rows up to this in-degree: one thread each
-constexpr int64_t HUB_DEG = 4096;    // rows above: cut into HUB_CHUNK-edge block units
-constexpr int64_t HUB_CHUNK = 4096;  // edges per hub unit (256 threads x 16)
-constexpr int64_t ROW_COST = 8;      // per-row drain cost in edge units (unit sizing)
-constexpr int64_t UNITS_PER_BLOCK = 4;  // target work units per block of the persistent grid
+#ifndef PR_HUB_CHUNK
+#define PR_HUB_CHUNK 4096
+#endif
+#ifndef PR_UNITS_PB
+#define PR_UNITS_PB 8
+#endif
+constexpr int64_t HUB_DEG = PR_HUB_CHUNK;      // rows above: cut into HUB_CHUNK-edge block units
+constexpr int64_t HUB_CHUNK = PR_HUB_CHUNK;    // edges per hub unit (256 threads x HUB_CHUNK/256)
+constexpr int64_t ROW_COST = 8;                // per-row drain cost in edge units (unit sizing)
+constexpr int64_t UNITS_PER_BLOCK = PR_UNITS_PB;  // target work units per block of the persistent grid
 
 // PUSHRANK_TIMING=1: host-side phase timings (synchronising) on stderr
 void phase_mark(cudaStream_t st, const char *what);

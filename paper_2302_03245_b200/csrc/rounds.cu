@@ -478,10 +478,13 @@ __global__ void k_ex_pull(RunArgs A) {
 // ---------------------------------------------------------------- settle + normalise (K7)
 
 // engines.py:269-289: reserved[d] = h[d] + sum_{u in S(d)} (c*reserved[u])/deg[u]
-__global__ void k_settle(RunArgs A, const int32_t *dang_ids, int64_t nd, const int64_t *src_off,
-                         const int32_t *src_ids, int exact) {
-    if (exact) {
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd; i += (int64_t)gridDim.x * blockDim.x) {
+// Dangling vertices [lo, hi): thread per vertex (sequential, ascending
+// source order) when `thread_mode`, else warp per vertex (fixed tree).
+__global__ void k_settle(RunArgs A, const int32_t *dang_ids, int64_t lo, int64_t nd, const int64_t *src_off,
+                         const int32_t *src_ids, int thread_mode) {
+    if (thread_mode) {
+        for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd;
+             i += (int64_t)gridDim.x * blockDim.x) {
             double acc = 0.0;
             for (int64_t e = src_off[i]; e < src_off[i + 1]; ++e) {
                 int32_t u = src_ids[e];
@@ -496,7 +499,7 @@ __global__ void k_settle(RunArgs A, const int32_t *dang_ids, int64_t nd, const i
     int lane = threadIdx.x & 31;
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < nd; i += nwarps) {
+    for (int64_t i = lo + warp; i < nd; i += nwarps) {
         double acc = 0.0;
         for (int64_t e = src_off[i] + lane; e < src_off[i + 1]; e += 32) {
             int32_t u = src_ids[e];
@@ -509,6 +512,29 @@ __global__ void k_settle(RunArgs A, const int32_t *dang_ids, int64_t nd, const i
             A.h[d] = 0.0;
         }
     }
+}
+
+// first index of dangling vertices with <= 32 sources (run layout: receivers
+// sorted by descending in-degree, so the big ones lead)
+__global__ void k_count_big(const int64_t *src_off, int64_t nd, unsigned long long *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd; i += (int64_t)gridDim.x * blockDim.x)
+        if (src_off[i + 1] - src_off[i] > 32) atomicAdd(out, 1ull);
+}
+
+static int count_settle_big(Graph &g, int64_t *big) {
+    if (g.settle_big < 0) {
+        DevBuf c;
+        PR_TRY(ensure(c, 8));
+        PR_CUDA(cudaMemsetAsync(c.ptr, 0, 8, g.ctx->stream));
+        k_count_big<<<grid_for(g.ifp2.dangling, 256) > 2048 ? 2048 : grid_for(g.ifp2.dangling, 256), 256, 0,
+                      g.ctx->stream>>>(g.src_off.as<int64_t>(), g.ifp2.dangling, c.as<unsigned long long>());
+        unsigned long long h = 0;
+        PR_CUDA(cudaMemcpyAsync(&h, c.ptr, 8, cudaMemcpyDeviceToHost, g.ctx->stream));
+        PR_CUDA(cudaStreamSynchronize(g.ctx->stream));
+        g.settle_big = (int64_t)h;
+    }
+    *big = g.settle_big;
+    return PR_OK;
 }
 
 // total mass (deterministic; x = reserved [+ h]) and, for IFP2, the
@@ -892,9 +918,19 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     if (algo == PR_ALGO_IFP2) {
         settled = g.ifp2.source_edges;
         if (g.ifp2.dangling)
-            k_settle<<<exact ? grid_for(g.ifp2.dangling, 256) : grid_for(g.ifp2.dangling * 32, 256), 256, 0, st>>>(
-                A, g.dang_ids.as<int32_t>(), g.ifp2.dangling, g.src_off.as<int64_t>(), g.src_ids.as<int32_t>(),
-                exact ? 1 : 0);
+        {
+            // exact: thread per vertex in ascending source order; fast: a warp
+            // for each dangling vertex with > 32 sources, a thread for the rest
+            const int64_t nd = g.ifp2.dangling;
+            int64_t big = 0;
+            if (!exact) PR_TRY(count_settle_big(g, &big));
+            if (big)
+                k_settle<<<grid_for(big * 32, 256), 256, 0, st>>>(A, g.dang_ids.as<int32_t>(), 0, big,
+                                                                  g.src_off.as<int64_t>(), g.src_ids.as<int32_t>(), 0);
+            if (nd > big)
+                k_settle<<<grid_for(nd - big, 256), 256, 0, st>>>(A, g.dang_ids.as<int32_t>(), big, nd,
+                                                                   g.src_off.as<int64_t>(), g.src_ids.as<int32_t>(), 1);
+        }
     }
     int include_h = algo == PR_ALGO_IFP1 ? 1 : 0;
     k_total<<<P.g_all, 256, 0, st>>>(A, include_h, settled, algo == PR_ALGO_IFP2 ? 1 : 0);
