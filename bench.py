@@ -190,6 +190,8 @@ def run_ours(args):
     cls = P.classify(g)
     pg = P.preprocess_ifp2(g, cls)
     preprocess_s = time.perf_counter() - t0
+    if world > 1:
+        return run_partitioned_bench(args, g, rank, world, local, preprocess_s)
     dev = g.dev
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
@@ -267,6 +269,56 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
+    """N > 1: vertex-range partitions, one per rank, NCCL all-gather of shares
+    per round (paper_2302_03245_b200/distributed.py, csrc/part.cu).  Each rank
+    holds the same global graph here (built on its own GPU) and keeps only its
+    partition for the run.  Time = max over ranks of the solve, measured with
+    CUDA-synchronised barriers on both sides."""
+    import torch
+    import torch.distributed as dist
+    from paper_2302_03245_b200 import distributed as D
+    host = __import__("oracle").graph_arrays(g)
+    part = D.partition_graph(host, world, rank, args.algo)
+    comm = D.Comm(device=torch.device("cuda", local))
+
+    def solve():
+        step = D.CudaLocalStep(part, DAMPING, XI, args.algo, device=local)
+        vals, rows, info = D.run_partitioned(step, comm, part, args.algo, DAMPING, XI)
+        return vals, info
+
+    for _ in range(args.warmup):
+        solve()
+    times, info = [], None
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            vals, info = solve()
+            torch.cuda.synchronize()
+            dist.barrier()
+            times.append(time.perf_counter() - t0)
+    t = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_s = float(t.item())
+    value = info["push_ops"] * args.steps / total_s / 1e9
+    if rank == 0:
+        line = {"metric": "GTEPS", "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": dict(config_desc(args, g.n, g.m), parallelism=f"vertex-range x{world}"),
+                "rounds": info["rounds"], "push_ops_per_step": info["push_ops"], "preprocess_s": preprocess_s,
+                "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": int(part.in_sources.nbytes +
+                                                                                  part.in_offsets.nbytes),
+                        "d2h_bytes_per_step": int(8 * part.owned),
+                        "path": "per step: partition upload (pr_part_create) + rounds + owned values D2H"},
+                "gpu_launches": int(2 * (info["rounds"] + 2)), "clocks": clocks.summary(),
+                "note": "host-driven partitioned rounds; exchange = NCCL all-gather of shares per round"}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 def e2e_measure(args, g, dev_resident):

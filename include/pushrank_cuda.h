@@ -189,6 +189,30 @@ int pr_rmat_generate(pr_ctx *ctx, int scale, int64_t edge_factor, double a, doub
 int pr_graph_rmat(pr_ctx *ctx, int scale, int64_t edge_factor, double a, double b, double c,
                   uint64_t seed, pr_graph **out);
 
+/* ---- vertex-range partitions (multi-GPU) ---------------
+ * Local step of the bulk-synchronous partitioned rounds driven by
+ * paper_2302_03245_b200/distributed.py: the rank owns `owned` vertices and
+ * their in-edge rows, with source ids in a padded global space (rank r at
+ * [r*slot, r*slot + owned_r)).  Shares are exchanged by the caller (NCCL
+ * all-gather) between calls; d_* pointers are device memory.  Statistics:
+ * ints = {active, work, push_ops, push_ops_dangling, converged_all,
+ * converged_scan}, floats = {h_l1, active_mass, nd_active_mass} -- the
+ * caller all-reduces them into the TraceSample row (engines.py:421-435). */
+typedef struct pr_part pr_part;
+int pr_part_create(pr_ctx *ctx, int64_t owned, int64_t slot, const int64_t *in_offsets,
+                   const int64_t *in_sources, int64_t edges, const int64_t *out_degree,
+                   const int64_t *row_len, const int64_t *dangling_target_counts,
+                   const uint8_t *dangling, const uint8_t *receives, int32_t algorithm,
+                   double damping, double threshold, pr_part **out);
+int pr_part_init(pr_part *p, double *d_shares_mine, int64_t *ints, double *floats);
+int pr_part_round(pr_part *p, const double *d_shares_full, double *d_shares_mine, int64_t *ints,
+                  double *floats);
+int pr_part_settle_shares(pr_part *p, double *d_x_mine);
+int pr_part_settle(pr_part *p, const double *d_x_full, int64_t *settled, int64_t *ints, double *floats);
+int pr_part_total(pr_part *p, int32_t include_pending, double *total);
+int pr_part_export(pr_part *p, double *reserved, double *pending);
+int pr_part_destroy(pr_part *p);
+
 /* ---- device buffers (for torch-free hosts and tests) ---------------------- */
 int pr_device_alloc(pr_ctx *ctx, int64_t bytes, void **d_ptr);
 int pr_device_free(pr_ctx *ctx, void *d_ptr);

@@ -99,6 +99,15 @@ SIGNATURES = {
                                         ctypes.c_uint64, c_i64, c_i64, c_vp, c_vp]),
     "pr_graph_rmat": (ctypes.c_int, [c_vp, ctypes.c_int, c_i64, c_f64, c_f64, c_f64, ctypes.c_uint64,
                                      _PP]),
+    "pr_part_create": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                       c_i32, c_f64, c_f64, _PP]),
+    "pr_part_init": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "pr_part_round": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "pr_part_settle_shares": (ctypes.c_int, [c_vp, c_vp]),
+    "pr_part_settle": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "pr_part_total": (ctypes.c_int, [c_vp, c_i32, ctypes.POINTER(c_f64)]),
+    "pr_part_export": (ctypes.c_int, [c_vp, c_vp, c_vp]),
+    "pr_part_destroy": (ctypes.c_int, [c_vp]),
     "pr_device_alloc": (ctypes.c_int, [c_vp, c_i64, _PP]),
     "pr_device_free": (ctypes.c_int, [c_vp, c_vp]),
     "pr_memcpy_h2d": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64]),

@@ -42,6 +42,18 @@ int export_graph(Graph &g, int64_t *out_off, int64_t *out_tgt, int64_t *in_off, 
 int export_i32(Ctx &ctx, const DevBuf &src, int64_t count, int64_t *host);
 int export_i64(Ctx &ctx, const DevBuf &src, int64_t count, int64_t *host);
 int debug_gather(Graph &g0, int variant, int iters, int blocks_per_sm, double *ms_out);
+struct Part;
+int part_create(Ctx &ctx, int64_t owned, int64_t slot, const int64_t *in_off, const int64_t *in_src, int64_t edges,
+                const int64_t *deg, const int64_t *row_len, const int64_t *dtc, const uint8_t *dang,
+                const uint8_t *recv, int algorithm, double c, double xi, Part **out);
+int part_init(Part &P, double *d_s_mine, int64_t *ints, double *floats);
+int part_round(Part &P, const double *d_s_full, double *d_s_mine, int64_t *ints, double *floats);
+int part_settle_shares(Part &P, double *d_x_mine);
+int part_settle(Part &P, const double *d_x_full, int64_t *settled, int64_t *ints, double *floats);
+int part_total(Part &P, int include_h, double *total);
+int part_export(Part &P, double *reserved, double *pending);
+void part_destroy(Part *P);
+Ctx &part_ctx(Part &P);
 
 static int set_device(Ctx &ctx) {
     PR_CUDA(cudaSetDevice(ctx.device));
@@ -372,6 +384,61 @@ int pr_memcpy_d2h(pr_ctx *ctx, void *h_dst, const void *d_src, int64_t bytes) {
     PR_TRY(set_device(ctx->c));
     PR_CUDA(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, ctx->c.stream));
     PR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    return PR_OK;
+}
+
+struct pr_part {
+    Part *p;
+};
+
+int pr_part_create(pr_ctx *ctx, int64_t owned, int64_t slot, const int64_t *in_offsets, const int64_t *in_sources,
+                   int64_t edges, const int64_t *out_degree, const int64_t *row_len,
+                   const int64_t *dangling_target_counts, const uint8_t *dangling, const uint8_t *receives,
+                   int32_t algorithm, double damping, double threshold, pr_part **out) {
+    CHECK_PTR(ctx, "ctx");
+    CHECK_PTR(out, "out");
+    CHECK_PTR(in_offsets, "in_offsets");
+    PR_TRY(set_device(ctx->c));
+    Part *P = nullptr;
+    PR_TRY(part_create(ctx->c, owned, slot, in_offsets, in_sources, edges, out_degree, row_len,
+                       dangling_target_counts, dangling, receives, algorithm, damping, threshold, &P));
+    *out = new pr_part{P};
+    return PR_OK;
+}
+
+#define PART_ENTER(p)            \
+    CHECK_PTR(p, "partition");   \
+    PR_TRY(set_device(part_ctx(*(p)->p)))
+
+int pr_part_init(pr_part *p, double *d_shares_mine, int64_t *ints, double *floats) {
+    PART_ENTER(p);
+    return part_init(*p->p, d_shares_mine, ints, floats);
+}
+int pr_part_round(pr_part *p, const double *d_shares_full, double *d_shares_mine, int64_t *ints, double *floats) {
+    PART_ENTER(p);
+    return part_round(*p->p, d_shares_full, d_shares_mine, ints, floats);
+}
+int pr_part_settle_shares(pr_part *p, double *d_x_mine) {
+    PART_ENTER(p);
+    return part_settle_shares(*p->p, d_x_mine);
+}
+int pr_part_settle(pr_part *p, const double *d_x_full, int64_t *settled, int64_t *ints, double *floats) {
+    PART_ENTER(p);
+    return part_settle(*p->p, d_x_full, settled, ints, floats);
+}
+int pr_part_total(pr_part *p, int32_t include_pending, double *total) {
+    PART_ENTER(p);
+    return part_total(*p->p, include_pending, total);
+}
+int pr_part_export(pr_part *p, double *reserved, double *pending) {
+    PART_ENTER(p);
+    return part_export(*p->p, reserved, pending);
+}
+int pr_part_destroy(pr_part *p) {
+    if (!p) return PR_OK;
+    set_device(part_ctx(*p->p));
+    part_destroy(p->p);
+    delete p;
     return PR_OK;
 }
 

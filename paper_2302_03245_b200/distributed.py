@@ -274,3 +274,124 @@ class NumpyLocalStep:
     def values(self, total):
         x = self.reserved + self.h if self.algo == "ifp1" else self.reserved
         return x / total
+
+
+class CudaLocalStep:
+    """Production local step: libpushrank_cuda ``pr_part_*`` (csrc/part.cu).
+
+    Exchange tensors may live on the GPU (NCCL; used directly) or on the CPU
+    (gloo; staged through device buffers).  Library calls return with their
+    stream synchronised; torch's stream is synchronised before each call that
+    reads torch-written data.
+    """
+
+    def __init__(self, part: Partition, damping: float, threshold: float, algorithm: str, device=None):
+        import ctypes
+
+        import torch
+
+        from . import _lib
+        self._lib, self._ct, self.torch = _lib, ctypes, torch
+        self.part, self.algo = part, algorithm
+        ctx = _lib.context(device)
+        self.dev = torch.device("cuda", ctx.device)
+        L = _lib.load()
+        self.L = L
+        k = part.owned
+        arr = {
+            "off": np.ascontiguousarray(part.in_offsets, np.int64),
+            "src": np.ascontiguousarray(part.in_sources if part.in_sources.size else np.zeros(1), np.int64),
+            "deg": np.ascontiguousarray(part.out_degree if k else np.zeros(1), np.int64),
+            "len": np.ascontiguousarray(part.row_len if k else np.zeros(1), np.int64),
+            "dtc": np.ascontiguousarray(part.dtc if k else np.zeros(1), np.int64),
+            "dang": np.ascontiguousarray(part.dangling if k else np.zeros(1), np.uint8),
+            "recv": np.ascontiguousarray(part.receives if k else np.zeros(1), np.uint8),
+        }
+        h = ctypes.c_void_p()
+        _lib.check(L.pr_part_create(ctx.handle, k, part.slot, *[_lib.ptr(arr[x]) for x in ("off", "src")],
+                                    int(part.in_sources.size), *[_lib.ptr(arr[x]) for x in
+                                                                 ("deg", "len", "dtc", "dang", "recv")],
+                                    _lib.ALGO[algorithm], float(damping), float(threshold), ctypes.byref(h)),
+                   "pr_part_create")
+        self.h = h
+        self.s_full = torch.zeros(part.slot * part.parts, dtype=torch.float64, device=self.dev)
+        self.s_mine = torch.zeros(part.slot, dtype=torch.float64, device=self.dev)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            self.L.pr_part_destroy(h)
+            self.h = None
+
+    def _sync(self):
+        self.torch.cuda.current_stream(self.dev).synchronize()
+
+    def _stats(self):
+        return np.zeros(6, np.int64), np.zeros(3, np.float64)
+
+    def _out(self, t):
+        return t if t.is_cuda else self.s_mine
+
+    def _back(self, t):
+        if not t.is_cuda:
+            t.copy_(self.s_mine.cpu())
+
+    def init(self, s_mine):
+        ints, floats = self._stats()
+        out = self._out(s_mine)
+        self._sync()
+        self._lib.check(self.L.pr_part_init(self.h, self._ct.c_void_p(out.data_ptr()), self._lib.ptr(ints),
+                                            self._lib.ptr(floats)), "pr_part_init")
+        self._back(s_mine)
+        return ints, floats
+
+    def round(self, t, s_in, s_mine):
+        ints, floats = self._stats()
+        if s_in.is_cuda:
+            src = s_in
+        else:
+            self.s_full.copy_(s_in)
+            src = self.s_full
+        out = self._out(s_mine)
+        self._sync()
+        self._lib.check(self.L.pr_part_round(self.h, self._ct.c_void_p(src.data_ptr()),
+                                             self._ct.c_void_p(out.data_ptr()), self._lib.ptr(ints),
+                                             self._lib.ptr(floats)), "pr_part_round")
+        self._back(s_mine)
+        return ints, floats
+
+    def settle_shares(self, x_mine):
+        out = self._out(x_mine)
+        self._sync()
+        self._lib.check(self.L.pr_part_settle_shares(self.h, self._ct.c_void_p(out.data_ptr())), "settle_shares")
+        self._back(x_mine)
+
+    def settle(self, x_full):
+        ints, floats = self._stats()
+        if x_full.is_cuda:
+            src = x_full
+        else:
+            self.s_full.copy_(x_full)
+            src = self.s_full
+        settled = self._ct.c_int64(0)
+        self._sync()
+        self._lib.check(self.L.pr_part_settle(self.h, self._ct.c_void_p(src.data_ptr()), self._ct.byref(settled),
+                                              self._lib.ptr(ints), self._lib.ptr(floats)), "pr_part_settle")
+        return int(settled.value), ints, floats
+
+    def local_total(self):
+        tot = self._ct.c_double(0.0)
+        self._lib.check(self.L.pr_part_total(self.h, 1 if self.algo == "ifp1" else 0, self._ct.byref(tot)),
+                        "pr_part_total")
+        return float(tot.value)
+
+    def export(self):
+        k = self.part.owned
+        r, h = np.zeros(max(k, 1)), np.zeros(max(k, 1))
+        self._lib.check(self.L.pr_part_export(self.h, self._lib.ptr(r), self._lib.ptr(h)), "pr_part_export")
+        return r[:k], h[:k]
+
+    def values(self, total):
+        r, h = self.export()
+        x = r + h if self.algo == "ifp1" else r
+        return x / total
