@@ -28,6 +28,7 @@ struct BinView {
     int64_t n_units;
     int32_t *row_cnt;
     double *chunk_part;          // per hub chunk unit
+    unsigned long long *unit_ctr;  // dynamic dispatch counter (0 at kernel start)
 };
 
 __device__ __forceinline__ double row_sum_thread(const int32_t *__restrict__ csc, int64_t lo, int64_t hi,
@@ -72,9 +73,17 @@ template <class ThreadRow, class SingleRow>
 __device__ __forceinline__ void bins_run(const BinView &B, const double *__restrict__ x, ThreadRow &thread_row,
                                          SingleRow &single_row) {
     __shared__ double red[8];
+    __shared__ int64_t next_unit;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int64_t warp_rows = B.n_hub + B.n_warp;
-    for (int64_t u = blockIdx.x; u < B.n_units; u += gridDim.x) {
+    // dynamic unit dispatch: first unit = blockIdx.x, then one atomic per unit
+    // (units are ordered heaviest first); the round finaliser resets the counter
+    for (int64_t u = blockIdx.x; u < B.n_units;) {
+#if PR_DYNAMIC_UNITS
+        // claim the following unit now; the atomic's latency hides behind this unit
+        unsigned long long claim = 0;
+        if (tid == 0) claim = atomicAdd(B.unit_ctr, 1ull);
+#endif
         const int2 d = B.units[u];
         if (d.y < 0) {
             // ---- HUB_CHUNK edges of one hub row, whole block
@@ -134,6 +143,14 @@ __device__ __forceinline__ void bins_run(const BinView &B, const double *__restr
                 thread_row(valid, row, s);
             }
         }
+#if PR_DYNAMIC_UNITS
+        if (tid == 0) next_unit = (int64_t)gridDim.x + (int64_t)claim;
+        __syncthreads();
+        u = next_unit;
+        __syncthreads();
+#else
+        u += gridDim.x;
+#endif
     }
 }
 

@@ -80,6 +80,7 @@ struct RunCtl {
     int64_t c_conv_all, c_conv_scan;
     double mass_total;
     int64_t settled;
+    unsigned long long unit_ctr;  // pull-unit dispatch counter (bins.cuh), reset every round
 };
 
 // Per-block partial statistics of one round (reduced in fixed order).
@@ -185,6 +186,9 @@ constexpr int CSC_PAD = 1024;  // int32 padding past the compacted CSC for vecto
 constexpr int64_t THREAD_DEG = 32;   // rows up to this in-degree: one thread each
 #ifndef PR_HUB_CHUNK
 #define PR_HUB_CHUNK 4096
+#endif
+#ifndef PR_DYNAMIC_UNITS
+#define PR_DYNAMIC_UNITS 1
 #endif
 #ifndef PR_UNITS_PB
 #define PR_UNITS_PB 8

@@ -25,6 +25,7 @@ struct PowCtl {
     double total;            // sum(nxt) of the current iteration
     double restart;          // restart coefficient for the current iteration
     double delta;
+    unsigned long long unit_ctr;  // gather-unit dispatch counter (bins.cuh)
 };
 
 struct PowArgs {
@@ -116,7 +117,10 @@ __global__ void __launch_bounds__(256, 4) k_pw_gather(PowArgs A) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.n_zero;
          i += (int64_t)gridDim.x * blockDim.x)
         finish(A.zero_ids[i], 0.0);
-    pow_finish(A, p, [&](const Partial &acc) { A.ctl->total = acc.l1; });
+    pow_finish(A, p, [&](const Partial &acc) {
+        A.ctl->total = acc.l1;
+        A.ctl->unit_ctr = 0;
+    });
 }
 
 // pi' = nxt / total; delta, converged count; next z and dangling sum
@@ -212,6 +216,7 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
     A.conv = (int64_t *)(base + off_c);
     A.partials = (Partial *)(base + off_part);
     A.ctl = (PowCtl *)(base + off_ctl);
+    A.T.unit_ctr = &A.ctl->unit_ctr;
     A.c = damping;
     A.tolerance = tolerance;
     A.threshold = threshold;

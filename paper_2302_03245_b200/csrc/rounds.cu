@@ -189,6 +189,7 @@ __device__ void finalize_row(const RunArgs &A, const Partial &tot, int64_t r, bo
     // record the next state's frontier when a push round is likely after it
     ctl->append = A.policy == PR_MODE_PUSH || (A.policy == PR_MODE_AUTO && (double)tot.work < 4.0 * A.push_work);
     ctl->fsize[(r + 1) & 1] = 0;
+    ctl->unit_ctr = 0;
     ctl->blocks_done = 0;
     __threadfence();
     if (A.use_graph) {
@@ -265,6 +266,7 @@ __global__ void k_reset(RunArgs A) {
     c->c_conv_all = c->c_conv_scan = 0;
     c->mass_total = 0.0;
     c->settled = 0;
+    c->unit_ctr = 0;
 }
 
 // State 0 (h = 1 everywhere, MassState.fresh engines.py:51-54): trace row 0
@@ -828,6 +830,7 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     A.partials = g.partials.as<Partial>();
     A.max_blocks = g.max_blocks;
     A.ctl = g.ctl.as<RunCtl>();
+    A.T.unit_ctr = &A.ctl->unit_ctr;
     A.rows = g.rows.as<pr_round_stats>();
     A.rows_cap = g.rows_cap;
     A.c = p.damping;

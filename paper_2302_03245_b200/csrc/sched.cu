@@ -130,7 +130,7 @@ int ensure_units(Graph &g, int which, int64_t blocks) {
     PR_CUDA(cudaStreamSynchronize(st));
     const int64_t cw = cum[1] - cum[0], ct = cum[2] - cum[1];
     int64_t T = (cw + ct) / (blocks * UNITS_PER_BLOCK);
-    if (T < 384 * ROW_COST) T = 384 * ROW_COST;  // >= 3072: smaller units cost more than they balance
+    if (T < 400 * ROW_COST) T = 400 * ROW_COST;  // >= 3200 edge-units per unit
     const int64_t kw = S.n_warp ? (cw + T - 1) / T : 0, kt = (S.count - S.n_hub - S.n_warp) ? (ct + T - 1) / T : 0;
     S.n_units = S.n_chunks + kw + kt;
     PR_TRY(ensure(S.units, 8 * (S.n_units + 1)));
