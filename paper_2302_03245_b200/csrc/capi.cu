@@ -257,7 +257,7 @@ int pr_dangling_target_counts(pr_graph *g, int64_t *out) {
 int pr_preprocess_ifp2(pr_graph *g, pr_ifp2_counts *counts) {
     CHECK_PTR(g, "graph");
     PR_TRY(set_device(*g->g->ctx));
-    PR_TRY(preprocess_ifp2_device(*g->g));
+    PR_TRY(ifp2_counts_device(*g->g));
     if (counts) *counts = g->g->ifp2;
     return PR_OK;
 }
@@ -266,8 +266,9 @@ int pr_ifp2_export(pr_graph *g, int64_t *live_offsets, int64_t *live_targets, in
                    int64_t *dangling_ids, int64_t *source_offsets, int64_t *source_ids) {
     CHECK_PTR(g, "graph");
     Graph &G = *g->g;
-    if (!G.has_ifp2) return fail(PR_ERR_STATE, "pr_preprocess_ifp2 has not run");
+    if (!G.has_ifp2 && !G.ifp2_counted) return fail(PR_ERR_STATE, "pr_preprocess_ifp2 has not run");
     PR_TRY(set_device(*G.ctx));
+    PR_TRY(preprocess_ifp2_device(G));
     Ctx &c = *G.ctx;
     PR_TRY(export_i64(c, G.live_off, G.n + 1, live_offsets));
     PR_TRY(export_i32(c, G.live_tgt, G.ifp2.live_edges, live_targets));

@@ -370,18 +370,64 @@ int classify_export(Graph &g, int64_t *outs[4]) {
 // ---------------------------------------------------------------- K3
 
 // graph.py:334-340: per-row count of dangling targets
+// warp per 32 consecutive vertices: short rows (<= 32 edges) on their own
+// lane, long rows walked by the whole warp with 4 loads in flight per lane
 __global__ void k_dtc(const int64_t *__restrict__ out_off, const int32_t *__restrict__ out_tgt,
                       const int32_t *__restrict__ out_deg, int64_t n, int32_t *__restrict__ dtc) {
-    GRID_STRIDE(v, n) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w * 32 < n; w += nwarps) {
+        const int64_t v = w * 32 + lane;
+        int64_t lo = 0, hi = 0;
+        if (v < n) {
+            lo = out_off[v];
+            hi = out_off[v + 1];
+        }
+        const bool big = hi - lo > 32;
         int32_t c = 0;
-        for (int64_t e = out_off[v]; e < out_off[v + 1]; ++e) c += out_deg[out_tgt[e]] == 0;
-        dtc[v] = c;
+        if (!big)
+            for (int64_t e = lo; e < hi; ++e) c += __ldg(&out_deg[__ldg(&out_tgt[e])]) == 0;
+        unsigned m = __ballot_sync(0xffffffffu, big);
+        while (m) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
+            const int64_t blo = __shfl_sync(0xffffffffu, lo, j), bhi = __shfl_sync(0xffffffffu, hi, j);
+            int32_t k = 0;
+            for (int64_t e = blo + lane; e < bhi; e += 128) {
+                int t[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) t[q] = e + 32 * q < bhi ? __ldg(&out_tgt[e + 32 * q]) : -1;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) k += t[q] >= 0 && __ldg(&out_deg[t[q]]) == 0;
+            }
+            k = __reduce_add_sync(0xffffffffu, (unsigned)k);
+            if (lane == j) c = k;
+        }
+        if (v < n) dtc[v] = c;
     }
+}
+
+// run layout: the in-edges of the dangling tail [live_end, n) are the CSC
+// suffix, so dtc is a histogram of their sources (edge-parallel, balanced)
+__global__ void k_dtc_tail(const int64_t *__restrict__ in_off, const int32_t *__restrict__ in_src, int64_t live_end,
+                           int64_t n, int32_t *__restrict__ dtc) {
+    const int64_t lo = in_off[live_end], hi = in_off[n];
+    for (int64_t e = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < hi; e += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&dtc[__ldg(&in_src[e])], 1);
 }
 
 int ensure_dtc(Graph &g) {
     if (g.has_dtc) return PR_OK;
     PR_TRY(ensure(g.dtc, 4 * g.n));
+    if (g.live_end >= 0) {
+        PR_CUDA(cudaMemsetAsync(g.dtc.ptr, 0, 4 * g.n, g.ctx->stream));
+        if (g.live_end < g.n)
+            k_dtc_tail<<<gs_grid(*g.ctx, g.m), 256, 0, g.ctx->stream>>>(g.in_off.as<int64_t>(), g.in_src.as<int32_t>(),
+                                                                      g.live_end, g.n, g.dtc.as<int32_t>());
+        PR_CUDA(cudaGetLastError());
+        g.has_dtc = true;
+        return PR_OK;
+    }
     k_dtc<<<gs_grid(*g.ctx, g.n), 256, 0, g.ctx->stream>>>(g.out_off.as<int64_t>(), g.out_tgt.as<int32_t>(),
                                                            g.out_deg.as<int32_t>(), g.n, g.dtc.as<int32_t>());
     PR_CUDA(cudaGetLastError());
@@ -429,6 +475,14 @@ __global__ void k_gather_rows(const int32_t *__restrict__ ids, int64_t count, co
     }
 }
 
+__global__ void k_tail_rows(const int64_t *__restrict__ in_off, int64_t live_end, int64_t nd,
+                            int32_t *__restrict__ ids, int64_t *__restrict__ off) {
+    GRID_STRIDE(i, nd + 1) {
+        if (i < nd) ids[i] = (int32_t)(live_end + i);
+        off[i] = in_off[live_end + i] - in_off[live_end];
+    }
+}
+
 int preprocess_ifp2_device(Graph &g) {
     if (g.has_ifp2) return PR_OK;
     Ctx &ctx = *g.ctx;
@@ -464,35 +518,54 @@ int preprocess_ifp2_device(Graph &g) {
                                                                g.live_tgt.as<int32_t>());
     }
     // dangling ids (ascending) and their source CSR (graph.py:363-367)
-    int64_t nd = 0;
-    PR_TRY(ensure(g.dang_ids, 4 * n));
-    auto vfirst = thrust::make_counting_iterator<int32_t>(0);
-    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
-        return cub::DeviceSelect::If(t, b, vfirst, g.dang_ids.as<int32_t>(), dcount.as<int64_t>(), (int)n,
-                                     IsDangling{g.out_deg.as<int32_t>()}, st);
-    }));
-    PR_CUDA(cudaMemcpyAsync(&nd, dcount.ptr, 8, cudaMemcpyDeviceToHost, st));
-    PR_CUDA(cudaStreamSynchronize(st));
-    PR_TRY(ensure(g.src_off, 8 * (nd + 1)));
-    DevBuf cnt;
-    PR_TRY(ensure(cnt, 8 * (nd + 1)));
-    PR_CUDA(cudaMemsetAsync(cnt.ptr, 0, 8 * (nd + 1), st));
-    if (nd)
-        k_gather_count<<<gs_grid(ctx, nd), 256, 0, st>>>(g.dang_ids.as<int32_t>(), nd, g.in_off.as<int64_t>(),
-                                                         cnt.as<int64_t>());
-    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
-        return cub::DeviceScan::ExclusiveSum(t, b, cnt.as<int64_t>(), g.src_off.as<int64_t>(), (int)(nd + 1), st);
-    }));
-    int64_t md = 0;
-    PR_CUDA(cudaMemcpyAsync(&md, g.src_off.as<int64_t>() + nd, 8, cudaMemcpyDeviceToHost, st));
-    PR_CUDA(cudaStreamSynchronize(st));
-    PR_TRY(ensure(g.src_ids, 4 * (md ? md : 1)));
-    if (md)
-        k_gather_rows<<<gs_grid(ctx, nd * 32), 256, 0, st>>>(g.dang_ids.as<int32_t>(), nd, g.in_off.as<int64_t>(),
-                                                             g.in_src.as<int32_t>(), g.src_off.as<int64_t>(),
-                                                             g.src_ids.as<int32_t>());
-    PR_CUDA(cudaStreamSynchronize(st));
-    PR_CUDA(cudaGetLastError());
+    int64_t nd = 0, md = 0;
+    if (g.live_end >= 0) {
+        // run layout: the dangling vertices are the id tail and their
+        // source rows the CSC suffix -- slices, no selection or gather
+        nd = n - g.live_end;
+        int64_t base = m;
+        if (nd) {
+            PR_CUDA(cudaMemcpyAsync(&base, g.in_off.as<int64_t>() + g.live_end, 8, cudaMemcpyDeviceToHost, st));
+            PR_CUDA(cudaStreamSynchronize(st));
+        }
+        md = m - base;
+        PR_TRY(ensure(g.dang_ids, 4 * (nd ? nd : 1)));
+        PR_TRY(ensure(g.src_off, 8 * (nd + 1)));
+        PR_TRY(ensure(g.src_ids, 4 * (md ? md : 1)));
+        k_tail_rows<<<gs_grid(ctx, nd + 1), 256, 0, st>>>(g.in_off.as<int64_t>(), g.live_end, nd,
+                                                          g.dang_ids.as<int32_t>(), g.src_off.as<int64_t>());
+        if (md)
+            PR_CUDA(cudaMemcpyAsync(g.src_ids.ptr, g.in_src.as<int32_t>() + base, 4 * md, cudaMemcpyDeviceToDevice,
+                                    st));
+    } else {
+        PR_TRY(ensure(g.dang_ids, 4 * n));
+        auto vfirst = thrust::make_counting_iterator<int32_t>(0);
+        PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceSelect::If(t, b, vfirst, g.dang_ids.as<int32_t>(), dcount.as<int64_t>(), (int)n,
+                                         IsDangling{g.out_deg.as<int32_t>()}, st);
+        }));
+        PR_CUDA(cudaMemcpyAsync(&nd, dcount.ptr, 8, cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+        PR_TRY(ensure(g.src_off, 8 * (nd + 1)));
+        DevBuf cnt;
+        PR_TRY(ensure(cnt, 8 * (nd + 1)));
+        PR_CUDA(cudaMemsetAsync(cnt.ptr, 0, 8 * (nd + 1), st));
+        if (nd)
+            k_gather_count<<<gs_grid(ctx, nd), 256, 0, st>>>(g.dang_ids.as<int32_t>(), nd, g.in_off.as<int64_t>(),
+                                                             cnt.as<int64_t>());
+        PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceScan::ExclusiveSum(t, b, cnt.as<int64_t>(), g.src_off.as<int64_t>(), (int)(nd + 1), st);
+        }));
+        PR_CUDA(cudaMemcpyAsync(&md, g.src_off.as<int64_t>() + nd, 8, cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+        PR_TRY(ensure(g.src_ids, 4 * (md ? md : 1)));
+        if (md)
+            k_gather_rows<<<gs_grid(ctx, nd * 32), 256, 0, st>>>(g.dang_ids.as<int32_t>(), nd, g.in_off.as<int64_t>(),
+                                                                 g.in_src.as<int32_t>(), g.src_off.as<int64_t>(),
+                                                                 g.src_ids.as<int32_t>());
+        PR_CUDA(cudaStreamSynchronize(st));
+        PR_CUDA(cudaGetLastError());
+    }
     g.ifp2.live_edges = live_m;
     g.ifp2.dangling = nd;
     g.ifp2.source_edges = md;
@@ -500,26 +573,75 @@ int preprocess_ifp2_device(Graph &g) {
     return PR_OK;
 }
 
-// ---------------------------------------------------------------- run layout
-
-// sort key: class (2 bits) | descending in-degree inside the receiving
-// classes 0 and 2 (31 bits) | id (31 bits)
-__global__ void k_relabel_keys(const int64_t *__restrict__ out_off, const int64_t *__restrict__ in_off, int64_t n,
-                               unsigned long long *__restrict__ keys) {
+// IFP2Graph's three counts without building the split (graph.py:343-378):
+// dangling = #(deg == 0), source_edges = m_d = the dangling vertices'
+// in-degree sum, live_edges = m - m_d (every edge into a dangling vertex is
+// dead).  The fast engines build their split on the run layout; the
+// original-layout arrays are built only when exported or run in exact mode.
+__global__ void k_ifp2_counts(const int32_t *__restrict__ out_deg, const int64_t *__restrict__ in_off, int64_t n,
+                              unsigned long long *acc) {
+    unsigned long long nd = 0, md = 0;
     GRID_STRIDE(v, n) {
-        int64_t od = out_off[v + 1] - out_off[v], id = in_off[v + 1] - in_off[v];
-        unsigned long long cls = od > 0 ? (id > 0 ? 0 : 1) : (id > 0 ? 2 : 3);
-        unsigned long long dk = (cls == 0 || cls == 2) ? (unsigned long long)(0x7FFFFFFFll - id) : 0ull;
-        keys[v] = (cls << 62) | (dk << 31) | (unsigned long long)v;
+        if (out_deg[v] == 0) {
+            nd += 1;
+            md += (unsigned long long)(in_off[v + 1] - in_off[v]);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        nd += __shfl_xor_sync(0xffffffffu, nd, o);
+        md += __shfl_xor_sync(0xffffffffu, md, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (nd) atomicAdd(acc, nd);
+        if (md) atomicAdd(acc + 1, md);
     }
 }
 
-__global__ void k_perm_from_keys(const unsigned long long *__restrict__ keys, int64_t n, int32_t *__restrict__ perm,
-                                 int32_t *__restrict__ rank) {
+int ifp2_counts_device(Graph &g) {
+    if (g.has_ifp2 || g.ifp2_counted) return PR_OK;
+    Ctx &ctx = *g.ctx;
+    cudaStream_t st = ctx.stream;
+    DevBuf acc;
+    PR_TRY(ensure(acc, 2 * sizeof(unsigned long long)));
+    PR_CUDA(cudaMemsetAsync(acc.ptr, 0, 2 * sizeof(unsigned long long), st));
+    if (g.n)
+        k_ifp2_counts<<<gs_grid(ctx, g.n), 256, 0, st>>>(g.out_deg.as<int32_t>(), g.in_off.as<int64_t>(), g.n,
+                                                         acc.as<unsigned long long>());
+    unsigned long long h[2] = {0, 0};
+    PR_CUDA(cudaMemcpyAsync(h, acc.ptr, sizeof(h), cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaStreamSynchronize(st));
+    g.ifp2.dangling = (int64_t)h[0];
+    g.ifp2.source_edges = (int64_t)h[1];
+    g.ifp2.live_edges = g.m - (int64_t)h[1];
+    g.n_dangling = (int64_t)h[0];
+    g.ifp2_counted = true;
+    return PR_OK;
+}
+
+// ---------------------------------------------------------------- run layout
+
+// sort key: class (2 bits) | descending in-degree (clipped to 30 bits)
+// inside the receiving classes 0 and 2; a stable sort of (key, id) pairs
+// keeps ascending ids inside equal keys
+__global__ void k_relabel_keys(const int64_t *__restrict__ out_off, const int64_t *__restrict__ in_off, int64_t n,
+                               uint32_t *__restrict__ keys, int32_t *__restrict__ ids) {
+    GRID_STRIDE(v, n) {
+        int64_t od = out_off[v + 1] - out_off[v], id = in_off[v + 1] - in_off[v];
+        uint32_t cls = od > 0 ? (id > 0 ? 0u : 1u) : (id > 0 ? 2u : 3u);
+        if (id > 0x3FFFFFFF) id = 0x3FFFFFFF;
+        uint32_t dk = (cls == 0 || cls == 2) ? (uint32_t)(0x3FFFFFFF - id) : 0u;
+        keys[v] = (cls << 30) | dk;
+        ids[v] = (int32_t)v;
+    }
+}
+
+// rank = inverse permutation; live_end = first run id of the dangling classes
+__global__ void k_rank_from_perm(const uint32_t *__restrict__ keys, const int32_t *__restrict__ perm, int64_t n,
+                                 int32_t *__restrict__ rank, int64_t *__restrict__ live_end) {
     GRID_STRIDE(i, n) {
-        int32_t v = (int32_t)(keys[i] & 0x7FFFFFFFull);
-        perm[i] = v;
-        rank[v] = (int32_t)i;
+        rank[perm[i]] = (int32_t)i;
+        const bool dang = (keys[i] >> 30) >= 2;
+        if (dang && (i == 0 || (keys[i - 1] >> 30) < 2)) *live_end = i;
     }
 }
 
@@ -534,6 +656,7 @@ __global__ void k_perm_len(const int64_t *__restrict__ off, const int32_t *__res
 }
 
 // warp per new row: copy the old row, renaming its column ids through rank
+// (4 loads in flight per lane on long rows)
 __global__ void k_perm_rows(const int64_t *__restrict__ off, const int32_t *__restrict__ col,
                             const int32_t *__restrict__ perm, const int32_t *__restrict__ rank, int64_t n,
                             const int64_t *__restrict__ noff, int32_t *__restrict__ ncol) {
@@ -543,7 +666,17 @@ __global__ void k_perm_rows(const int64_t *__restrict__ off, const int32_t *__re
     for (int64_t i = warp; i < n; i += nw) {
         int32_t v = perm[i];
         int64_t lo = off[v], len = off[v + 1] - lo, o = noff[i];
-        for (int64_t k = lane; k < len; k += 32) ncol[o + k] = rank[col[lo + k]];
+        for (int64_t k = lane; k < len; k += 128) {
+            int c[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) c[q] = k + 32 * q < len ? __ldg(&col[lo + k + 32 * q]) : -1;
+            int r[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) r[q] = c[q] >= 0 ? __ldg(&rank[c[q]]) : 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (c[q] >= 0) ncol[o + k + 32 * q] = r[q];
+        }
     }
 }
 
@@ -573,19 +706,23 @@ int ensure_run_layout(Graph &g) {
     Ctx &ctx = *g.ctx;
     cudaStream_t st = ctx.stream;
     int64_t n = g.n, m = g.m;
-    DevBuf keys, sorted;
-    PR_TRY(ensure(keys, 8 * n));
-    PR_TRY(ensure(sorted, 8 * n));
+    DevBuf keys, sorted, ids, dl;
+    PR_TRY(ensure(keys, 4 * n));
+    PR_TRY(ensure(sorted, 4 * n));
+    PR_TRY(ensure(ids, 4 * n));
+    PR_TRY(ensure(dl, 8));
     PR_TRY(ensure(g.perm, 4 * n));
     PR_TRY(ensure(g.rank, 4 * n));
     k_relabel_keys<<<gs_grid(ctx, n), 256, 0, st>>>(g.out_off.as<int64_t>(), g.in_off.as<int64_t>(), n,
-                                                   keys.as<unsigned long long>());
+                                                   keys.as<uint32_t>(), ids.as<int32_t>());
     PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
-        return cub::DeviceRadixSort::SortKeys(t, b, keys.as<unsigned long long>(), sorted.as<unsigned long long>(),
-                                              (int)n, 0, 64, st);
+        return cub::DeviceRadixSort::SortPairs(t, b, keys.as<uint32_t>(), sorted.as<uint32_t>(), ids.as<int32_t>(),
+                                               g.perm.as<int32_t>(), (int)n, 0, 32, st);
     }));
-    k_perm_from_keys<<<gs_grid(ctx, n), 256, 0, st>>>(sorted.as<unsigned long long>(), n, g.perm.as<int32_t>(),
-                                                     g.rank.as<int32_t>());
+    const int64_t none = n;
+    PR_CUDA(cudaMemcpyAsync(dl.ptr, &none, 8, cudaMemcpyHostToDevice, st));
+    k_rank_from_perm<<<gs_grid(ctx, n), 256, 0, st>>>(sorted.as<uint32_t>(), g.perm.as<int32_t>(), n,
+                                                      g.rank.as<int32_t>(), dl.as<int64_t>());
     Graph *r = new Graph();
     r->ctx = &ctx;
     r->n = n;
@@ -595,9 +732,14 @@ int ensure_run_layout(Graph &g) {
     if (!rc) rc = permute_adjacency(ctx, g.in_off, g.in_src, g.perm, g.rank, n, m, r->in_off, r->in_src);
     if (!rc) rc = ensure(r->out_deg, 4 * n);
     if (!rc) k_degree<<<gs_grid(ctx, n), 256, 0, st>>>(r->out_off.as<int64_t>(), n, r->out_deg.as<int32_t>());
+    int64_t live_end = n;
+    if (!rc && cudaMemcpyAsync(&live_end, dl.ptr, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        rc = fail(PR_ERR_CUDA, "run layout build failed");
     if (!rc && (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess))
         rc = fail(PR_ERR_CUDA, "run layout build failed");
     if (rc) { delete r; return rc; }
+    r->live_end = live_end;
+    r->n_dangling = n - live_end;
     g.run = r;
     return PR_OK;
 }

@@ -93,6 +93,9 @@ struct Partial {
 struct Graph {
     Ctx *ctx = nullptr;
     int64_t n = 0, m = 0, raw = 0;
+    // run layout only: vertices [live_end, n) are the dangling ones (classes
+    // out=0&in>0, isolated), so their in-edges are the CSC tail
+    int64_t live_end = -1;
     DevBuf out_off;   // int64 [n+1]
     DevBuf out_tgt;   // int32 [m]
     DevBuf out_deg;   // int32 [n]
@@ -106,7 +109,8 @@ struct Graph {
     bool has_dtc = false;
     DevBuf dtc;
     // IFP2 split (pr_preprocess_ifp2)
-    bool has_ifp2 = false;
+    bool has_ifp2 = false;       // split arrays built
+    bool ifp2_counted = false;   // counts known (pr_preprocess_ifp2 ran)
     pr_ifp2_counts ifp2{};
     DevBuf live_off, live_tgt, live_deg;     // int64 [n+1], int32 [live_m], int32 [n]
     DevBuf dang_ids, src_off, src_ids;       // int32 [n_d], int64 [n_d+1], int32 [m_d]
@@ -174,6 +178,7 @@ int build_from_device_edges(Ctx &ctx, int64_t n, const int64_t *d_src, const int
                             int64_t m_raw, Graph **out);
 int classify_device(Graph &g);
 int preprocess_ifp2_device(Graph &g);
+int ifp2_counts_device(Graph &g);
 int run_rounds(Graph &g, const pr_run_params &p, double *d_values, double *d_reserved, double *d_pending,
                pr_round_stats *rows,
                int64_t row_cap, pr_run_result *res);

@@ -275,50 +275,55 @@ __global__ void k_reset(RunArgs A) {
 // every later row (recorded as constants) and their round-0 shares are
 // scattered once by k_seed_scatter.
 __global__ void __launch_bounds__(256) k_init(RunArgs A) {
-    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     Partial p, cst;
     zero(p);
     zero(cst);
-    int items = 0;
-    if (v < A.n) {
-        A.reserved[v] = 0.0;
-        A.s[A.n + v] = 0.0;
-        if (A.in_d[v]) {
-            items = drain_vertex(A, v, 1.0, 0, p);
-        } else {
-            int32_t dv = A.deg[v];
-            bool scan = A.algo == PR_ALGO_FPFULL || dv > 0;
-            bool above = 1.0 > A.xi;
-            p.l1 += 1.0;
-            if (above) {
-                p.above += 1.0;
-                if (dv > 0) p.nd_above += 1.0;
+    const bool app = A.ctl->append != 0;
+    // grid-stride over a capped grid (whole blocks iterate together): few
+    // partials for the last-block reduction
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < A.n; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = base + threadIdx.x;
+        int items = 0;
+        if (v < A.n) {
+            A.reserved[v] = 0.0;
+            A.s[A.n + v] = 0.0;
+            if (A.in_d[v]) {
+                items = drain_vertex(A, v, 1.0, 0, p);
             } else {
-                p.conv_all += 1;
-                if (scan) p.conv_scan += 1;
-            }
-            bool active = above && scan;
-            double after = active ? 0.0 : 1.0;
-            if (active) {
-                A.reserved[v] = A.frac;
-                p.nact += 1;
-                p.work += (int64_t)dv + 1;
-                p.push_ops += A.row_len[v];
-                if (A.dtc) p.push_dang += A.dtc[v];
-            }
-            A.h[v] = after;
-            A.s[v] = 0.0;
-            cst.l1 += after;
-            if (after > A.xi) {
-                cst.above += after;
-                if (dv > 0) cst.nd_above += after;
-            } else {
-                cst.conv_all += 1;
-                if (scan) cst.conv_scan += 1;
+                int32_t dv = A.deg[v];
+                bool scan = A.algo == PR_ALGO_FPFULL || dv > 0;
+                bool above = 1.0 > A.xi;
+                p.l1 += 1.0;
+                if (above) {
+                    p.above += 1.0;
+                    if (dv > 0) p.nd_above += 1.0;
+                } else {
+                    p.conv_all += 1;
+                    if (scan) p.conv_scan += 1;
+                }
+                bool active = above && scan;
+                double after = active ? 0.0 : 1.0;
+                if (active) {
+                    A.reserved[v] = A.frac;
+                    p.nact += 1;
+                    p.work += (int64_t)dv + 1;
+                    p.push_ops += A.row_len[v];
+                    if (A.dtc) p.push_dang += A.dtc[v];
+                }
+                A.h[v] = after;
+                A.s[v] = 0.0;
+                cst.l1 += after;
+                if (after > A.xi) {
+                    cst.above += after;
+                    if (dv > 0) cst.nd_above += after;
+                } else {
+                    cst.conv_all += 1;
+                    if (scan) cst.conv_scan += 1;
+                }
             }
         }
+        append_warp(app, items, (int32_t)v, A.frontier, &A.ctl->fsize[0]);
     }
-    append_warp(A.ctl->append != 0, items, (int32_t)v, A.frontier, &A.ctl->fsize[0]);
     finish_round(A, p, 0, true, true, cst);
 }
 
@@ -403,18 +408,24 @@ __global__ void __launch_bounds__(256) k_push(RunArgs A) {
 
 // Sparse round t, step 2: drain state t+1 over D
 __global__ void __launch_bounds__(256) k_scan(RunArgs A) {
-    int64_t t = A.ctl->round;
-    int64_t r = t + 1;
+    const int64_t t = A.ctl->round;
+    const int64_t r = t + 1;
+    const bool app = A.ctl->append != 0;
+    long long *F = A.frontier + (r & 1) * A.fcap;
+    int64_t *fsize = &A.ctl->fsize[r & 1];
     Partial p;
     zero(p);
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    int items = 0;
-    int32_t v = 0;
-    if (i < A.d_count) {
-        v = __ldg(&A.ids[i]);
-        items = drain_vertex(A, v, A.h[v], r, p);
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < A.d_count;
+         base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        int items = 0;
+        int32_t v = 0;
+        if (i < A.d_count) {
+            v = __ldg(&A.ids[i]);
+            items = drain_vertex(A, v, A.h[v], r, p);
+        }
+        append_warp(app, items, v, F, fsize);
     }
-    append_warp(A.ctl->append != 0, items, v, A.frontier + (r & 1) * A.fcap, &A.ctl->fsize[r & 1]);
     finish_round(A, p, r, true, false, p);
 }
 
@@ -543,22 +554,21 @@ static int count_settle_big(Graph &g, int64_t *big) {
 // post-settle trace row (engines.py:331-335)
 __global__ void __launch_bounds__(256) k_total(RunArgs A, int include_h, int64_t settled, int write_row) {
     __shared__ bool is_last;
-    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     Partial p, x;
     zero(p);
     zero(x);
-    if (v < A.n) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < A.n; v += (int64_t)gridDim.x * blockDim.x) {
         double hv = A.h[v];
-        x.l1 = include_h ? A.reserved[v] + hv : A.reserved[v];
+        x.l1 += include_h ? A.reserved[v] + hv : A.reserved[v];
         int32_t dv = A.deg[v];
         bool scan = A.algo == PR_ALGO_FPFULL || dv > 0;
-        p.l1 = hv;
+        p.l1 += hv;
         if (hv > A.xi) {
-            p.above = hv;
-            if (dv > 0) p.nd_above = hv;
+            p.above += hv;
+            if (dv > 0) p.nd_above += hv;
         } else {
-            p.conv_all = 1;
-            if (scan) p.conv_scan = 1;
+            p.conv_all += 1;
+            if (scan) p.conv_scan += 1;
         }
     }
     block_reduce(p);
@@ -647,7 +657,7 @@ static int add_kernel(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_
 struct Plan {
     RunArgs A;
     bool exact;
-    unsigned g_all, g_pull, g_push, g_scan;
+    unsigned g_all, g_red, g_pull, g_push, g_scan;
 };
 
 static bool same_key(const pr_run_params &a, const pr_run_params &b) {
@@ -684,7 +694,7 @@ static int build_graph(Plan &P, cudaGraph_t *out_g, cudaGraphExec_t *out_exec) {
         PR_TRY(add_kernel(G, &n_init, &n_reset, 1, (void *)k_ex_init, P.g_all, 256, args));
         PR_TRY(add_kernel(G, &n_seed, &n_init, 1, (void *)k_ex_prep, P.g_all, 256, args));
     } else {
-        PR_TRY(add_kernel(G, &n_init, &n_reset, 1, (void *)k_init, P.g_all, 256, args));
+        PR_TRY(add_kernel(G, &n_init, &n_reset, 1, (void *)k_init, P.g_red, 256, args));
         PR_TRY(add_kernel(G, &n_seed, &n_init, 1, (void *)k_seed_scatter, P.g_push, 256, args));
     }
     cudaGraphNodeParams wp = {};
@@ -756,7 +766,7 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     const bool exact = p.mode == PR_MODE_EXACT;
     if (p.on_round && !exact) return fail(PR_ERR_ARG, "on_round observers need PR_MODE_EXACT");
     const bool host_loop = p.host_loop || p.on_round;
-    if (algo == PR_ALGO_IFP2 && !g_in.has_ifp2) return fail(PR_ERR_STATE, "IFP2 needs pr_preprocess_ifp2 first");
+    if (algo == PR_ALGO_IFP2 && !g_in.has_ifp2 && !g_in.ifp2_counted) return fail(PR_ERR_STATE, "IFP2 needs pr_preprocess_ifp2 first");
     // fast engines run on the relabelled layout; exact mode on the original
     Graph *gp = &g_in;
     phase_mark(ctx.stream, "run: enter");
@@ -847,7 +857,11 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     P.exact = exact;
     P.g_all = grid_for(n, 256);
     P.g_pull = (unsigned)pull_blocks;
+    // reducing kernels of the fast engine: capped grid-stride grids (8 blocks/SM)
+    const unsigned g_cap = (unsigned)ctx.sm_count * 8;
+    P.g_red = P.g_all < g_cap ? P.g_all : g_cap;
     P.g_scan = grid_for(S.count, 256);
+    if (P.g_scan > g_cap) P.g_scan = g_cap;
     P.g_push = (unsigned)ctx.sm_count * 8;
 
     PR_CUDA(cudaMemsetAsync(g.in_d.ptr, 0, n, st));
@@ -885,7 +899,7 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
             k_ex_init<<<P.g_all, 256, 0, st>>>(A);
             k_ex_prep<<<P.g_all, 256, 0, st>>>(A);
         } else {
-            k_init<<<P.g_all, 256, 0, st>>>(A);
+            k_init<<<P.g_red, 256, 0, st>>>(A);
             k_seed_scatter<<<P.g_push, 256, 0, st>>>(A);
         }
         std::vector<double> obs_r, obs_h;
@@ -936,7 +950,7 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
         }
     }
     int include_h = algo == PR_ALGO_IFP1 ? 1 : 0;
-    k_total<<<P.g_all, 256, 0, st>>>(A, include_h, settled, algo == PR_ALGO_IFP2 ? 1 : 0);
+    k_total<<<P.g_red, 256, 0, st>>>(A, include_h, settled, algo == PR_ALGO_IFP2 ? 1 : 0);
     {
         unsigned gs = grid_for(n, 256);
         if (gs > 4096) gs = 4096;

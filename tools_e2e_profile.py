@@ -19,8 +19,9 @@ def t():
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 n, src, dst = synthetic.make(cfg)
 g = P.from_edges(n, src, dst)
-host = SimpleNamespace(n=g.n, m=g.m, **{k: np.ascontiguousarray(getattr(g, k)) for k in
-                                        ("out_offsets", "out_targets", "in_offsets", "in_sources")})
+import torch
+host = SimpleNamespace(n=g.n, m=g.m, **{k: torch.from_numpy(np.ascontiguousarray(getattr(g, k))).pin_memory().numpy()
+                                        for k in ("out_offsets", "out_targets", "in_offsets", "in_sources")})
 for it in range(4):
     t0 = t()
     dev = DeviceGraph.upload(host)
