@@ -9,6 +9,7 @@
 #include <cstring>
 
 #include "internal.cuh"
+#include "seg.cuh"
 #include "cubutil.cuh"
 
 namespace pr {
@@ -461,19 +462,7 @@ __global__ void k_gather_count(const int32_t *__restrict__ ids, int64_t count, c
     }
 }
 
-// _gather_rows(in_offsets, in_sources, dangling_ids) (graph.py:262-271, 367)
-__global__ void k_gather_rows(const int32_t *__restrict__ ids, int64_t count, const int64_t *__restrict__ in_off,
-                              const int32_t *__restrict__ in_src, const int64_t *__restrict__ dst_off,
-                              int32_t *__restrict__ dst) {
-    int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < count; i += nwarps) {
-        int32_t d = ids[i];
-        int64_t lo = in_off[d], len = in_off[d + 1] - lo, o = dst_off[i];
-        for (int64_t k = lane; k < len; k += 32) dst[o + k] = in_src[lo + k];
-    }
-}
+// _gather_rows(in_offsets, in_sources, dangling_ids) (graph.py:262-271, 367): k_seg_gather<false>
 
 __global__ void k_tail_rows(const int64_t *__restrict__ in_off, int64_t live_end, int64_t nd,
                             int32_t *__restrict__ ids, int64_t *__restrict__ off) {
@@ -560,9 +549,10 @@ int preprocess_ifp2_device(Graph &g) {
         PR_CUDA(cudaStreamSynchronize(st));
         PR_TRY(ensure(g.src_ids, 4 * (md ? md : 1)));
         if (md)
-            k_gather_rows<<<gs_grid(ctx, nd * 32), 256, 0, st>>>(g.dang_ids.as<int32_t>(), nd, g.in_off.as<int64_t>(),
-                                                                 g.in_src.as<int32_t>(), g.src_off.as<int64_t>(),
-                                                                 g.src_ids.as<int32_t>());
+            k_seg_gather<false><<<seg_grid(ctx, md), 256, 0, st>>>(g.src_off.as<int64_t>(), nd,
+                                                                   g.dang_ids.as<int32_t>(), g.in_off.as<int64_t>(),
+                                                                   g.in_src.as<int32_t>(), nullptr,
+                                                                   g.src_ids.as<int32_t>(), md);
         PR_CUDA(cudaStreamSynchronize(st));
         PR_CUDA(cudaGetLastError());
     }
@@ -635,13 +625,15 @@ __global__ void k_relabel_keys(const int64_t *__restrict__ out_off, const int64_
     }
 }
 
-// rank = inverse permutation; live_end = first run id of the dangling classes
+// rank = inverse permutation; bounds[k] = first run id of class > k
+// (bounds[0] = end of class 0, bounds[1] = live_end, the dangling tail)
 __global__ void k_rank_from_perm(const uint32_t *__restrict__ keys, const int32_t *__restrict__ perm, int64_t n,
-                                 int32_t *__restrict__ rank, int64_t *__restrict__ live_end) {
+                                 int32_t *__restrict__ rank, int64_t *__restrict__ bounds) {
     GRID_STRIDE(i, n) {
         rank[perm[i]] = (int32_t)i;
-        const bool dang = (keys[i] >> 30) >= 2;
-        if (dang && (i == 0 || (keys[i - 1] >> 30) < 2)) *live_end = i;
+        const uint32_t c = keys[i] >> 30, p = i > 0 ? keys[i - 1] >> 30 : 0u;
+        if (c >= 1 && (i == 0 || p < 1)) bounds[0] = i;
+        if (c >= 2 && (i == 0 || p < 2)) bounds[1] = i;
     }
 }
 
@@ -652,31 +644,6 @@ __global__ void k_perm_len(const int64_t *__restrict__ off, const int32_t *__res
         if (i == n) { len[n] = 0; continue; }
         int32_t v = perm[i];
         len[i] = off[v + 1] - off[v];
-    }
-}
-
-// warp per new row: copy the old row, renaming its column ids through rank
-// (4 loads in flight per lane on long rows)
-__global__ void k_perm_rows(const int64_t *__restrict__ off, const int32_t *__restrict__ col,
-                            const int32_t *__restrict__ perm, const int32_t *__restrict__ rank, int64_t n,
-                            const int64_t *__restrict__ noff, int32_t *__restrict__ ncol) {
-    int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < n; i += nw) {
-        int32_t v = perm[i];
-        int64_t lo = off[v], len = off[v + 1] - lo, o = noff[i];
-        for (int64_t k = lane; k < len; k += 128) {
-            int c[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) c[q] = k + 32 * q < len ? __ldg(&col[lo + k + 32 * q]) : -1;
-            int r[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) r[q] = c[q] >= 0 ? __ldg(&rank[c[q]]) : 0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (c[q] >= 0) ncol[o + k + 32 * q] = r[q];
-        }
     }
 }
 
@@ -695,9 +662,9 @@ static int permute_adjacency(Ctx &ctx, const DevBuf &off, const DevBuf &col, con
         return cub::DeviceScan::ExclusiveSum(t, b, len.as<int64_t>(), noff.as<int64_t>(), (int)(n + 1), st);
     }));
     if (m)
-        k_perm_rows<<<(unsigned)(ctx.sm_count * 32), 256, 0, st>>>(off.as<int64_t>(), col.as<int32_t>(),
-                                                                 perm.as<int32_t>(), rank.as<int32_t>(), n,
-                                                                 noff.as<int64_t>(), ncol.as<int32_t>());
+        k_seg_gather<true><<<seg_grid(ctx, m), 256, 0, st>>>(noff.as<int64_t>(), n, perm.as<int32_t>(),
+                                                             off.as<int64_t>(), col.as<int32_t>(), rank.as<int32_t>(),
+                                                             ncol.as<int32_t>(), m);
     return PR_OK;
 }
 
@@ -710,7 +677,7 @@ int ensure_run_layout(Graph &g) {
     PR_TRY(ensure(keys, 4 * n));
     PR_TRY(ensure(sorted, 4 * n));
     PR_TRY(ensure(ids, 4 * n));
-    PR_TRY(ensure(dl, 8));
+    PR_TRY(ensure(dl, 16));
     PR_TRY(ensure(g.perm, 4 * n));
     PR_TRY(ensure(g.rank, 4 * n));
     k_relabel_keys<<<gs_grid(ctx, n), 256, 0, st>>>(g.out_off.as<int64_t>(), g.in_off.as<int64_t>(), n,
@@ -719,8 +686,8 @@ int ensure_run_layout(Graph &g) {
         return cub::DeviceRadixSort::SortPairs(t, b, keys.as<uint32_t>(), sorted.as<uint32_t>(), ids.as<int32_t>(),
                                                g.perm.as<int32_t>(), (int)n, 0, 32, st);
     }));
-    const int64_t none = n;
-    PR_CUDA(cudaMemcpyAsync(dl.ptr, &none, 8, cudaMemcpyHostToDevice, st));
+    const int64_t none[2] = {n, n};
+    PR_CUDA(cudaMemcpyAsync(dl.ptr, none, 16, cudaMemcpyHostToDevice, st));
     k_rank_from_perm<<<gs_grid(ctx, n), 256, 0, st>>>(sorted.as<uint32_t>(), g.perm.as<int32_t>(), n,
                                                       g.rank.as<int32_t>(), dl.as<int64_t>());
     Graph *r = new Graph();
@@ -732,14 +699,15 @@ int ensure_run_layout(Graph &g) {
     if (!rc) rc = permute_adjacency(ctx, g.in_off, g.in_src, g.perm, g.rank, n, m, r->in_off, r->in_src);
     if (!rc) rc = ensure(r->out_deg, 4 * n);
     if (!rc) k_degree<<<gs_grid(ctx, n), 256, 0, st>>>(r->out_off.as<int64_t>(), n, r->out_deg.as<int32_t>());
-    int64_t live_end = n;
-    if (!rc && cudaMemcpyAsync(&live_end, dl.ptr, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    int64_t bounds[2] = {n, n};
+    if (!rc && cudaMemcpyAsync(bounds, dl.ptr, 16, cudaMemcpyDeviceToHost, st) != cudaSuccess)
         rc = fail(PR_ERR_CUDA, "run layout build failed");
     if (!rc && (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess))
         rc = fail(PR_ERR_CUDA, "run layout build failed");
     if (rc) { delete r; return rc; }
-    r->live_end = live_end;
-    r->n_dangling = n - live_end;
+    r->class0_end = bounds[0];
+    r->live_end = bounds[1];
+    r->n_dangling = n - bounds[1];
     g.run = r;
     return PR_OK;
 }

@@ -96,6 +96,7 @@ struct Graph {
     // run layout only: vertices [live_end, n) are the dangling ones (classes
     // out=0&in>0, isolated), so their in-edges are the CSC tail
     int64_t live_end = -1;
+    int64_t class0_end = -1;   // run layout: [0, class0_end) have in>0 & out>0
     DevBuf out_off;   // int64 [n+1]
     DevBuf out_tgt;   // int32 [m]
     DevBuf out_deg;   // int32 [n]

@@ -657,7 +657,7 @@ static int add_kernel(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_
 struct Plan {
     RunArgs A;
     bool exact;
-    unsigned g_all, g_red, g_pull, g_push, g_scan;
+    unsigned g_all, g_red, g_total, g_pull, g_push, g_scan;
 };
 
 static bool same_key(const pr_run_params &a, const pr_run_params &b) {
@@ -857,11 +857,19 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     P.exact = exact;
     P.g_all = grid_for(n, 256);
     P.g_pull = (unsigned)pull_blocks;
-    // reducing kernels of the fast engine: capped grid-stride grids (8 blocks/SM)
-    const unsigned g_cap = (unsigned)ctx.sm_count * 8;
-    P.g_red = P.g_all < g_cap ? P.g_all : g_cap;
+    // reducing kernels of the fast engine: one resident wave, grid-stride
+    // (a block's lifetime -- reduce, publish -- is latency, not bandwidth)
+    auto wave = [&](const void *k) -> unsigned {
+        int b = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, 256, 0) != cudaSuccess || b < 1) b = 1;
+        return (unsigned)(ctx.sm_count * b);
+    };
+    const unsigned w_init = wave((const void *)k_init), w_scan = wave((const void *)k_scan),
+                   w_total = wave((const void *)k_total);
+    P.g_red = P.g_all < w_init ? P.g_all : w_init;
+    P.g_total = P.g_all < w_total ? P.g_all : w_total;
     P.g_scan = grid_for(S.count, 256);
-    if (P.g_scan > g_cap) P.g_scan = g_cap;
+    if (P.g_scan > w_scan) P.g_scan = w_scan;
     P.g_push = (unsigned)ctx.sm_count * 8;
 
     PR_CUDA(cudaMemsetAsync(g.in_d.ptr, 0, n, st));
@@ -950,7 +958,7 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
         }
     }
     int include_h = algo == PR_ALGO_IFP1 ? 1 : 0;
-    k_total<<<P.g_red, 256, 0, st>>>(A, include_h, settled, algo == PR_ALGO_IFP2 ? 1 : 0);
+    k_total<<<P.g_total, 256, 0, st>>>(A, include_h, settled, algo == PR_ALGO_IFP2 ? 1 : 0);
     {
         unsigned gs = grid_for(n, 256);
         if (gs > 4096) gs = 4096;

@@ -17,6 +17,7 @@
 
 #include "cubutil.cuh"
 #include "internal.cuh"
+#include "seg.cuh"
 
 namespace pr {
 
@@ -39,6 +40,10 @@ struct SeedPred {
     __host__ __device__ bool operator()(int32_t v) const { return in_off[v + 1] == in_off[v] && out_deg[v] > 0; }
 };
 
+__global__ void k_iota(int32_t *__restrict__ out, int64_t start, int64_t count) {
+    GRID_STRIDE(i, count) out[i] = (int32_t)(start + i);
+}
+
 // descending-degree sort key (ascending radix sort of ~degree)
 __global__ void k_deg_keys(const int32_t *__restrict__ ids, int64_t cnt, const int64_t *__restrict__ in_off,
                            unsigned *__restrict__ keys) {
@@ -54,20 +59,6 @@ __global__ void k_row_len(const int32_t *__restrict__ ids, int64_t cnt, const in
         if (i == cnt) { len[cnt] = 0; continue; }
         int32_t v = ids[i];
         len[i] = in_off[v + 1] - in_off[v];
-    }
-}
-
-// warp per row: copy the row's sources into the compacted CSC
-__global__ void k_fill_csc(const int32_t *__restrict__ ids, int64_t cnt, const int64_t *__restrict__ in_off,
-                           const int32_t *__restrict__ in_src, const int64_t *__restrict__ doff,
-                           int32_t *__restrict__ csc) {
-    int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < cnt; i += nw) {
-        int32_t v = ids[i];
-        int64_t lo = in_off[v], len = in_off[v + 1] - lo, o = doff[i];
-        for (int64_t k = lane; k < len; k += 32) csc[o + k] = in_src[lo + k];
     }
 }
 
@@ -160,45 +151,64 @@ int ensure_sched(Graph &g, int which) {
     PR_TRY(ensure(S.ids, 4 * n));
     auto first = thrust::make_counting_iterator<int32_t>(0);
     int mode = which;
-    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
-        return cub::DeviceSelect::If(t, b, first, unsorted.as<int32_t>(), dcount.as<int64_t>(), (int)n,
-                                     RowMember{g.in_off.as<int64_t>(), g.out_deg.as<int32_t>(), mode}, st);
-    }));
+    // run layout, IFP2: D = class 0, already the id prefix [0, class0_end) in
+    // descending in-degree order (ties by id, as the stable sort below would
+    // leave them) -- its rows are the CSC prefix
+    const bool prefix = which == 1 && g.class0_end >= 0;
     int64_t cnt = 0;
-    PR_CUDA(cudaMemcpyAsync(&cnt, dcount.ptr, 8, cudaMemcpyDeviceToHost, st));
-    PR_CUDA(cudaStreamSynchronize(st));
-    S.count = cnt;
-    // rows by descending in-degree (stable)
-    PR_TRY(ensure(keys, 4 * (cnt ? cnt : 1)));
-    PR_TRY(ensure(keys2, 4 * (cnt ? cnt : 1)));
-    if (cnt) {
-        k_deg_keys<<<grid_for(cnt, 256) > 4096 ? 4096 : grid_for(cnt, 256), 256, 0, st>>>(
-            unsorted.as<int32_t>(), cnt, g.in_off.as<int64_t>(), keys.as<unsigned>());
+    if (prefix) {
+        cnt = g.class0_end;
+        S.count = cnt;
+        PR_TRY(ensure(S.doff, 8 * (cnt + 1)));
+        int64_t edges = 0;
+        PR_CUDA(cudaMemcpyAsync(&edges, g.in_off.as<int64_t>() + cnt, 8, cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaMemcpyAsync(S.doff.ptr, g.in_off.ptr, 8 * (cnt + 1), cudaMemcpyDeviceToDevice, st));
+        if (cnt) k_iota<<<grid_for(cnt, 256) > 4096 ? 4096 : grid_for(cnt, 256), 256, 0, st>>>(S.ids.as<int32_t>(), 0, cnt);
+        PR_CUDA(cudaStreamSynchronize(st));
+        S.edges = edges;
+        PR_TRY(ensure(S.csc, 4 * (edges + CSC_PAD)));
+        PR_CUDA(cudaMemsetAsync(S.csc.as<int32_t>() + edges, 0, 4 * CSC_PAD, st));
+        if (edges) PR_CUDA(cudaMemcpyAsync(S.csc.ptr, g.in_src.ptr, 4 * edges, cudaMemcpyDeviceToDevice, st));
+    } else {
         PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
-            return cub::DeviceRadixSort::SortPairs(t, b, keys.as<unsigned>(), keys2.as<unsigned>(),
-                                                   unsorted.as<int32_t>(), S.ids.as<int32_t>(), (int)cnt, 0, 32, st);
+            return cub::DeviceSelect::If(t, b, first, unsorted.as<int32_t>(), dcount.as<int64_t>(), (int)n,
+                                         RowMember{g.in_off.as<int64_t>(), g.out_deg.as<int32_t>(), mode}, st);
         }));
+        PR_CUDA(cudaMemcpyAsync(&cnt, dcount.ptr, 8, cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+        S.count = cnt;
+        // rows by descending in-degree (stable)
+        PR_TRY(ensure(keys, 4 * (cnt ? cnt : 1)));
+        PR_TRY(ensure(keys2, 4 * (cnt ? cnt : 1)));
+        if (cnt) {
+            k_deg_keys<<<grid_for(cnt, 256) > 4096 ? 4096 : grid_for(cnt, 256), 256, 0, st>>>(
+                unsorted.as<int32_t>(), cnt, g.in_off.as<int64_t>(), keys.as<unsigned>());
+            PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+                return cub::DeviceRadixSort::SortPairs(t, b, keys.as<unsigned>(), keys2.as<unsigned>(),
+                                                       unsorted.as<int32_t>(), S.ids.as<int32_t>(), (int)cnt, 0, 32, st);
+            }));
+        }
+        // compacted CSC in row order
+        PR_TRY(ensure(len, 8 * (cnt + 1)));
+        PR_TRY(ensure(S.doff, 8 * (cnt + 1)));
+        k_row_len<<<grid_for(cnt + 1, 256) > 4096 ? 4096 : grid_for(cnt + 1, 256), 256, 0, st>>>(S.ids.as<int32_t>(), cnt, g.in_off.as<int64_t>(), len.as<int64_t>());
+        PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceScan::ExclusiveSum(t, b, len.as<int64_t>(), S.doff.as<int64_t>(), (int)(cnt + 1), st);
+        }));
+        int64_t edges = 0;
+        PR_CUDA(cudaMemcpyAsync(&edges, S.doff.as<int64_t>() + cnt, 8, cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+        S.edges = edges;
+        PR_TRY(ensure(S.csc, 4 * (edges + CSC_PAD)));
+        PR_CUDA(cudaMemsetAsync(S.csc.ptr, 0, 4 * (edges + CSC_PAD), st));
+        if (cnt) {
+            if (edges)
+                k_seg_gather<false><<<seg_grid(ctx, edges), 256, 0, st>>>(S.doff.as<int64_t>(), cnt, S.ids.as<int32_t>(),
+                                                                      g.in_off.as<int64_t>(), g.in_src.as<int32_t>(),
+                                                                      nullptr, S.csc.as<int32_t>(), edges);
+        }
     }
-    // compacted CSC in row order
-    PR_TRY(ensure(len, 8 * (cnt + 1)));
-    PR_TRY(ensure(S.doff, 8 * (cnt + 1)));
-    unsigned gc = grid_for(cnt + 1, 256) > 4096 ? 4096 : grid_for(cnt + 1, 256);
-    k_row_len<<<gc, 256, 0, st>>>(S.ids.as<int32_t>(), cnt, g.in_off.as<int64_t>(), len.as<int64_t>());
-    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
-        return cub::DeviceScan::ExclusiveSum(t, b, len.as<int64_t>(), S.doff.as<int64_t>(), (int)(cnt + 1), st);
-    }));
-    int64_t edges = 0;
-    PR_CUDA(cudaMemcpyAsync(&edges, S.doff.as<int64_t>() + cnt, 8, cudaMemcpyDeviceToHost, st));
-    PR_CUDA(cudaStreamSynchronize(st));
-    S.edges = edges;
-    PR_TRY(ensure(S.csc, 4 * (edges + CSC_PAD)));
-    PR_CUDA(cudaMemsetAsync(S.csc.ptr, 0, 4 * (edges + CSC_PAD), st));
-    if (cnt) {
-        unsigned gr = grid_for(cnt * 32, 256);
-        if (gr > (unsigned)ctx.sm_count * 32) gr = ctx.sm_count * 32;
-        k_fill_csc<<<gr, 256, 0, st>>>(S.ids.as<int32_t>(), cnt, g.in_off.as<int64_t>(), g.in_src.as<int32_t>(),
-                                       S.doff.as<int64_t>(), S.csc.as<int32_t>());
-    }
+    const unsigned gc = grid_for(cnt + 1, 256) > 4096 ? 4096 : grid_for(cnt + 1, 256);
     // bins
     PR_CUDA(cudaMemsetAsync(dcount.ptr, 0, 16, st));
     if (cnt)
@@ -242,12 +252,21 @@ int ensure_sched(Graph &g, int which) {
         PR_CUDA(cudaStreamSynchronize(st));
     }
     PR_TRY(ensure(S.seed_ids, 4 * n));
-    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
-        return cub::DeviceSelect::If(t, b, first, S.seed_ids.as<int32_t>(), dcount.as<int64_t>(), (int)n,
-                                     SeedPred{g.in_off.as<int64_t>(), g.out_deg.as<int32_t>()}, st);
-    }));
-    PR_CUDA(cudaMemcpyAsync(&S.n_seed, dcount.ptr, 8, cudaMemcpyDeviceToHost, st));
-    PR_CUDA(cudaStreamSynchronize(st));
+    if (g.class0_end >= 0) {
+        // run layout: seeds (in = 0, out > 0) are class 1, [class0_end, live_end)
+        S.n_seed = g.live_end - g.class0_end;
+        if (S.n_seed)
+            k_iota<<<grid_for(S.n_seed, 256) > 4096 ? 4096 : grid_for(S.n_seed, 256), 256, 0, st>>>(
+                S.seed_ids.as<int32_t>(), g.class0_end, S.n_seed);
+        PR_CUDA(cudaStreamSynchronize(st));
+    } else {
+        PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceSelect::If(t, b, first, S.seed_ids.as<int32_t>(), dcount.as<int64_t>(), (int)n,
+                                         SeedPred{g.in_off.as<int64_t>(), g.out_deg.as<int32_t>()}, st);
+        }));
+        PR_CUDA(cudaMemcpyAsync(&S.n_seed, dcount.ptr, 8, cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+    }
     PR_CUDA(cudaGetLastError());
     S.built = true;
     return PR_OK;
