@@ -43,7 +43,7 @@ extern "C" {
 #define PR_ERR_NOT_SETTLED (-4) /* max_rounds exhausted (engines.py:455-456 RuntimeError) */
 #define PR_ERR_NOMEM (-5)       /* device allocation failed */
 
-#define PR_ABI_VERSION 1
+#define PR_ABI_VERSION 2
 
 typedef struct pr_ctx pr_ctx;       /* one device + stream + workspace */
 typedef struct pr_graph pr_graph;   /* device-resident CSR+CSC and derived data */
@@ -109,6 +109,10 @@ typedef struct pr_run_result {
     double push_ms;           /* device time: first round .. normalised output (CUDA events) */
     double round_ms;          /* device time of the round loop alone */
     double bytes_moved;       /* algorithmic bytes of the round loop (DESIGN.md roofline) */
+    double pull_ms;           /* device time inside the dense-round kernels (globaltimer, first block
+                                 start .. last block finalise), summed over pull rounds */
+    double pull_bytes;        /* algorithmic bytes of those pull rounds */
+    double sparse_ms;         /* same for the sparse rounds (push + scan kernels) */
 } pr_run_result;
 
 /* ---- library / context ------------------------------------------------ */

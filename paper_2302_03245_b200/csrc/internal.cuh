@@ -81,6 +81,13 @@ struct RunCtl {
     double mass_total;
     int64_t settled;
     unsigned long long unit_ctr;  // pull-unit dispatch counter (bins.cuh), reset every round
+    // per-kernel device timing (globaltimer): the first block of a round's
+    // first kernel stamps t_k0, the finalising block closes the round
+    uint32_t k_started;
+    int32_t next_mode;        // mode of the round being timed (set when it was chosen)
+    uint64_t t_k0;
+    double next_bytes;        // algorithmic bytes of that round
+    double pull_ns, pull_bytes, sparse_ns;
 };
 
 // Per-block partial statistics of one round (reduced in fixed order).

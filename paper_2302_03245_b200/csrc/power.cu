@@ -288,6 +288,7 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
     if (h_conv && k) PR_CUDA(cudaMemcpy(h_conv, A.conv, 8 * k, cudaMemcpyDeviceToHost));
     if (res) {
         memset(res, 0, sizeof(*res));
+        memset(res, 0, sizeof(*res));
         res->rounds = k;
         res->rows = k;
         res->push_ops = k * g.m;

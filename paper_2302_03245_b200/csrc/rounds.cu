@@ -165,10 +165,23 @@ __device__ void finalize_row(const RunArgs &A, const Partial &tot, int64_t r, bo
         A.rows[r] = row;
     }
     ctl->rows = r + 1;
+    if (fast && r >= 1) {
+        // close the round that produced this state (its kernels started at t_k0)
+        const double dt = (double)(globaltimer() - ctl->t_k0);
+        if (ctl->next_mode == 0) {
+            ctl->pull_ns += dt;
+            ctl->pull_bytes += ctl->next_bytes;
+        } else {
+            ctl->sparse_ns += dt;
+        }
+    }
+    ctl->k_started = 0;
     ctl->push_ops += tot.push_ops;
     ctl->push_ops_dangling += tot.push_dang;
     // algorithmic bytes of the round that drains this state
-    if (tot.nact > 0) ctl->bytes += 12.0 * (double)tot.push_ops + 40.0 * (double)tot.nact + 8.0 * A.n_scan;
+    const double rb = tot.nact > 0 ? 12.0 * (double)tot.push_ops + 40.0 * (double)tot.nact + 8.0 * A.n_scan : 0.0;
+    ctl->bytes += rb;
+    ctl->next_bytes = rb;
     int done = 0;
     if (tot.nact == 0) done = 1;
     else if (r >= A.max_rounds) done = 2;
@@ -182,6 +195,7 @@ __device__ void finalize_row(const RunArgs &A, const Partial &tot, int64_t r, bo
         else if (A.policy == PR_MODE_AUTO && (double)tot.work < A.push_work) mode = 1;
     }
     ctl->mode = mode;
+    ctl->next_mode = mode;
     if (!done) {
         if (mode) ctl->push_rounds += 1;
         else ctl->pull_rounds += 1;
@@ -267,6 +281,11 @@ __global__ void k_reset(RunArgs A) {
     c->mass_total = 0.0;
     c->settled = 0;
     c->unit_ctr = 0;
+    c->k_started = 0;
+    c->next_mode = 0;
+    c->t_k0 = 0;
+    c->next_bytes = 0.0;
+    c->pull_ns = c->pull_bytes = c->sparse_ns = 0.0;
 }
 
 // State 0 (h = 1 everywhere, MassState.fresh engines.py:51-54): trace row 0
@@ -349,7 +368,12 @@ __global__ void __launch_bounds__(256) k_seed_scatter(RunArgs A) {
 #ifndef PULL_MIN_BLOCKS
 #define PULL_MIN_BLOCKS 4
 #endif
+__device__ __forceinline__ void stamp_round_start(RunCtl *ctl) {
+    if (threadIdx.x == 0 && atomicExch(&ctl->k_started, 1u) == 0u) ctl->t_k0 = globaltimer();
+}
+
 __global__ void __launch_bounds__(256, PULL_MIN_BLOCKS) k_pull(RunArgs A) {
+    stamp_round_start(A.ctl);
     const int64_t t = A.ctl->round;
     const double *__restrict__ s_in = A.s + (t & 1) * A.n;
     const int64_t r = t + 1;
@@ -380,6 +404,7 @@ __global__ void __launch_bounds__(256, PULL_MIN_BLOCKS) k_pull(RunArgs A) {
 // one warp per push item (a TILE-edge chunk of one vertex's out-row), the 8
 // target loads of a lane issued before its 8 reductions.
 __global__ void __launch_bounds__(256) k_push(RunArgs A) {
+    stamp_round_start(A.ctl);
     int64_t t = A.ctl->round;
     const double *__restrict__ s_in = A.s + (t & 1) * A.n;
     const long long *F = A.frontier + (t & 1) * A.fcap;
@@ -996,6 +1021,9 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
         res->push_ms = ms_all;
         res->round_ms = ms_loop;
         res->bytes_moved = hc.bytes;
+        res->pull_ms = hc.pull_ns * 1e-6;
+        res->pull_bytes = hc.pull_bytes;
+        res->sparse_ms = hc.sparse_ns * 1e-6;
     }
     if (hc.done == 2)
         return fail(PR_ERR_NOT_SETTLED,
