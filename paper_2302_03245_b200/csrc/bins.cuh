@@ -18,6 +18,18 @@
 
 namespace pr {
 
+// Cache policy of the index stream (compacted CSC, read once per round):
+// when a round's working set overflows L2 (C3, C5) it is loaded with
+// ld.global.cs (evict-first) so that it does not push the share vector out
+// of L2; when everything fits (C1, C2) the CSC stays L2-resident across
+// rounds with plain loads.  Measured: C3 -5%, C5 -1%, C2 +4% if streamed.
+template <bool STREAM>
+__device__ __forceinline__ int ld_idx(const int32_t *p) {
+    if constexpr (STREAM) return __ldcs(p);
+    else return __ldg(p);
+}
+__device__ __forceinline__ double ld_share(const double *p) { return __ldg(p); }
+
 struct BinView {
     const int32_t *ids;      // row -> vertex id
     const int64_t *doff;     // row offsets in csc
@@ -31,16 +43,17 @@ struct BinView {
     unsigned long long *unit_ctr;  // dynamic dispatch counter (0 at kernel start)
 };
 
+template <bool STREAM>
 __device__ __forceinline__ double row_sum_thread(const int32_t *__restrict__ csc, int64_t lo, int64_t hi,
                                                  const double *__restrict__ x) {
     double acc = 0.0;
     for (int64_t e = lo; e < hi; e += 8) {
         int idx[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) idx[q] = e + q < hi ? __ldg(&csc[e + q]) : -1;
+        for (int q = 0; q < 8; ++q) idx[q] = e + q < hi ? ld_idx<STREAM>(&csc[e + q]) : -1;
         double t[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) t[q] = idx[q] >= 0 ? __ldg(&x[idx[q]]) : 0.0;
+        for (int q = 0; q < 8; ++q) t[q] = idx[q] >= 0 ? ld_share(&x[idx[q]]) : 0.0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc += t[q];
     }
@@ -48,6 +61,7 @@ __device__ __forceinline__ double row_sum_thread(const int32_t *__restrict__ csc
 }
 
 // lanes stride [lo, hi) with 8 gathers in flight; warp-reduced (fixed tree)
+template <bool STREAM>
 __device__ __forceinline__ double span_sum_warp(const int32_t *__restrict__ csc, int64_t lo, int64_t hi,
                                                 const double *__restrict__ x) {
     const int lane = threadIdx.x & 31;
@@ -55,10 +69,10 @@ __device__ __forceinline__ double span_sum_warp(const int32_t *__restrict__ csc,
     for (int64_t e = lo + lane; e < hi; e += 256) {
         int idx[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) idx[q] = e + 32 * q < hi ? __ldg(&csc[e + 32 * q]) : -1;
+        for (int q = 0; q < 8; ++q) idx[q] = e + 32 * q < hi ? ld_idx<STREAM>(&csc[e + 32 * q]) : -1;
         double t[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) t[q] = idx[q] >= 0 ? __ldg(&x[idx[q]]) : 0.0;
+        for (int q = 0; q < 8; ++q) t[q] = idx[q] >= 0 ? ld_share(&x[idx[q]]) : 0.0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc += t[q];
     }
@@ -69,7 +83,7 @@ __device__ __forceinline__ double span_sum_warp(const int32_t *__restrict__ csc,
 
 // thread_row(valid, row, sum): all 32 lanes of a warp (warp-collective safe)
 // single_row(row, sum): one thread
-template <class ThreadRow, class SingleRow>
+template <bool STREAM, class ThreadRow, class SingleRow>
 __device__ __forceinline__ void bins_run(const BinView &B, const double *__restrict__ x, ThreadRow &thread_row,
                                          SingleRow &single_row) {
     __shared__ double red[8];
@@ -95,11 +109,11 @@ __device__ __forceinline__ void bins_run(const BinView &B, const double *__restr
 #pragma unroll
             for (int q = 0; q < HUB_CHUNK / 256; ++q) {
                 const int64_t e = c0 + tid + 256 * q;
-                idx[q] = e < c1 ? __ldg(&B.csc[e]) : -1;
+                idx[q] = e < c1 ? ld_idx<STREAM>(&B.csc[e]) : -1;
             }
             double acc = 0.0;
 #pragma unroll
-            for (int q = 0; q < HUB_CHUNK / 256; ++q) acc += idx[q] >= 0 ? __ldg(&x[idx[q]]) : 0.0;
+            for (int q = 0; q < HUB_CHUNK / 256; ++q) acc += idx[q] >= 0 ? ld_share(&x[idx[q]]) : 0.0;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             __syncthreads();
@@ -128,7 +142,7 @@ __device__ __forceinline__ void bins_run(const BinView &B, const double *__restr
                 for (int j = 0; j < 32; ++j) {
                     const int64_t row = base + 8 * j;
                     if (row >= d.y) break;
-                    const double s = span_sum_warp(B.csc, B.doff[row], B.doff[row + 1], x);
+                    const double s = span_sum_warp<STREAM>(B.csc, B.doff[row], B.doff[row + 1], x);
                     if (lane == j) mine = s;
                 }
                 const int64_t row = base + 8 * lane;
@@ -139,7 +153,7 @@ __device__ __forceinline__ void bins_run(const BinView &B, const double *__restr
             for (int64_t base = d.x; base < d.y; base += 256) {
                 const int64_t row = base + tid;
                 const bool valid = row < d.y;
-                const double s = valid ? row_sum_thread(B.csc, B.doff[row], B.doff[row + 1], x) : 0.0;
+                const double s = valid ? row_sum_thread<STREAM>(B.csc, B.doff[row], B.doff[row + 1], x) : 0.0;
                 thread_row(valid, row, s);
             }
         }

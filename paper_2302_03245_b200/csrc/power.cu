@@ -100,6 +100,7 @@ __global__ void __launch_bounds__(256) k_pw_init(PowArgs A) {
 }
 
 // nxt_v = sum z over in-edges + restart * p_v; block partial of sum(nxt)
+template <bool STREAM>
 __global__ void __launch_bounds__(256, 4) k_pw_gather(PowArgs A) {
     const double restart = A.ctl->restart;
     Partial p;
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(256, 4) k_pw_gather(PowArgs A) {
         if (valid) finish(__ldg(&A.T.ids[row]), sum);
     };
     auto single_row = [&](int64_t row, double sum) { finish(__ldg(&A.T.ids[row]), sum); };
-    bins_run(A.T, A.z, thread_row, single_row);
+    bins_run<STREAM>(A.T, A.z, thread_row, single_row);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.n_zero;
          i += (int64_t)gridDim.x * blockDim.x)
         finish(A.zero_ids[i], 0.0);
@@ -173,7 +174,7 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
     Ctx &ctx = *g.ctx;
     cudaStream_t st = ctx.stream;
     int per_sm = 0;
-    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pw_gather, 256, 0));
+    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pw_gather<false>, 256, 0));
     if (per_sm < 1) per_sm = 1;
     PR_TRY(ensure_sched(g, 2));
     auto &S = g.sched[2];
@@ -182,6 +183,10 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
     memset(&A, 0, sizeof(A));
     const int64_t blk = (int64_t)ctx.sm_count * per_sm;
     PR_TRY(ensure_units(g, 2, blk));
+    // stream the CSC when an iteration's working set overflows L2 (bins.cuh)
+    const bool stream = 4.0 * (double)S.edges + 16.0 * (double)n >
+                        0.6 * (double)(ctx.l2_bytes ? ctx.l2_bytes : (size_t)126 << 20);
+    const void *gather_fn = stream ? (const void *)k_pw_gather<true> : (const void *)k_pw_gather<false>;
     int64_t maxb = blk > (n + 255) / 256 ? blk : (n + 255) / 256;
     int64_t it_cap = iterations > 0 ? iterations : 1;
     // workspace: pi, nxt, z, p (opt), deltas, conv, partials, ctl
@@ -236,7 +241,8 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
         PR_CUDA(cudaEventRecord(e0, st));
         k_pw_init<<<g_all, 256, 0, st>>>(A);
         for (int64_t k = 0; k < iterations; ++k) {
-            k_pw_gather<<<g_gather, 256, 0, st>>>(A);
+            if (stream) k_pw_gather<true><<<g_gather, 256, 0, st>>>(A);
+            else k_pw_gather<false><<<g_gather, 256, 0, st>>>(A);
             k_pw_norm<<<g_all, 256, 0, st>>>(A);
             PR_CUDA(cudaGetLastError());
             PowCtl hc;
@@ -263,7 +269,7 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
         wp.conditional.size = 1;
         PR_CUDA(cudaGraphAddNode(&n_while, G, &n_init, 1, &wp));
         cudaGraph_t body = wp.conditional.phGraph_out[0];
-        PR_TRY(add_node(body, &n_a, nullptr, 0, (void *)k_pw_gather, g_gather, args));
+        PR_TRY(add_node(body, &n_a, nullptr, 0, (void *)gather_fn, g_gather, args));
         PR_TRY(add_node(body, &n_b, &n_a, 1, (void *)k_pw_norm, g_all, args));
         cudaGraphExec_t ex;
         PR_CUDA(cudaGraphInstantiate(&ex, G, 0));

@@ -372,6 +372,7 @@ __device__ __forceinline__ void stamp_round_start(RunCtl *ctl) {
     if (threadIdx.x == 0 && atomicExch(&ctl->k_started, 1u) == 0u) ctl->t_k0 = globaltimer();
 }
 
+template <bool STREAM>
 __global__ void __launch_bounds__(256, PULL_MIN_BLOCKS) k_pull(RunArgs A) {
     stamp_round_start(A.ctl);
     const int64_t t = A.ctl->round;
@@ -396,7 +397,7 @@ __global__ void __launch_bounds__(256, PULL_MIN_BLOCKS) k_pull(RunArgs A) {
         int it = drain_vertex(A, v, A.h[v] + sum, r, p);
         if (app) append_one(it, v, F, fsize);
     };
-    bins_run(A.T, s_in, thread_row, single_row);
+    bins_run<STREAM>(A.T, s_in, thread_row, single_row);
     finish_round(A, p, r, true, false, p);
 }
 
@@ -683,6 +684,7 @@ struct Plan {
     RunArgs A;
     bool exact;
     unsigned g_all, g_red, g_total, g_pull, g_push, g_scan;
+    const void *k_pull_fn;   // k_pull<false> or k_pull<true> (streamed index loads)
 };
 
 static bool same_key(const pr_run_params &a, const pr_run_params &b) {
@@ -740,7 +742,7 @@ static int build_graph(Plan &P, cudaGraph_t *out_g, cudaGraphExec_t *out_exec) {
         sp.conditional.size = 2;
         PR_CUDA(cudaGraphAddNode(&n_sw, body, nullptr, 0, &sp));
         cudaGraph_t b_pull = sp.conditional.phGraph_out[0], b_push = sp.conditional.phGraph_out[1];
-        PR_TRY(add_kernel(b_pull, &n_a, nullptr, 0, (void *)k_pull, P.g_pull, 256, args));
+        PR_TRY(add_kernel(b_pull, &n_a, nullptr, 0, (void *)P.k_pull_fn, P.g_pull, 256, args));
         PR_TRY(add_kernel(b_push, &n_a, nullptr, 0, (void *)k_push, P.g_push, 256, args));
         PR_TRY(add_kernel(b_push, &n_b, &n_a, 1, (void *)k_scan, P.g_scan, 256, args));
     }
@@ -809,7 +811,7 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     const int which = algo == PR_ALGO_IFP2 ? 1 : 0;
     // persistent pull grid: as many blocks as fit on the device at once,
     int per_sm = 0;
-    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pull, 256, 0));
+    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pull<false>, 256, 0));
     if (per_sm < 1) per_sm = 1;
     PR_TRY(ensure_sched(g, which));
     auto &S = g.sched[which];
@@ -882,6 +884,14 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     P.exact = exact;
     P.g_all = grid_for(n, 256);
     P.g_pull = (unsigned)pull_blocks;
+    {
+        // a dense round touches the compacted CSC, the share vector of the
+        // sources and ~44 B of state per row; stream the CSC when that
+        // overflows ~60% of L2
+        const double ws = 4.0 * (double)S.edges + 8.0 * (double)n + 44.0 * (double)S.count;
+        const bool stream = ws > 0.6 * (double)(ctx.l2_bytes ? ctx.l2_bytes : (size_t)126 << 20);
+        P.k_pull_fn = stream ? (const void *)k_pull<true> : (const void *)k_pull<false>;
+    }
     // reducing kernels of the fast engine: one resident wave, grid-stride
     // (a block's lifetime -- reduce, publish -- is latency, not bandwidth)
     auto wave = [&](const void *k) -> unsigned {
@@ -955,7 +965,8 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
                 }
                 k_ex_prep<<<P.g_all, 256, 0, st>>>(A);
             } else if (hc.mode == 0) {
-                k_pull<<<P.g_pull, 256, 0, st>>>(A);
+                if (P.k_pull_fn == (const void *)k_pull<true>) k_pull<true><<<P.g_pull, 256, 0, st>>>(A);
+                else k_pull<false><<<P.g_pull, 256, 0, st>>>(A);
             } else {
                 k_push<<<P.g_push, 256, 0, st>>>(A);
                 k_scan<<<P.g_scan, 256, 0, st>>>(A);
