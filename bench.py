@@ -252,6 +252,10 @@ def run_ours(args):
             "time_to_l1_ms": statistics.median(dev_ms), "round_loop_ms": statistics.median(loop_ms),
             "rounds": int(r0.rounds), "pull_rounds": int(r0.pull_rounds), "push_rounds": int(r0.push_rounds),
             "push_ops_per_step": int(r0.push_ops), "preprocess_s": preprocess_s,
+            "split_ms": {"pull_kernels": statistics.median(r.pull_ms for r in results),
+                         "sparse_kernels": statistics.median(r.sparse_ms for r in results),
+                         "loop_other": statistics.median(r.round_ms - r.pull_ms - r.sparse_ms for r in results),
+                         "outside_loop": statistics.median(r.push_ms - r.round_ms for r in results)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "k_pull (algorithmic bytes 12*E_pushed + 40*V_active + 8*n_scan per round)",

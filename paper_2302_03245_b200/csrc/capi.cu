@@ -42,6 +42,7 @@ int export_graph(Graph &g, int64_t *out_off, int64_t *out_tgt, int64_t *in_off, 
 int export_i32(Ctx &ctx, const DevBuf &src, int64_t count, int64_t *host);
 int export_i64(Ctx &ctx, const DevBuf &src, int64_t count, int64_t *host);
 int debug_gather(Graph &g0, int variant, int iters, int blocks_per_sm, double *ms_out);
+int debug_graph(Ctx &ctx, int variant, int64_t iters, int blocks, double *us_out);
 struct Part;
 int part_create(Ctx &ctx, int64_t owned, int64_t slot, const int64_t *in_off, const int64_t *in_src, int64_t edges,
                 const int64_t *deg, const int64_t *row_len, const int64_t *dtc, const uint8_t *dang,
@@ -448,6 +449,12 @@ int pr_debug_gather(pr_graph *g, int variant, int iters, int blocks_per_sm, doub
     CHECK_PTR(g, "graph");
     PR_TRY(set_device(*g->g->ctx));
     return debug_gather(*g->g, variant, iters, blocks_per_sm, ms_out);
+}
+
+int pr_debug_graph(pr_ctx *ctx, int variant, int64_t iters, int blocks, double *us_out) {
+    CHECK_PTR(ctx, "ctx");
+    PR_TRY(set_device(ctx->c));
+    return debug_graph(ctx->c, variant, iters, blocks, us_out);
 }
 
 }  // extern "C"

@@ -109,5 +109,115 @@ int debug_gather(Graph &g0, int variant, int iters, int blocks_per_sm, double *m
     return PR_OK;
 }
 
+
+// ---- round-loop launch overhead: a trivial "round" kernel whose last block
+// decrements a counter and drives the conditional(s), like k_pull's finaliser
+struct UbCtl {
+    int64_t left;
+    uint32_t arrive;
+};
+
+__global__ void ub_round(UbCtl *c, cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_sw, int mode) {
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&c->arrive, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    c->arrive = 0;
+    if (c->left > 0) c->left -= 1;
+    __threadfence();
+    if (mode >= 1) cudaGraphSetConditional(h_loop, c->left > 0 ? 1u : 0u);
+    if (mode == 2) cudaGraphSetConditional(h_sw, 0u);
+}
+
+__global__ void ub_init(UbCtl *c, int64_t iters) {
+    c->left = iters;
+    c->arrive = 0;
+}
+
+// variant 0: stream launches; 1: WHILE{round}; 2: WHILE{SWITCH{round}};
+// 3: WHILE{round x4}; 4: WHILE{round x8}; 5: WHILE{cooperative round}
+int debug_graph(Ctx &ctx, int variant, int64_t iters, int blocks, double *us_out) {
+    cudaStream_t st = ctx.stream;
+    DevBuf cb;
+    PR_TRY(ensure(cb, sizeof(UbCtl)));
+    UbCtl *c = cb.as<UbCtl>();
+    cudaEvent_t e0, e1;
+    PR_CUDA(cudaEventCreate(&e0));
+    PR_CUDA(cudaEventCreate(&e1));
+    cudaGraphExec_t ex = nullptr;
+    cudaGraph_t G = nullptr;
+    if (variant >= 1) {
+        PR_CUDA(cudaGraphCreate(&G, 0));
+        cudaGraphConditionalHandle hl = 0, hs = 0;
+        PR_CUDA(cudaGraphConditionalHandleCreate(&hl, G, 1, cudaGraphCondAssignDefault));
+        if (variant == 2) PR_CUDA(cudaGraphConditionalHandleCreate(&hs, G, 0, cudaGraphCondAssignDefault));
+        cudaGraphNode_t n_init, n_while, n_sw, n_k;
+        int64_t it64 = iters;
+        void *a_init[] = {&c, &it64};
+        cudaKernelNodeParams kp = {};
+        kp.func = (void *)ub_init;
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(1);
+        kp.kernelParams = a_init;
+        PR_CUDA(cudaGraphAddKernelNode(&n_init, G, nullptr, 0, &kp));
+        cudaGraphNodeParams wp = {};
+        wp.type = cudaGraphNodeTypeConditional;
+        wp.conditional.handle = hl;
+        wp.conditional.type = cudaGraphCondTypeWhile;
+        wp.conditional.size = 1;
+        PR_CUDA(cudaGraphAddNode(&n_while, G, &n_init, 1, &wp));
+        cudaGraph_t body = wp.conditional.phGraph_out[0];
+        if (variant == 2) {
+            cudaGraphNodeParams sp = {};
+            sp.type = cudaGraphNodeTypeConditional;
+            sp.conditional.handle = hs;
+            sp.conditional.type = cudaGraphCondTypeSwitch;
+            sp.conditional.size = 2;
+            PR_CUDA(cudaGraphAddNode(&n_sw, body, nullptr, 0, &sp));
+            body = sp.conditional.phGraph_out[0];
+        }
+        int mode = variant == 2 ? 2 : 1;
+        void *a_r[] = {&c, &hl, &hs, &mode};
+        kp.func = (void *)ub_round;
+        kp.gridDim = dim3((unsigned)blocks);
+        kp.blockDim = dim3(256);
+        kp.kernelParams = a_r;
+        const int copies = variant == 3 ? 4 : variant == 4 ? 8 : 1;
+        cudaGraphNode_t prev = nullptr;
+        for (int k = 0; k < copies; ++k) {
+            PR_CUDA(cudaGraphAddKernelNode(&n_k, body, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
+            if (variant == 5) {
+                cudaKernelNodeAttrValue v = {};
+                v.cooperative = 1;
+                PR_CUDA(cudaGraphKernelNodeSetAttribute(n_k, cudaLaunchAttributeCooperative, &v));
+            }
+            prev = n_k;
+        }
+        PR_CUDA(cudaGraphInstantiate(&ex, G, 0));
+    }
+    float ms = 0.f;
+    for (int rep = 0; rep < 3; ++rep) {
+        PR_CUDA(cudaEventRecord(e0, st));
+        if (variant == 0) {
+            ub_init<<<1, 1, 0, st>>>(c, iters);
+            for (int64_t i = 0; i < iters; ++i) ub_round<<<blocks, 256, 0, st>>>(c, 0, 0, 0);
+        } else {
+            PR_CUDA(cudaGraphLaunch(ex, st));
+        }
+        PR_CUDA(cudaEventRecord(e1, st));
+        PR_CUDA(cudaEventSynchronize(e1));
+        PR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    }
+    if (ex) cudaGraphExecDestroy(ex);
+    if (G) cudaGraphDestroy(G);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *us_out = 1e3 * ms / (double)iters;
+    return PR_OK;
+}
+
 }  // namespace pr
 
