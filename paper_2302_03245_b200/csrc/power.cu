@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(256) k_pw_init(PowArgs A) {
 // nxt_v = sum z over in-edges + restart * p_v; block partial of sum(nxt)
 template <bool STREAM>
 __global__ void __launch_bounds__(256, 4) k_pw_gather(PowArgs A) {
+    if (A.use_graph && ((volatile PowCtl *)A.ctl)->done) return;  // unrolled slot after the stop
     const double restart = A.ctl->restart;
     Partial p;
     zero(p);
@@ -126,18 +127,19 @@ __global__ void __launch_bounds__(256, 4) k_pw_gather(PowArgs A) {
 
 // pi' = nxt / total; delta, converged count; next z and dangling sum
 __global__ void __launch_bounds__(256) k_pw_norm(PowArgs A) {
+    if (A.use_graph && ((volatile PowCtl *)A.ctl)->done) return;
     double total = A.ctl->total;
     Partial p;
     zero(p);
-    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (v < A.n) {
+    // grid-stride over one resident wave (few partials for the last block)
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < A.n; v += (int64_t)gridDim.x * blockDim.x) {
         double x = __ddiv_rn(A.nxt[v], total);
         double d = fabs(x - A.pi[v]);
-        p.l1 = d;                                       // delta (solvers.py:222)
-        p.conv_all = d <= A.threshold ? 1 : 0;          // solvers.py:227
+        p.l1 += d;                                      // delta (solvers.py:222)
+        p.conv_all += d <= A.threshold ? 1 : 0;         // solvers.py:227
         A.pi[v] = x;
         A.z[v] = z_of(A, v, x);
-        if (A.deg[v] == 0) p.above = x;                 // dangling mass for the next restart
+        if (A.deg[v] == 0) p.above += x;                // dangling mass for the next restart
     }
     pow_finish(A, p, [&](const Partial &acc) {
         PowCtl *c = A.ctl;
@@ -230,6 +232,10 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
     if (h_p) PR_CUDA(cudaMemcpyAsync((void *)A.p, h_p, 8 * n, cudaMemcpyHostToDevice, st));
     PR_CUDA(cudaMemsetAsync(A.ctl, 0, sizeof(PowCtl), st));
     unsigned g_all = grid_for(n, 256), g_gather = (unsigned)blk;
+    int occ_norm = 0;
+    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_norm, k_pw_norm, 256, 0));
+    const unsigned wave = (unsigned)(ctx.sm_count * (occ_norm > 0 ? occ_norm : 1));
+    const unsigned g_norm = g_all < wave ? g_all : wave;
 
     cudaEvent_t e0, e1;
     PR_CUDA(cudaEventCreate(&e0));
@@ -243,7 +249,7 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
         for (int64_t k = 0; k < iterations; ++k) {
             if (stream) k_pw_gather<true><<<g_gather, 256, 0, st>>>(A);
             else k_pw_gather<false><<<g_gather, 256, 0, st>>>(A);
-            k_pw_norm<<<g_all, 256, 0, st>>>(A);
+            k_pw_norm<<<g_norm, 256, 0, st>>>(A);
             PR_CUDA(cudaGetLastError());
             PowCtl hc;
             PR_CUDA(cudaMemcpyAsync(&hc, A.ctl, sizeof(hc), cudaMemcpyDeviceToHost, st));
@@ -269,8 +275,14 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
         wp.conditional.size = 1;
         PR_CUDA(cudaGraphAddNode(&n_while, G, &n_init, 1, &wp));
         cudaGraph_t body = wp.conditional.phGraph_out[0];
-        PR_TRY(add_node(body, &n_a, nullptr, 0, (void *)gather_fn, g_gather, args));
-        PR_TRY(add_node(body, &n_b, &n_a, 1, (void *)k_pw_norm, g_all, args));
+        // body unrolled into plain kernel nodes (a conditional iteration
+        // costs more than a kernel launch; slots after the stop exit at once)
+        cudaGraphNode_t prev = nullptr;
+        for (int k = 0; k < 4; ++k) {
+            PR_TRY(add_node(body, &n_a, prev ? &prev : nullptr, prev ? 1 : 0, (void *)gather_fn, g_gather, args));
+            PR_TRY(add_node(body, &n_b, &n_a, 1, (void *)k_pw_norm, g_norm, args));
+            prev = n_b;
+        }
         cudaGraphExec_t ex;
         PR_CUDA(cudaGraphInstantiate(&ex, G, 0));
         PR_CUDA(cudaEventRecord(e0, st));

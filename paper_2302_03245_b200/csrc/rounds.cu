@@ -566,6 +566,43 @@ __global__ void k_settle(RunArgs A, const int32_t *dang_ids, int64_t lo, int64_t
     }
 }
 
+// Fast-engine settle: w[u] = (c*reserved[u])/deg[u] once per source (the
+// same two-rounding term as engines.py:281), then a gather-sum per dangling
+// row with 8 loads in flight (bins.cuh helpers): one random load per edge
+// instead of two loads and a division.
+__global__ void k_settle_w(RunArgs A, int64_t n_src, double *__restrict__ w) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n_src; u += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t du = A.deg[u];
+        w[u] = du > 0 ? __ddiv_rn(__dmul_rn(A.c, A.reserved[u]), (double)du) : 0.0;
+    }
+}
+
+__global__ void k_settle_fast(RunArgs A, const double *__restrict__ w, const int32_t *__restrict__ dang_ids, int64_t lo,
+                              int64_t nd, const int64_t *__restrict__ src_off, const int32_t *__restrict__ src_ids,
+                              int thread_mode) {
+    if (thread_mode) {
+        for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const double acc = row_sum_thread<false>(src_ids, src_off[i], src_off[i + 1], w);
+            const int32_t d = dang_ids[i];
+            A.reserved[d] = A.h[d] + acc;
+            A.h[d] = 0.0;
+        }
+        return;
+    }
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = lo + warp; i < nd; i += nwarps) {
+        const double acc = span_sum_warp<false>(src_ids, src_off[i], src_off[i + 1], w);
+        if (lane == 0) {
+            const int32_t d = dang_ids[i];
+            A.reserved[d] = A.h[d] + acc;
+            A.h[d] = 0.0;
+        }
+    }
+}
+
 // first index of dangling vertices with <= 32 sources (run layout: receivers
 // sorted by descending in-degree, so the big ones lead)
 __global__ void k_count_big(const int64_t *src_off, int64_t nd, unsigned long long *out) {
@@ -1022,12 +1059,22 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
             const int64_t nd = g.ifp2.dangling;
             int64_t big = 0;
             if (!exact) PR_TRY(count_settle_big(g, &big));
-            if (big)
-                k_settle<<<grid_for(big * 32, 256), 256, 0, st>>>(A, g.dang_ids.as<int32_t>(), 0, big,
-                                                                  g.src_off.as<int64_t>(), g.src_ids.as<int32_t>(), 0);
-            if (nd > big)
-                k_settle<<<grid_for(nd - big, 256), 256, 0, st>>>(A, g.dang_ids.as<int32_t>(), big, nd,
-                                                                   g.src_off.as<int64_t>(), g.src_ids.as<int32_t>(), 1);
+            if (exact) {
+                k_settle<<<grid_for(nd, 256), 256, 0, st>>>(A, g.dang_ids.as<int32_t>(), 0, nd,
+                                                           g.src_off.as<int64_t>(), g.src_ids.as<int32_t>(), 1);
+            } else {
+                // sources are the non-dangling run ids [0, live_end); the
+                // round loop is over, so the share buffer holds w
+                const int64_t n_src = g.live_end >= 0 ? g.live_end : n;
+                double *w = A.s;
+                k_settle_w<<<grid_for(n_src, 256) > 4096 ? 4096 : grid_for(n_src, 256), 256, 0, st>>>(A, n_src, w);
+                if (big)
+                    k_settle_fast<<<grid_for(big * 32, 256), 256, 0, st>>>(
+                        A, w, g.dang_ids.as<int32_t>(), 0, big, g.src_off.as<int64_t>(), g.src_ids.as<int32_t>(), 0);
+                if (nd > big)
+                    k_settle_fast<<<grid_for(nd - big, 256), 256, 0, st>>>(
+                        A, w, g.dang_ids.as<int32_t>(), big, nd, g.src_off.as<int64_t>(), g.src_ids.as<int32_t>(), 1);
+            }
         }
     }
     int include_h = algo == PR_ALGO_IFP1 ? 1 : 0;
