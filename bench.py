@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--cpu-sample-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--push-switch", type=float, default=0.0,
+                    help="AUTO policy: push when the next round's work < this fraction of (E_D+|D|) (0 = library default)")
     return ap.parse_args()
 
 
@@ -198,7 +200,8 @@ def run_ours(args):
     def step():
         flush.zero_()
         torch.cuda.synchronize()
-        _, _, res, _, _ = dev.run(args.algo, args.mode, DAMPING, XI, 1_000_000, _lib.CONV_SCAN, row_cap=1)
+        _, _, res, _, _ = dev.run(args.algo, args.mode, DAMPING, XI, 1_000_000, _lib.CONV_SCAN,
+                                  push_switch=args.push_switch, row_cap=1)
         return res
 
     for _ in range(args.warmup):
@@ -338,8 +341,11 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
 
 def e2e_measure(args, g, dev_resident):
     """Same metric through the public API from HOST buffers: each step uploads
-    the reference-layout graph (int64 CSR+CSC, pinned), rebuilds the IFP2
-    split on the device, solves, and copies the vector back."""
+    the reference-layout graph (pinned int64 arrays; the upload copies what the
+    fast engine needs -- in-adjacency + out_offsets -- and defers out_targets),
+    builds the run layout and IFP2 split on the device, solves, and copies the
+    vector back.  h2d_bytes_per_step counts the bytes actually copied."""
+    from paper_2302_03245_b200.graph import device_graph
     import torch
     import paper_2302_03245_b200 as P
     from types import SimpleNamespace
@@ -362,6 +368,7 @@ def e2e_measure(args, g, dev_resident):
         if i >= args.warmup:
             times.append(dt)
             ops = tr.final.push_ops
+            h2d = device_graph(obj).h2d_bytes
         del obj
     mean = sum(times) / len(times)
     return {"value": ops / mean / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": int(h2d),

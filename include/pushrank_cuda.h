@@ -131,10 +131,16 @@ int pr_graph_from_edges(pr_ctx *ctx, int64_t n, const int64_t *src, const int64_
 /* Same from device-resident int64 edge arrays (e.g. pr_rmat_generate output). */
 int pr_graph_from_device_edges(pr_ctx *ctx, int64_t n, const int64_t *d_src,
                                const int64_t *d_dst, int64_t m_raw, pr_graph **out);
-/* Upload an already-built reference Graph (graph.py:21-42 arrays). */
+/* Upload an already-built reference Graph (graph.py:21-42 arrays).
+ * out_targets may be NULL: the fast engines (pr_run, modes auto/pull/push)
+ * and pr_power only need the in-adjacency and out_offsets (they rebuild the
+ * out-adjacency of their own layout on the device); classify, the
+ * original-layout IFP2 arrays, exact mode and exporting out_targets then
+ * fail with PR_ERR_STATE until pr_graph_attach_out_targets is called. */
 int pr_graph_upload(pr_ctx *ctx, int64_t n, int64_t m, const int64_t *out_offsets,
                     const int64_t *out_targets, const int64_t *in_offsets,
                     const int64_t *in_sources, pr_graph **out);
+int pr_graph_attach_out_targets(pr_graph *g, const int64_t *out_targets);
 int pr_graph_destroy(pr_graph *g);
 int pr_graph_info(const pr_graph *g, int64_t *n, int64_t *m);
 /* Graph arrays back to the host (int64, reference layout); NULL skips one. */
@@ -222,6 +228,11 @@ int pr_device_alloc(pr_ctx *ctx, int64_t bytes, void **d_ptr);
 int pr_device_free(pr_ctx *ctx, void *d_ptr);
 int pr_memcpy_h2d(pr_ctx *ctx, void *d_dst, const void *h_src, int64_t bytes);
 int pr_memcpy_d2h(pr_ctx *ctx, void *h_dst, const void *d_src, int64_t bytes);
+/* Page-locked host blocks from a process-wide cache (a freed block is reused
+ * by the next request of the same size): output buffers that pr_run copies
+ * into at full link speed instead of through pageable staging. */
+int pr_host_alloc(int64_t bytes, void **h_ptr);
+int pr_host_free(void *h_ptr);
 
 #ifdef __cplusplus
 }

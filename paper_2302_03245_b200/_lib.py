@@ -8,6 +8,7 @@ every entry point raises ``RuntimeError`` ("fail loudly").
 from __future__ import annotations
 
 import ctypes
+import weakref
 import os
 import threading
 
@@ -80,6 +81,9 @@ SIGNATURES = {
     "pr_graph_from_edges": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_i64, _PP]),
     "pr_graph_from_device_edges": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_i64, _PP]),
     "pr_graph_upload": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, _PP]),
+    "pr_graph_attach_out_targets": (ctypes.c_int, [c_vp, c_vp]),
+    "pr_host_alloc": (ctypes.c_int, [c_i64, _PP]),
+    "pr_host_free": (ctypes.c_int, [c_vp]),
     "pr_graph_destroy": (ctypes.c_int, [c_vp]),
     "pr_graph_info": (ctypes.c_int, [c_vp, _PI64, _PI64]),
     "pr_graph_export": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
@@ -161,6 +165,25 @@ def ptr(a) -> c_vp | None:
     if a is None:
         return None
     return c_vp(a.ctypes.data)
+
+
+def pinned_empty(n: int, dtype=np.float64) -> np.ndarray:
+    """numpy array in a page-locked block from the library's cache
+    (pr_host_alloc); the block returns to the cache when the array dies."""
+    dt = np.dtype(dtype)
+    nbytes = max(int(n), 1) * dt.itemsize
+    p = c_vp()
+    check(load().pr_host_alloc(nbytes, ctypes.byref(p)), "host_alloc")
+    buf = (ctypes.c_char * nbytes).from_address(p.value)
+    weakref.finalize(buf, _host_free, p.value)
+    return np.frombuffer(buf, dtype=dt, count=int(n))
+
+
+def _host_free(addr: int) -> None:
+    try:
+        load().pr_host_free(c_vp(addr))
+    except Exception:
+        pass
 
 
 def device_count() -> int:

@@ -3,7 +3,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "internal.cuh"
 
@@ -196,10 +198,7 @@ int pr_graph_upload(pr_ctx *ctx, int64_t n, int64_t m, const int64_t *out_offset
     CHECK_PTR(out, "out");
     CHECK_PTR(out_offsets, "out_offsets");
     CHECK_PTR(in_offsets, "in_offsets");
-    if (m > 0) {
-        CHECK_PTR(out_targets, "out_targets");
-        CHECK_PTR(in_sources, "in_sources");
-    }
+    if (m > 0) CHECK_PTR(in_sources, "in_sources");
     PR_TRY(set_device(ctx->c));
     Graph *g = nullptr;
     PR_TRY(upload_graph(ctx->c, n, m, out_offsets, out_targets, in_offsets, in_sources, &g));
@@ -207,12 +206,22 @@ int pr_graph_upload(pr_ctx *ctx, int64_t n, int64_t m, const int64_t *out_offset
     return PR_OK;
 }
 
+int pr_graph_attach_out_targets(pr_graph *g, const int64_t *out_targets) {
+    CHECK_PTR(g, "graph");
+    if (g->g->m > 0) CHECK_PTR(out_targets, "out_targets");
+    PR_TRY(set_device(*g->g->ctx));
+    return attach_out_targets(*g->g, out_targets);
+}
+
 int pr_graph_destroy(pr_graph *g) {
     if (!g) return PR_OK;
     cudaSetDevice(g->g->ctx->device);
     alloc_stream() = g->g->ctx->stream;
     cudaStreamSynchronize(g->g->ctx->stream);
+    phase_mark(g->g->ctx->stream, "destroy: sync");
+    cudaStream_t st = g->g->ctx->stream;
     delete g->g;
+    phase_mark(st, "destroy: free");
     delete g;
     return PR_OK;
 }
@@ -370,6 +379,39 @@ int pr_device_free(pr_ctx *ctx, void *d_ptr) {
     CHECK_PTR(ctx, "ctx");
     PR_TRY(set_device(ctx->c));
     PR_CUDA(cudaFree(d_ptr));
+    return PR_OK;
+}
+
+static std::mutex g_host_mu;
+static std::unordered_map<void *, size_t> g_host_size;          // live + cached blocks
+static std::unordered_multimap<size_t, void *> g_host_free;     // cached blocks by size
+
+int pr_host_alloc(int64_t bytes, void **h_ptr) {
+    CHECK_PTR(h_ptr, "h_ptr");
+    const size_t sz = bytes > 0 ? (size_t)bytes : 16;
+    {
+        std::lock_guard<std::mutex> lk(g_host_mu);
+        auto it = g_host_free.find(sz);
+        if (it != g_host_free.end()) {
+            *h_ptr = it->second;
+            g_host_free.erase(it);
+            return PR_OK;
+        }
+    }
+    void *p = nullptr;
+    PR_CUDA(cudaHostAlloc(&p, sz, cudaHostAllocPortable));
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    g_host_size[p] = sz;
+    *h_ptr = p;
+    return PR_OK;
+}
+
+int pr_host_free(void *h_ptr) {
+    if (!h_ptr) return PR_OK;
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    auto it = g_host_size.find(h_ptr);
+    if (it == g_host_size.end()) return fail(PR_ERR_ARG, "pr_host_free: not a pr_host_alloc block");
+    g_host_free.emplace(it->second, h_ptr);
     return PR_OK;
 }
 

@@ -122,7 +122,7 @@ static int alloc_graph_arrays(Graph &g) {
     PR_TRY(ensure(g.out_off, sizeof(int64_t) * (g.n + 1)));
     PR_TRY(ensure(g.in_off, sizeof(int64_t) * (g.n + 1)));
     PR_TRY(ensure(g.out_deg, sizeof(int32_t) * g.n));
-    PR_TRY(ensure(g.out_tgt, sizeof(int32_t) * g.m));
+    if (g.has_csr) PR_TRY(ensure(g.out_tgt, sizeof(int32_t) * g.m));
     PR_TRY(ensure(g.in_src, sizeof(int32_t) * g.m));
     return PR_OK;
 }
@@ -287,6 +287,7 @@ static int compact_flag(Ctx &ctx, const uint8_t *flags, uint8_t bit, int64_t n, 
 
 int classify_device(Graph &g) {
     if (g.classified) return PR_OK;
+    PR_TRY(need_csr(g, "classify"));
     Ctx &ctx = *g.ctx;
     cudaStream_t st = ctx.stream;
     int64_t n = g.n;
@@ -371,40 +372,26 @@ int classify_export(Graph &g, int64_t *outs[4]) {
 // ---------------------------------------------------------------- K3
 
 // graph.py:334-340: per-row count of dangling targets
-// warp per 32 consecutive vertices: short rows (<= 32 edges) on their own
-// lane, long rows walked by the whole warp with 4 loads in flight per lane
-__global__ void k_dtc(const int64_t *__restrict__ out_off, const int32_t *__restrict__ out_tgt,
-                      const int32_t *__restrict__ out_deg, int64_t n, int32_t *__restrict__ dtc) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w * 32 < n; w += nwarps) {
-        const int64_t v = w * 32 + lane;
-        int64_t lo = 0, hi = 0;
-        if (v < n) {
-            lo = out_off[v];
-            hi = out_off[v + 1];
+// dtc[u] = #(out-neighbours of u with out-degree 0), counted from the CSC:
+// every in-edge (u -> v) of a dangling v adds one to dtc[u].  Edge-parallel
+// and load-balanced (the row of an edge by binary search inside the block's
+// tile, as in k_seg_gather), so hub rows cost what short rows cost, and the
+// out-adjacency is not needed.
+__global__ void __launch_bounds__(256) k_dtc_csc(const int64_t *__restrict__ in_off, const int32_t *__restrict__ in_src,
+                                                 const int32_t *__restrict__ out_deg, int64_t n, int64_t m,
+                                                 int32_t *__restrict__ dtc) {
+    __shared__ int64_t s_r0, s_r1;
+    for (int64_t base = blockIdx.x * (int64_t)SEG_TILE; base < m; base += (int64_t)gridDim.x * SEG_TILE) {
+        const int64_t end = base + SEG_TILE < m ? base + SEG_TILE : m;
+        if (threadIdx.x == 0) s_r0 = seg_upper(in_off, 0, n + 1, base) - 1;
+        if (threadIdx.x == 32) s_r1 = seg_upper(in_off, 0, n + 1, end - 1);
+        __syncthreads();
+        const int64_t r0 = s_r0, r1 = s_r1;
+        for (int64_t e = base + threadIdx.x; e < end; e += blockDim.x) {
+            const int64_t v = seg_upper(in_off, r0, r1 + 1, e) - 1;
+            if (__ldg(&out_deg[v]) == 0) atomicAdd(&dtc[__ldg(&in_src[e])], 1);
         }
-        const bool big = hi - lo > 32;
-        int32_t c = 0;
-        if (!big)
-            for (int64_t e = lo; e < hi; ++e) c += __ldg(&out_deg[__ldg(&out_tgt[e])]) == 0;
-        unsigned m = __ballot_sync(0xffffffffu, big);
-        while (m) {
-            const int j = __ffs(m) - 1;
-            m &= m - 1;
-            const int64_t blo = __shfl_sync(0xffffffffu, lo, j), bhi = __shfl_sync(0xffffffffu, hi, j);
-            int32_t k = 0;
-            for (int64_t e = blo + lane; e < bhi; e += 128) {
-                int t[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) t[q] = e + 32 * q < bhi ? __ldg(&out_tgt[e + 32 * q]) : -1;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) k += t[q] >= 0 && __ldg(&out_deg[t[q]]) == 0;
-            }
-            k = __reduce_add_sync(0xffffffffu, (unsigned)k);
-            if (lane == j) c = k;
-        }
-        if (v < n) dtc[v] = c;
+        __syncthreads();
     }
 }
 
@@ -429,8 +416,11 @@ int ensure_dtc(Graph &g) {
         g.has_dtc = true;
         return PR_OK;
     }
-    k_dtc<<<gs_grid(*g.ctx, g.n), 256, 0, g.ctx->stream>>>(g.out_off.as<int64_t>(), g.out_tgt.as<int32_t>(),
-                                                           g.out_deg.as<int32_t>(), g.n, g.dtc.as<int32_t>());
+    PR_CUDA(cudaMemsetAsync(g.dtc.ptr, 0, 4 * g.n, g.ctx->stream));
+    if (g.m)
+        k_dtc_csc<<<seg_grid(*g.ctx, g.m), 256, 0, g.ctx->stream>>>(g.in_off.as<int64_t>(), g.in_src.as<int32_t>(),
+                                                                   g.out_deg.as<int32_t>(), g.n, g.m,
+                                                                   g.dtc.as<int32_t>());
     PR_CUDA(cudaGetLastError());
     g.has_dtc = true;
     return PR_OK;
@@ -474,6 +464,7 @@ __global__ void k_tail_rows(const int64_t *__restrict__ in_off, int64_t live_end
 
 int preprocess_ifp2_device(Graph &g) {
     if (g.has_ifp2) return PR_OK;
+    PR_TRY(need_csr(g, "the IFP2 live CSR"));
     Ctx &ctx = *g.ctx;
     cudaStream_t st = ctx.stream;
     int64_t n = g.n, m = g.m;
@@ -668,6 +659,75 @@ static int permute_adjacency(Ctx &ctx, const DevBuf &off, const DevBuf &col, con
     return PR_OK;
 }
 
+// row id of every edge of a CSR/CSC (load-balanced, as k_seg_gather)
+__global__ void __launch_bounds__(256) k_edge_rows(const int64_t *__restrict__ off, int64_t rows, int64_t m,
+                                                   int32_t *__restrict__ row_of) {
+    __shared__ int64_t s_r0, s_r1;
+    for (int64_t base = blockIdx.x * (int64_t)SEG_TILE; base < m; base += (int64_t)gridDim.x * SEG_TILE) {
+        const int64_t end = base + SEG_TILE < m ? base + SEG_TILE : m;
+        if (threadIdx.x == 0) s_r0 = seg_upper(off, 0, rows + 1, base) - 1;
+        if (threadIdx.x == 32) s_r1 = seg_upper(off, 0, rows + 1, end - 1);
+        __syncthreads();
+        const int64_t r0 = s_r0, r1 = s_r1;
+        for (int64_t e = base + threadIdx.x; e < end; e += blockDim.x)
+            row_of[e] = (int32_t)(seg_upper(off, r0, r1 + 1, e) - 1);
+        __syncthreads();
+    }
+}
+
+// The out-adjacency of the run layout from its in-adjacency: a stable sort of
+// the CSC's (source, destination) pairs by source.  Destinations come out
+// ascending inside every row, so the result is deterministic.  Used when the
+// graph was uploaded CSC-only (the fast engines never need the original
+// out_targets).
+static int csr_from_csc(Ctx &ctx, const DevBuf &orig_out_off, const DevBuf &perm, int64_t n, int64_t m,
+                        const DevBuf &in_off, const DevBuf &in_src, DevBuf &out_off, DevBuf &out_tgt) {
+    cudaStream_t st = ctx.stream;
+    DevBuf len, keys_out, rows;
+    PR_TRY(ensure(len, 8 * (n + 1)));
+    PR_TRY(ensure(out_off, 8 * (n + 1)));
+    PR_TRY(ensure(out_tgt, 4 * (m ? m : 1)));
+    k_perm_len<<<gs_grid(ctx, n + 1), 256, 0, st>>>(orig_out_off.as<int64_t>(), perm.as<int32_t>(), n, len.as<int64_t>());
+    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, len.as<int64_t>(), out_off.as<int64_t>(), (int)(n + 1), st);
+    }));
+    if (!m) return PR_OK;
+    PR_TRY(ensure(keys_out, 4 * m));
+    PR_TRY(ensure(rows, 4 * m));
+    k_edge_rows<<<seg_grid(ctx, m), 256, 0, st>>>(in_off.as<int64_t>(), n, m, rows.as<int32_t>());
+    int bits = 1;
+    while (bits < 31 && ((int64_t)1 << bits) < n) ++bits;
+    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, (const uint32_t *)in_src.ptr, keys_out.as<uint32_t>(),
+                                               rows.as<int32_t>(), out_tgt.as<int32_t>(), m, 0, bits, st);
+    }));
+    return PR_OK;
+}
+
+int need_csr(const Graph &g, const char *what) {
+    if (g.has_csr) return PR_OK;
+    return fail(PR_ERR_STATE, std::string(what) +
+                                  " needs the out-adjacency; the graph was uploaded without out_targets "
+                                  "(pr_graph_attach_out_targets)");
+}
+
+int attach_out_targets(Graph &g, const int64_t *out_tgt) {
+    if (g.has_csr) return PR_OK;
+    Ctx &ctx = *g.ctx;
+    cudaStream_t st = ctx.stream;
+    PR_TRY(ensure(g.out_tgt, 4 * (g.m ? g.m : 1)));
+    if (g.m) {
+        DevBuf stage;
+        PR_TRY(ensure(stage, 8 * g.m));
+        PR_CUDA(cudaMemcpyAsync(stage.ptr, out_tgt, 8 * g.m, cudaMemcpyHostToDevice, st));
+        k_narrow<<<gs_grid(ctx, g.m), 256, 0, st>>>(stage.as<int64_t>(), g.m, g.out_tgt.as<int32_t>());
+        PR_CUDA(cudaStreamSynchronize(st));
+        PR_CUDA(cudaGetLastError());
+    }
+    g.has_csr = true;
+    return PR_OK;
+}
+
 int ensure_run_layout(Graph &g) {
     if (g.run) return PR_OK;
     Ctx &ctx = *g.ctx;
@@ -695,8 +755,9 @@ int ensure_run_layout(Graph &g) {
     r->n = n;
     r->m = m;
     r->raw = g.raw;
-    int rc = permute_adjacency(ctx, g.out_off, g.out_tgt, g.perm, g.rank, n, m, r->out_off, r->out_tgt);
-    if (!rc) rc = permute_adjacency(ctx, g.in_off, g.in_src, g.perm, g.rank, n, m, r->in_off, r->in_src);
+    int rc = permute_adjacency(ctx, g.in_off, g.in_src, g.perm, g.rank, n, m, r->in_off, r->in_src);
+    if (!rc) rc = g.has_csr ? permute_adjacency(ctx, g.out_off, g.out_tgt, g.perm, g.rank, n, m, r->out_off, r->out_tgt)
+                            : csr_from_csc(ctx, g.out_off, g.perm, n, m, r->in_off, r->in_src, r->out_off, r->out_tgt);
     if (!rc) rc = ensure(r->out_deg, 4 * n);
     if (!rc) k_degree<<<gs_grid(ctx, n), 256, 0, st>>>(r->out_off.as<int64_t>(), n, r->out_deg.as<int32_t>());
     int64_t bounds[2] = {n, n};
@@ -820,6 +881,7 @@ int upload_graph(Ctx &ctx, int64_t n, int64_t m, const int64_t *out_off, const i
     g->n = n;
     g->m = m;
     g->raw = m;
+    g->has_csr = out_tgt != nullptr || m == 0;
     int rc = alloc_graph_arrays(*g);
     DevBuf stage;
     if (!rc) rc = ensure(stage, 8 * (m > 0 ? m : 1));
@@ -827,8 +889,10 @@ int upload_graph(Ctx &ctx, int64_t n, int64_t m, const int64_t *out_off, const i
         cudaError_t e = cudaMemcpyAsync(g->out_off.ptr, out_off, 8 * (n + 1), cudaMemcpyHostToDevice, st);
         if (e == cudaSuccess) e = cudaMemcpyAsync(g->in_off.ptr, in_off, 8 * (n + 1), cudaMemcpyHostToDevice, st);
         if (e == cudaSuccess && m) {
-            e = cudaMemcpyAsync(stage.ptr, out_tgt, 8 * m, cudaMemcpyHostToDevice, st);
-            k_narrow<<<gs_grid(ctx, m), 256, 0, st>>>(stage.as<int64_t>(), m, g->out_tgt.as<int32_t>());
+            if (out_tgt) {
+                e = cudaMemcpyAsync(stage.ptr, out_tgt, 8 * m, cudaMemcpyHostToDevice, st);
+                k_narrow<<<gs_grid(ctx, m), 256, 0, st>>>(stage.as<int64_t>(), m, g->out_tgt.as<int32_t>());
+            }
             if (e == cudaSuccess) e = cudaMemcpyAsync(stage.ptr, in_src, 8 * m, cudaMemcpyHostToDevice, st);
             k_narrow<<<gs_grid(ctx, m), 256, 0, st>>>(stage.as<int64_t>(), m, g->in_src.as<int32_t>());
         }
@@ -850,6 +914,7 @@ int export_graph(Graph &g, int64_t *out_off, int64_t *out_tgt, int64_t *in_off, 
     if (out_off) PR_CUDA(cudaMemcpyAsync(out_off, g.out_off.ptr, 8 * (g.n + 1), cudaMemcpyDeviceToHost, st));
     if (in_off) PR_CUDA(cudaMemcpyAsync(in_off, g.in_off.ptr, 8 * (g.n + 1), cudaMemcpyDeviceToHost, st));
     if (out_tgt && g.m) {
+        PR_TRY(need_csr(g, "exporting out_targets"));
         k_widen<<<gs_grid(ctx, g.m), 256, 0, st>>>(g.out_tgt.as<int32_t>(), g.m, wide.as<int64_t>());
         PR_CUDA(cudaMemcpyAsync(out_tgt, wide.ptr, 8 * g.m, cudaMemcpyDeviceToHost, st));
         PR_CUDA(cudaStreamSynchronize(st));

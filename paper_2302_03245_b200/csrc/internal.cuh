@@ -105,7 +105,8 @@ struct Graph {
     int64_t live_end = -1;
     int64_t class0_end = -1;   // run layout: [0, class0_end) have in>0 & out>0
     DevBuf out_off;   // int64 [n+1]
-    DevBuf out_tgt;   // int32 [m]
+    DevBuf out_tgt;   // int32 [m] (absent until attached when uploaded CSC-only)
+    bool has_csr = true;
     DevBuf out_deg;   // int32 [n]
     DevBuf in_off;    // int64 [n+1]
     DevBuf in_src;    // int32 [m]
@@ -177,6 +178,8 @@ struct Graph {
 };
 
 int ensure_dtc(Graph &g);
+int need_csr(const Graph &g, const char *what);
+int attach_out_targets(Graph &g, const int64_t *out_tgt);
 int count_dangling(Graph &g);
 int ensure_run_layout(Graph &g);
 void invalidate_cache(Graph &g);

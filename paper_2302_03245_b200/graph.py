@@ -32,6 +32,8 @@ class DeviceGraph:
         self.n, self.m = int(n.value), int(m.value)
         self._counts = None
         self._ifp2 = None
+        self._pending_out_targets = None   # host out_targets not yet on the device
+        self.h2d_bytes = 0                 # bytes copied host -> device so far
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -52,14 +54,34 @@ class DeviceGraph:
         return cls(h, ctx)
 
     @classmethod
-    def upload(cls, g, ctx=None) -> "DeviceGraph":
+    def upload(cls, g, ctx=None, lazy_out_targets: bool = True) -> "DeviceGraph":
+        """Upload a reference-layout graph.  With ``lazy_out_targets`` only the
+        in-adjacency and ``out_offsets`` are copied: the fast engines rebuild
+        the out-adjacency of their own vertex layout on the device, and
+        ``out_targets`` follows on the first call that needs the original one
+        (classify, IFP2 exports, exact mode, export)."""
         ctx = ctx or _lib.context()
-        arrs = [np.ascontiguousarray(getattr(g, k), dtype=np.int64)
-                for k in ("out_offsets", "out_targets", "in_offsets", "in_sources")]
+        arrs = {k: np.ascontiguousarray(getattr(g, k), dtype=np.int64)
+                for k in ("out_offsets", "out_targets", "in_offsets", "in_sources")}
+        lazy = lazy_out_targets and int(g.m) > 0
         h = ctypes.c_void_p()
-        _lib.check(_lib.load().pr_graph_upload(ctx.handle, int(g.n), int(g.m), *[_lib.ptr(a) for a in arrs],
+        _lib.check(_lib.load().pr_graph_upload(ctx.handle, int(g.n), int(g.m), _lib.ptr(arrs["out_offsets"]),
+                                               None if lazy else _lib.ptr(arrs["out_targets"]),
+                                               _lib.ptr(arrs["in_offsets"]), _lib.ptr(arrs["in_sources"]),
                                                ctypes.byref(h)), "upload")
-        return cls(h, ctx)
+        dev = cls(h, ctx)
+        dev.h2d_bytes = sum(a.nbytes for k, a in arrs.items() if not (lazy and k == "out_targets"))
+        if lazy:
+            dev._pending_out_targets = arrs["out_targets"]
+        return dev
+
+    def need_out_targets(self) -> None:
+        """Copy the original out_targets to the device if the upload deferred them."""
+        a = self._pending_out_targets
+        if a is not None:
+            _lib.check(_lib.load().pr_graph_attach_out_targets(self.handle, _lib.ptr(a)), "attach_out_targets")
+            self.h2d_bytes += a.nbytes
+            self._pending_out_targets = None
 
     @classmethod
     def rmat(cls, scale: int, edge_factor: int, a=0.57, b=0.19, c=0.19, seed: int = 0, ctx=None):
@@ -71,6 +93,7 @@ class DeviceGraph:
 
     # -- exports
     def export(self) -> dict:
+        self.need_out_targets()
         n, m = self.n, self.m
         out = {"out_offsets": np.zeros(n + 1, np.int64), "out_targets": np.zeros(max(m, 1), np.int64),
                "in_offsets": np.zeros(n + 1, np.int64), "in_sources": np.zeros(max(m, 1), np.int64)}
@@ -83,6 +106,7 @@ class DeviceGraph:
 
     def classify(self) -> _lib.ClassCounts:
         if self._counts is None:
+            self.need_out_targets()
             c = _lib.ClassCounts()
             _lib.check(_lib.load().pr_classify(self.handle, ctypes.byref(c)), "classify")
             self._counts = c
@@ -110,6 +134,7 @@ class DeviceGraph:
         return self._ifp2
 
     def ifp2_export(self) -> dict:
+        self.need_out_targets()
         c = self.preprocess_ifp2()
         n = self.n
         out = {"live_offsets": np.zeros(n + 1, np.int64), "live_targets": np.zeros(max(c.live_edges, 1), np.int64),
@@ -129,6 +154,8 @@ class DeviceGraph:
             on_round=None, row_cap: int = 1 << 16, values_out: np.ndarray | None = None):
         """One solve through pr_run; returns (values, rows, result, reserved, pending)."""
         n = self.n
+        if mode == "exact":
+            self.need_out_targets()
         # PUSHRANK_HOST_LOOP=1 launches the same kernels round by round from
         # the host (ncu cannot profile kernel nodes of conditional graphs)
         host_loop = host_loop or os.environ.get("PUSHRANK_HOST_LOOP", "0") == "1"
@@ -146,7 +173,14 @@ class DeviceGraph:
                 on_round(int(t), r, h)
             cb = _lib.ROUND_CB(_cb)
             params.on_round = cb
-        values = values_out if values_out is not None else np.empty(n, np.float64)
+        # page-locked output: the D2H copy runs at link speed (a pageable
+        # destination goes through driver staging at ~5 GB/s)
+        if values_out is not None:
+            values = values_out
+        elif os.environ.get("PUSHRANK_PINNED_OUT", "1") != "0":
+            values = _lib.pinned_empty(n)
+        else:
+            values = np.empty(n, np.float64)
         reserved = np.empty(n, np.float64) if want_state else None
         pending = np.empty(n, np.float64) if want_state else None
         rows = np.zeros(row_cap, _lib.ROUND_DTYPE)

@@ -93,6 +93,38 @@ def test_upload_roundtrip_and_errors():
         P.from_edges(0, [], [])
 
 
+def test_lazy_out_targets_upload():
+    """CSC-only upload: the fast engines rebuild their out-adjacency on the
+    device; calls that need the original out_targets attach them on demand,
+    and the C-ABI refuses them loudly before that."""
+    from paper_2302_03245_b200 import _lib
+    import ctypes
+    n, src, dst = synthetic.make("c1", seed=3)
+    ref = oracle.from_edges(n, src, dst)
+    lazy = P.graph.DeviceGraph.upload(ref)
+    eager = P.graph.DeviceGraph.upload(ref, lazy_out_targets=False)
+    assert lazy._pending_out_targets is not None
+    assert lazy.h2d_bytes == eager.h2d_bytes - 8 * ref.m
+    c = _lib.ClassCounts()
+    assert _lib.load().pr_classify(lazy.handle, ctypes.byref(c)) == _lib.PR_ERR_STATE
+    assert "out_targets" in _lib.load().pr_last_error().decode()
+    for algo in ("ifp1", "ifp2"):
+        lazy.preprocess_ifp2()
+        eager.preprocess_ifp2()
+        vl, _, rl, _, _ = lazy.run(algo, "auto", 0.85, 1e-10, 10_000, _lib.CONV_SCAN)
+        ve, _, re, _, _ = eager.run(algo, "auto", 0.85, 1e-10, 10_000, _lib.CONV_SCAN)
+        # push rounds add with atomics, so the two runs can differ in the last
+        # bits (and, rarely, in a vertex sitting exactly at the threshold)
+        assert abs(rl.push_ops - re.push_ops) <= 1e-3 * re.push_ops and abs(rl.rounds - re.rounds) <= 1, algo
+        assert np.abs(vl - ve).sum() <= 1e-11, algo
+    assert lazy._pending_out_targets is not None   # never needed by the fast engines
+    assert np.array_equal(lazy.dangling_target_counts(), eager.dangling_target_counts())
+    out = lazy.export()                            # attaches
+    assert lazy._pending_out_targets is None
+    assert np.array_equal(out["out_targets"], ref.out_targets)
+    assert lazy.classify().dangling == eager.classify().dangling
+
+
 def test_rmat_device_generator_matches_numpy():
     from paper_2302_03245_b200 import _lib
     import ctypes
