@@ -81,10 +81,141 @@ __device__ __forceinline__ double span_sum_warp(const int32_t *__restrict__ csc,
     return acc;
 }
 
+#ifndef PR_UNIT_RING
+#define PR_UNIT_RING 1
+#endif
+
+// Row callbacks R (a functor):
+//   R::Pre pre(bool valid, int64_t row)   per-row loads that do not depend on
+//                                         the sum (issued before the gathers)
+//   void fin(bool valid, const Pre&, double sum)   all 32 lanes of a warp
+//   void single(int64_t row, double sum)           one thread (hub rows)
+// PREFETCH: load a row's bounds and drain inputs before its gathers (more
+// live registers; pays when the round is latency-bound, i.e. L2-resident)
+template <bool STREAM, bool PREFETCH, class R>
+__device__ __forceinline__ void bins_run(const BinView &B, const double *__restrict__ x, R &rows) {
+    __shared__ double red[8];
+    __shared__ int64_t next_unit[2];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int64_t warp_rows = B.n_hub + B.n_warp;
+    // dynamic unit dispatch: first unit = blockIdx.x, then one atomic per unit
+    // (units are ordered heaviest first); the round finaliser resets the counter
+    int ring = 0;
+    for (int64_t u = blockIdx.x; u < B.n_units;) {
+#if PR_DYNAMIC_UNITS
+        // claim the following unit now; the atomic's latency hides behind this unit
+        unsigned long long claim = 0;
+        if (tid == 0) claim = atomicAdd(B.unit_ctr, 1ull);
+#endif
+        const int2 d = B.units[u];
+        if (d.y < 0) {
+            // ---- HUB_CHUNK edges of one hub row, whole block
+            const int64_t r = d.x, c = -(int64_t)d.y - 1;
+            const int64_t rb = B.doff[r], re = B.doff[r + 1];
+            const int64_t c0 = rb + c * HUB_CHUNK;
+            const int64_t c1 = c0 + HUB_CHUNK < re ? c0 + HUB_CHUNK : re;
+            int idx[HUB_CHUNK / 256];
+#pragma unroll
+            for (int q = 0; q < HUB_CHUNK / 256; ++q) {
+                const int64_t e = c0 + tid + 256 * q;
+                idx[q] = e < c1 ? ld_idx<STREAM>(&B.csc[e]) : -1;
+            }
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < HUB_CHUNK / 256; ++q) acc += idx[q] >= 0 ? ld_share(&x[idx[q]]) : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            __syncthreads();
+            if (lane == 0) red[wid] = acc;
+            __syncthreads();
+            if (tid == 0) {
+                double s = 0.0;
+                for (int k = 0; k < 8; ++k) s += red[k];
+                const int nch = (int)((re - rb + HUB_CHUNK - 1) / HUB_CHUNK);
+                B.chunk_part[u] = s;
+                __threadfence();
+                if (atomicAdd(&B.row_cnt[r], 1) == nch - 1) {
+                    __threadfence();
+                    const int64_t first = B.chunk_base[r];
+                    double tot = 0.0;
+                    for (int k = 0; k < nch; ++k) tot += __ldcg(&B.chunk_part[first + k]);
+                    B.row_cnt[r] = 0;
+                    rows.single(r, tot);
+                }
+            }
+        } else if (d.x < warp_rows) {
+            // ---- warp rows: warp w takes rows w, w+8, ...; lane j loads the
+            // bounds and drain inputs of row j of the batch up front, then the
+            // warp sums the rows one by one and drains them lane-parallel
+            for (int64_t base = d.x + wid; base < d.y; base += 8 * 32) {
+                const int64_t my_row = base + 8 * lane;
+                const bool my_valid = my_row < d.y;
+                const int cnt = __popc(__ballot_sync(0xffffffffu, my_valid));
+                double mine = 0.0;
+                if constexpr (PREFETCH) {
+                    int64_t my_lo = 0, my_hi = 0;
+                    if (my_valid) {
+                        my_lo = B.doff[my_row];
+                        my_hi = B.doff[my_row + 1];
+                    }
+                    const auto pre = rows.pre(my_valid, my_row);
+                    for (int j = 0; j < cnt; ++j) {
+                        const int64_t lo = __shfl_sync(0xffffffffu, my_lo, j),
+                                      hi = __shfl_sync(0xffffffffu, my_hi, j);
+                        const double s = span_sum_warp<STREAM>(B.csc, lo, hi, x);
+                        if (lane == j) mine = s;
+                    }
+                    rows.fin(my_valid, pre, mine);
+                } else {
+                    for (int j = 0; j < cnt; ++j) {
+                        const int64_t row = base + 8 * j;
+                        const double s = span_sum_warp<STREAM>(B.csc, B.doff[row], B.doff[row + 1], x);
+                        if (lane == j) mine = s;
+                    }
+                    rows.fin(my_valid, rows.pre(my_valid, my_row), mine);
+                }
+            }
+        } else {
+            // ---- thread rows: thread t takes rows t, t+256, ... (whole warps iterate together)
+            for (int64_t base = d.x; base < d.y; base += 256) {
+                const int64_t row = base + tid;
+                const bool valid = row < d.y;
+                if constexpr (PREFETCH) {
+                    const auto pre = rows.pre(valid, row);
+                    const double s = valid ? row_sum_thread<STREAM>(B.csc, B.doff[row], B.doff[row + 1], x) : 0.0;
+                    rows.fin(valid, pre, s);
+                } else {
+                    const double s = valid ? row_sum_thread<STREAM>(B.csc, B.doff[row], B.doff[row + 1], x) : 0.0;
+                    rows.fin(valid, rows.pre(valid, row), s);
+                }
+            }
+        }
+#if PR_DYNAMIC_UNITS
+#if PR_UNIT_RING
+        // two-slot ring: one barrier per unit
+        if (tid == 0) next_unit[ring] = (int64_t)gridDim.x + (int64_t)claim;
+        __syncthreads();
+        u = next_unit[ring];
+        ring ^= 1;
+#else
+        if (tid == 0) next_unit[0] = (int64_t)gridDim.x + (int64_t)claim;
+        __syncthreads();
+        u = next_unit[0];
+        __syncthreads();
+#endif
+#else
+        u += gridDim.x;
+#endif
+    }
+}
+
+// The same schedule with lambda callbacks and no prefetch (the streamed,
+// bandwidth-bound rounds and the power gather; this form measured ~3% faster
+// there than the functor form above with PREFETCH = false, same SASS mix).
 // thread_row(valid, row, sum): all 32 lanes of a warp (warp-collective safe)
 // single_row(row, sum): one thread
 template <bool STREAM, class ThreadRow, class SingleRow>
-__device__ __forceinline__ void bins_run(const BinView &B, const double *__restrict__ x, ThreadRow &thread_row,
+__device__ __forceinline__ void bins_run_plain(const BinView &B, const double *__restrict__ x, ThreadRow &thread_row,
                                          SingleRow &single_row) {
     __shared__ double red[8];
     __shared__ int64_t next_unit;

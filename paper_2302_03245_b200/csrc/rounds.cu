@@ -102,14 +102,37 @@ __device__ __forceinline__ void append_one(int items, int32_t v, long long *F, i
     for (int c = 0; c < items; ++c) F[base + c] = ((long long)v << 24) | c;
 }
 
+// Per-vertex drain inputs (loaded before the gathers by the pull rows).
+struct VtxIn {
+    int32_t v, dv, len, dt;
+    double h, rv;
+};
+
+__device__ __forceinline__ VtxIn load_vtx(const RunArgs &A, int32_t v) {
+    VtxIn q;
+    q.v = v;
+    q.dv = __ldg(&A.deg[v]);
+    q.len = __ldg(&A.row_len[v]);
+    q.dt = A.dtc ? __ldg(&A.dtc[v]) : 0;
+    q.h = A.h[v];
+    q.rv = A.reserved[v];
+    return q;
+}
+
+__device__ __forceinline__ int drain_loaded(const RunArgs &A, const VtxIn &q, double hv, int64_t r, Partial &p);
+
 // Drain one vertex of state r given its pre-drain pending mass hv:
 // statistics, reservation, shares s[r&1].  Returns its push-item count.
 __device__ __forceinline__ int drain_vertex(const RunArgs &A, int64_t v, double hv, int64_t r, Partial &p) {
     // every per-vertex load issued up front: one memory round trip per batch
-    const int32_t dv = __ldg(&A.deg[v]);
-    const int32_t len = __ldg(&A.row_len[v]);
-    const int32_t dt = A.dtc ? __ldg(&A.dtc[v]) : 0;
-    const double rv = A.reserved[v];
+    VtxIn q = load_vtx(A, (int32_t)v);
+    return drain_loaded(A, q, hv, r, p);
+}
+
+__device__ __forceinline__ int drain_loaded(const RunArgs &A, const VtxIn &q, double hv, int64_t r, Partial &p) {
+    const int64_t v = q.v;
+    const int32_t dv = q.dv, len = q.len, dt = q.dt;
+    const double rv = q.rv;
     const bool scan = A.algo == PR_ALGO_FPFULL || dv > 0;
     const bool above = hv > A.xi;  // strict (engines.py:421, _kernels.pyx:89)
     p.l1 += hv;
@@ -375,6 +398,37 @@ __device__ __forceinline__ void stamp_round_start(RunCtl *ctl) {
     if (threadIdx.x == 0 && atomicExch(&ctl->k_started, 1u) == 0u) ctl->t_k0 = globaltimer();
 }
 
+// Row callbacks of the dense round (bins.cuh): the drain inputs of a row are
+// loaded before its gathers, so the drain after the sum waits on no memory.
+struct PullRows {
+    const RunArgs &A;
+    int64_t r;
+    bool app;
+    long long *F;
+    int64_t *fsize;
+    Partial &p;
+    __device__ __forceinline__ VtxIn pre(bool valid, int64_t row) const {
+        VtxIn q;
+        if (valid) {
+            q = load_vtx(A, __ldg(&A.ids[row]));
+        } else {
+            q.v = 0;
+            q.dv = q.len = q.dt = 0;
+            q.h = q.rv = 0.0;
+        }
+        return q;
+    }
+    __device__ __forceinline__ void fin(bool valid, const VtxIn &q, double sum) {
+        const int items = valid ? drain_loaded(A, q, q.h + sum, r, p) : 0;
+        append_warp(app, items, q.v, F, fsize);
+    }
+    __device__ __forceinline__ void single(int64_t row, double sum) {
+        const int32_t v = __ldg(&A.ids[row]);
+        const int it = drain_vertex(A, v, A.h[v] + sum, r, p);
+        if (app) append_one(it, v, F, fsize);
+    }
+};
+
 // Unrolled loop bodies launch a kernel per slot; a slot whose round is not
 // of this kind (or after termination) exits at once.
 __device__ __forceinline__ bool round_is(const RunArgs &A, int mode) {
@@ -382,8 +436,8 @@ __device__ __forceinline__ bool round_is(const RunArgs &A, int mode) {
     return !c->done && c->mode == mode;
 }
 
-template <bool STREAM>
-__global__ void __launch_bounds__(256, PULL_MIN_BLOCKS) k_pull(RunArgs A) {
+template <bool STREAM, bool PREFETCH>
+__global__ void __launch_bounds__(256, PREFETCH ? PULL_MIN_BLOCKS - 1 : PULL_MIN_BLOCKS) k_pull(RunArgs A) {
     if (A.use_graph && !round_is(A, 0)) return;
     stamp_round_start(A.ctl);
     const int64_t t = A.ctl->round;
@@ -394,21 +448,26 @@ __global__ void __launch_bounds__(256, PULL_MIN_BLOCKS) k_pull(RunArgs A) {
     int64_t *fsize = &A.ctl->fsize[r & 1];
     Partial p;
     zero(p);
-    auto thread_row = [&](bool valid, int64_t row, double sum) {
-        int items = 0;
-        int32_t v = 0;
-        if (valid) {
-            v = __ldg(&A.ids[row]);
-            items = drain_vertex(A, v, A.h[v] + sum, r, p);
-        }
-        append_warp(app, items, v, F, fsize);
-    };
-    auto single_row = [&](int64_t row, double sum) {
-        int32_t v = __ldg(&A.ids[row]);
-        int it = drain_vertex(A, v, A.h[v] + sum, r, p);
-        if (app) append_one(it, v, F, fsize);
-    };
-    bins_run<STREAM>(A.T, s_in, thread_row, single_row);
+    if constexpr (PREFETCH) {
+        PullRows rows{A, r, app, F, fsize, p};
+        bins_run<STREAM, true>(A.T, s_in, rows);
+    } else {
+        auto thread_row = [&](bool valid, int64_t row, double sum) {
+            int items = 0;
+            int32_t v = 0;
+            if (valid) {
+                v = __ldg(&A.ids[row]);
+                items = drain_vertex(A, v, A.h[v] + sum, r, p);
+            }
+            append_warp(app, items, v, F, fsize);
+        };
+        auto single_row = [&](int64_t row, double sum) {
+            int32_t v = __ldg(&A.ids[row]);
+            int it = drain_vertex(A, v, A.h[v] + sum, r, p);
+            if (app) append_one(it, v, F, fsize);
+        };
+        bins_run_plain<STREAM>(A.T, s_in, thread_row, single_row);
+    }
     finish_round(A, p, r, true, false, p);
 }
 
@@ -734,7 +793,7 @@ struct Plan {
     RunArgs A;
     bool exact;
     unsigned g_all, g_red, g_total, g_pull, g_push, g_scan;
-    const void *k_pull_fn;   // k_pull<false> or k_pull<true> (streamed index loads)
+    const void *k_pull_fn;   // k_pull<STREAM, PREFETCH> chosen by the round's working set
 };
 
 static bool same_key(const pr_run_params &a, const pr_run_params &b) {
@@ -884,10 +943,21 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     phase_mark(ctx.stream, "run: ifp2 split/dtc");
     const int which = algo == PR_ALGO_IFP2 ? 1 : 0;
     // persistent pull grid: as many blocks as fit on the device at once,
-    int per_sm = 0;
-    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pull<false>, 256, 0));
-    if (per_sm < 1) per_sm = 1;
     PR_TRY(ensure_sched(g, which));
+    // A dense round touches the compacted CSC, the share vector of the
+    // sources and ~44 B of state per row.  When that overflows ~60% of L2 the
+    // round is bandwidth-bound: k_pull<true> streams the CSC (evict-first)
+    // at 4 blocks/SM.  Otherwise it is latency-bound: k_pull<false> issues
+    // each row's drain loads before its gathers, at 3 blocks/SM (the extra
+    // live registers).  Measured: C2 -9%, C4 -11%; C3 prefers the former.
+    const double ws = 4.0 * (double)g.sched[which].edges + 8.0 * (double)g.n + 44.0 * (double)g.sched[which].count;
+    const double l2 = (double)(ctx.l2_bytes ? ctx.l2_bytes : (size_t)126 << 20);
+    const bool stream = ws > 0.6 * l2, prefetch = ws < 1.2 * l2;
+    const void *k_pull_fn = stream ? (prefetch ? (const void *)k_pull<true, true> : (const void *)k_pull<true, false>)
+                                   : (prefetch ? (const void *)k_pull<false, true> : (const void *)k_pull<false, false>);
+    int per_sm = 0;
+    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pull_fn, 256, 0));
+    if (per_sm < 1) per_sm = 1;
     auto &S = g.sched[which];
     int64_t n = g.n;
     // persistent pull grid, ~UNITS_PER_BLOCK equal-cost units per block
@@ -958,14 +1028,7 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     P.exact = exact;
     P.g_all = grid_for(n, 256);
     P.g_pull = (unsigned)pull_blocks;
-    {
-        // a dense round touches the compacted CSC, the share vector of the
-        // sources and ~44 B of state per row; stream the CSC when that
-        // overflows ~60% of L2
-        const double ws = 4.0 * (double)S.edges + 8.0 * (double)n + 44.0 * (double)S.count;
-        const bool stream = ws > 0.6 * (double)(ctx.l2_bytes ? ctx.l2_bytes : (size_t)126 << 20);
-        P.k_pull_fn = stream ? (const void *)k_pull<true> : (const void *)k_pull<false>;
-    }
+    P.k_pull_fn = k_pull_fn;
     // reducing kernels of the fast engine: one resident wave, grid-stride
     // (a block's lifetime -- reduce, publish -- is latency, not bandwidth)
     auto wave = [&](const void *k) -> unsigned {
@@ -1039,8 +1102,8 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
                 }
                 k_ex_prep<<<P.g_all, 256, 0, st>>>(A);
             } else if (hc.mode == 0) {
-                if (P.k_pull_fn == (const void *)k_pull<true>) k_pull<true><<<P.g_pull, 256, 0, st>>>(A);
-                else k_pull<false><<<P.g_pull, 256, 0, st>>>(A);
+                void *kargs[] = {&A};
+                PR_CUDA(cudaLaunchKernel(P.k_pull_fn, dim3(P.g_pull), dim3(256), kargs, 0, st));
             } else {
                 k_push<<<P.g_push, 256, 0, st>>>(A);
                 k_scan<<<P.g_scan, 256, 0, st>>>(A);
