@@ -132,13 +132,31 @@ __global__ void ub_round(UbCtl *c, cudaGraphConditionalHandle h_loop, cudaGraphC
     if (mode == 2) cudaGraphSetConditional(h_sw, 0u);
 }
 
+// same, for programmatic (PDL) edges: trigger early, wait for the upstream grid
+__global__ void ub_round_pdl(UbCtl *c, cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_sw, int mode) {
+    cudaTriggerProgrammaticLaunchCompletion();
+    cudaGridDependencySynchronize();
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&c->arrive, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    c->arrive = 0;
+    if (c->left > 0) c->left -= 1;
+    __threadfence();
+    cudaGraphSetConditional(h_loop, c->left > 0 ? 1u : 0u);
+}
+
 __global__ void ub_init(UbCtl *c, int64_t iters) {
     c->left = iters;
     c->arrive = 0;
 }
 
 // variant 0: stream launches; 1: WHILE{round}; 2: WHILE{SWITCH{round}};
-// 3: WHILE{round x4}; 4: WHILE{round x8}; 5: WHILE{cooperative round}
+// 3: WHILE{round x4}; 4: WHILE{round x8}; 5: WHILE{cooperative round};
+// 6: WHILE{round x8, programmatic edges}; 7: same with launch-completion port
 int debug_graph(Ctx &ctx, int variant, int64_t iters, int blocks, double *us_out) {
     cudaStream_t st = ctx.stream;
     DevBuf cb;
@@ -181,13 +199,28 @@ int debug_graph(Ctx &ctx, int variant, int64_t iters, int blocks, double *us_out
         }
         int mode = variant == 2 ? 2 : 1;
         void *a_r[] = {&c, &hl, &hs, &mode};
-        kp.func = (void *)ub_round;
+        kp.func = variant >= 6 ? (void *)ub_round_pdl : (void *)ub_round;
         kp.gridDim = dim3((unsigned)blocks);
         kp.blockDim = dim3(256);
         kp.kernelParams = a_r;
-        const int copies = variant == 3 ? 4 : variant == 4 ? 8 : 1;
+        const int copies = variant == 3 ? 4 : (variant == 4 || variant >= 6) ? 8 : 1;
         cudaGraphNode_t prev = nullptr;
         for (int k = 0; k < copies; ++k) {
+            if (variant >= 6 && prev) {
+                cudaGraphNodeParams np = {};
+                np.type = cudaGraphNodeTypeKernel;
+                np.kernel.func = kp.func;
+                np.kernel.gridDim = kp.gridDim;
+                np.kernel.blockDim = kp.blockDim;
+                np.kernel.sharedMemBytes = 0;
+                np.kernel.kernelParams = kp.kernelParams;
+                cudaGraphEdgeData ed = {};
+                ed.from_port = variant == 6 ? cudaGraphKernelNodePortProgrammatic : cudaGraphKernelNodePortLaunchCompletion;
+                ed.type = cudaGraphDependencyTypeProgrammatic;
+                PR_CUDA(cudaGraphAddNode_v2(&n_k, body, &prev, &ed, 1, &np));
+                prev = n_k;
+                continue;
+            }
             PR_CUDA(cudaGraphAddKernelNode(&n_k, body, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
             if (variant == 5) {
                 cudaKernelNodeAttrValue v = {};

@@ -9,9 +9,9 @@ L = _lib.load()
 L.pr_debug_graph.restype = ctypes.c_int
 L.pr_debug_graph.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
 ctx = _lib.context()
-names = {0: "stream launches", 1: "WHILE{kernel}", 2: "WHILE{SWITCH{kernel}}", 3: "WHILE{kernel x4}", 4: "WHILE{kernel x8}", 5: "WHILE{coop kernel}"}
+names = {0: "stream launches", 1: "WHILE{kernel}", 2: "WHILE{SWITCH{kernel}}", 3: "WHILE{kernel x4}", 4: "WHILE{kernel x8}", 5: "WHILE{coop kernel}", 6: "WHILE{k x8 PDL prog}", 7: "WHILE{k x8 PDL launch}"}
 for blocks in (148, 592):
-    for v in (0, 1, 2, 3, 4, 5):
+    for v in (0, 1, 2, 3, 4, 5, 6, 7):
         us = ctypes.c_double()
         rc = L.pr_debug_graph(ctx.handle, v, 2000, blocks, ctypes.byref(us))
         if rc:
