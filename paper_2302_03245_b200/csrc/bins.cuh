@@ -30,6 +30,29 @@ __device__ __forceinline__ int ld_idx(const int32_t *p) {
 }
 __device__ __forceinline__ double ld_share(const double *p) { return __ldg(p); }
 
+// Share sources of a dense round (rounds.cu, Gauss-Seidel sections):
+//   Jacobi      gs_lo = tr_lo = 0:      x[u]
+//   GS sweep    gs_lo = section start:  u < gs_lo ? x_new[u] : x[u]
+//   transition  tr_lo = gs_lo:          x[u] + (u < gs_lo ? x_new[u] : 0)
+// x holds the shares still owed to this row, x_new the shares drained
+// earlier in the same sweep (sources of earlier sections).
+struct Src {
+    const double *x, *x_new;
+    int gs_lo, tr_lo;
+};
+
+// SRC: 0 Jacobi only (plain x), 1 section sweep (select), 2 transition
+template <int SRC>
+__device__ __forceinline__ double ld_src(const Src S, int idx) {
+    if constexpr (SRC == 0) {
+        return ld_share(S.x + idx);
+    } else if constexpr (SRC == 1) {
+        return ld_share((idx < S.gs_lo ? S.x_new : S.x) + idx);
+    } else {
+        return ld_share(S.x + idx) + (idx < S.gs_lo ? ld_share(S.x_new + idx) : 0.0);
+    }
+}
+
 struct BinView {
     const int32_t *ids;      // row -> vertex id
     const int64_t *doff;     // row offsets in csc
@@ -43,9 +66,9 @@ struct BinView {
     unsigned long long *unit_ctr;  // dynamic dispatch counter (0 at kernel start)
 };
 
-template <bool STREAM>
+template <bool STREAM, int SRC>
 __device__ __forceinline__ double row_sum_thread(const int32_t *__restrict__ csc, int64_t lo, int64_t hi,
-                                                 const double *__restrict__ x) {
+                                                 const Src x) {
     double acc = 0.0;
     for (int64_t e = lo; e < hi; e += 8) {
         int idx[8];
@@ -53,7 +76,7 @@ __device__ __forceinline__ double row_sum_thread(const int32_t *__restrict__ csc
         for (int q = 0; q < 8; ++q) idx[q] = e + q < hi ? ld_idx<STREAM>(&csc[e + q]) : -1;
         double t[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) t[q] = idx[q] >= 0 ? ld_share(&x[idx[q]]) : 0.0;
+        for (int q = 0; q < 8; ++q) t[q] = idx[q] >= 0 ? ld_src<SRC>(x, idx[q]) : 0.0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc += t[q];
     }
@@ -61,9 +84,9 @@ __device__ __forceinline__ double row_sum_thread(const int32_t *__restrict__ csc
 }
 
 // lanes stride [lo, hi) with 8 gathers in flight; warp-reduced (fixed tree)
-template <bool STREAM>
+template <bool STREAM, int SRC>
 __device__ __forceinline__ double span_sum_warp(const int32_t *__restrict__ csc, int64_t lo, int64_t hi,
-                                                const double *__restrict__ x) {
+                                                const Src x) {
     const int lane = threadIdx.x & 31;
     double acc = 0.0;
     for (int64_t e = lo + lane; e < hi; e += 256) {
@@ -72,7 +95,7 @@ __device__ __forceinline__ double span_sum_warp(const int32_t *__restrict__ csc,
         for (int q = 0; q < 8; ++q) idx[q] = e + 32 * q < hi ? ld_idx<STREAM>(&csc[e + 32 * q]) : -1;
         double t[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) t[q] = idx[q] >= 0 ? ld_share(&x[idx[q]]) : 0.0;
+        for (int q = 0; q < 8; ++q) t[q] = idx[q] >= 0 ? ld_src<SRC>(x, idx[q]) : 0.0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc += t[q];
     }
@@ -92,8 +115,9 @@ __device__ __forceinline__ double span_sum_warp(const int32_t *__restrict__ csc,
 //   void single(int64_t row, double sum)           one thread (hub rows)
 // PREFETCH: load a row's bounds and drain inputs before its gathers (more
 // live registers; pays when the round is latency-bound, i.e. L2-resident)
-template <bool STREAM, bool PREFETCH, class R>
-__device__ __forceinline__ void bins_run(const BinView &B, const double *__restrict__ x, R &rows) {
+template <bool STREAM, bool PREFETCH, int SRC, class R>
+__device__ __forceinline__ void bins_run(const BinView &B, const int64_t u_lo, const int64_t u_hi, const Src x,
+                                         R &rows) {
     __shared__ double red[8];
     __shared__ int64_t next_unit[2];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -101,7 +125,7 @@ __device__ __forceinline__ void bins_run(const BinView &B, const double *__restr
     // dynamic unit dispatch: first unit = blockIdx.x, then one atomic per unit
     // (units are ordered heaviest first); the round finaliser resets the counter
     int ring = 0;
-    for (int64_t u = blockIdx.x; u < B.n_units;) {
+    for (int64_t u = u_lo + blockIdx.x; u < u_hi;) {
 #if PR_DYNAMIC_UNITS
         // claim the following unit now; the atomic's latency hides behind this unit
         unsigned long long claim = 0;
@@ -122,7 +146,7 @@ __device__ __forceinline__ void bins_run(const BinView &B, const double *__restr
             }
             double acc = 0.0;
 #pragma unroll
-            for (int q = 0; q < HUB_CHUNK / 256; ++q) acc += idx[q] >= 0 ? ld_share(&x[idx[q]]) : 0.0;
+            for (int q = 0; q < HUB_CHUNK / 256; ++q) acc += idx[q] >= 0 ? ld_src<SRC>(x, idx[q]) : 0.0;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             __syncthreads();
@@ -132,7 +156,7 @@ __device__ __forceinline__ void bins_run(const BinView &B, const double *__restr
                 double s = 0.0;
                 for (int k = 0; k < 8; ++k) s += red[k];
                 const int nch = (int)((re - rb + HUB_CHUNK - 1) / HUB_CHUNK);
-                B.chunk_part[u] = s;
+                B.chunk_part[B.chunk_base[r] + c] = s;
                 __threadfence();
                 if (atomicAdd(&B.row_cnt[r], 1) == nch - 1) {
                     __threadfence();
@@ -162,14 +186,14 @@ __device__ __forceinline__ void bins_run(const BinView &B, const double *__restr
                     for (int j = 0; j < cnt; ++j) {
                         const int64_t lo = __shfl_sync(0xffffffffu, my_lo, j),
                                       hi = __shfl_sync(0xffffffffu, my_hi, j);
-                        const double s = span_sum_warp<STREAM>(B.csc, lo, hi, x);
+                        const double s = span_sum_warp<STREAM, SRC>(B.csc, lo, hi, x);
                         if (lane == j) mine = s;
                     }
                     rows.fin(my_valid, pre, mine);
                 } else {
                     for (int j = 0; j < cnt; ++j) {
                         const int64_t row = base + 8 * j;
-                        const double s = span_sum_warp<STREAM>(B.csc, B.doff[row], B.doff[row + 1], x);
+                        const double s = span_sum_warp<STREAM, SRC>(B.csc, B.doff[row], B.doff[row + 1], x);
                         if (lane == j) mine = s;
                     }
                     rows.fin(my_valid, rows.pre(my_valid, my_row), mine);
@@ -182,10 +206,10 @@ __device__ __forceinline__ void bins_run(const BinView &B, const double *__restr
                 const bool valid = row < d.y;
                 if constexpr (PREFETCH) {
                     const auto pre = rows.pre(valid, row);
-                    const double s = valid ? row_sum_thread<STREAM>(B.csc, B.doff[row], B.doff[row + 1], x) : 0.0;
+                    const double s = valid ? row_sum_thread<STREAM, SRC>(B.csc, B.doff[row], B.doff[row + 1], x) : 0.0;
                     rows.fin(valid, pre, s);
                 } else {
-                    const double s = valid ? row_sum_thread<STREAM>(B.csc, B.doff[row], B.doff[row + 1], x) : 0.0;
+                    const double s = valid ? row_sum_thread<STREAM, SRC>(B.csc, B.doff[row], B.doff[row + 1], x) : 0.0;
                     rows.fin(valid, rows.pre(valid, row), s);
                 }
             }
@@ -193,7 +217,7 @@ __device__ __forceinline__ void bins_run(const BinView &B, const double *__restr
 #if PR_DYNAMIC_UNITS
 #if PR_UNIT_RING
         // two-slot ring: one barrier per unit
-        if (tid == 0) next_unit[ring] = (int64_t)gridDim.x + (int64_t)claim;
+        if (tid == 0) next_unit[ring] = u_lo + (int64_t)gridDim.x + (int64_t)claim;
         __syncthreads();
         u = next_unit[ring];
         ring ^= 1;
@@ -214,16 +238,16 @@ __device__ __forceinline__ void bins_run(const BinView &B, const double *__restr
 // there than the functor form above with PREFETCH = false, same SASS mix).
 // thread_row(valid, row, sum): all 32 lanes of a warp (warp-collective safe)
 // single_row(row, sum): one thread
-template <bool STREAM, class ThreadRow, class SingleRow>
-__device__ __forceinline__ void bins_run_plain(const BinView &B, const double *__restrict__ x, ThreadRow &thread_row,
-                                         SingleRow &single_row) {
+template <bool STREAM, int SRC, class ThreadRow, class SingleRow>
+__device__ __forceinline__ void bins_run_plain(const BinView &B, const int64_t u_lo, const int64_t u_hi, const Src x,
+                                               ThreadRow &thread_row, SingleRow &single_row) {
     __shared__ double red[8];
     __shared__ int64_t next_unit;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int64_t warp_rows = B.n_hub + B.n_warp;
     // dynamic unit dispatch: first unit = blockIdx.x, then one atomic per unit
     // (units are ordered heaviest first); the round finaliser resets the counter
-    for (int64_t u = blockIdx.x; u < B.n_units;) {
+    for (int64_t u = u_lo + blockIdx.x; u < u_hi;) {
 #if PR_DYNAMIC_UNITS
         // claim the following unit now; the atomic's latency hides behind this unit
         unsigned long long claim = 0;
@@ -244,7 +268,7 @@ __device__ __forceinline__ void bins_run_plain(const BinView &B, const double *_
             }
             double acc = 0.0;
 #pragma unroll
-            for (int q = 0; q < HUB_CHUNK / 256; ++q) acc += idx[q] >= 0 ? ld_share(&x[idx[q]]) : 0.0;
+            for (int q = 0; q < HUB_CHUNK / 256; ++q) acc += idx[q] >= 0 ? ld_src<SRC>(x, idx[q]) : 0.0;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             __syncthreads();
@@ -254,7 +278,7 @@ __device__ __forceinline__ void bins_run_plain(const BinView &B, const double *_
                 double s = 0.0;
                 for (int k = 0; k < 8; ++k) s += red[k];
                 const int nch = (int)((re - rb + HUB_CHUNK - 1) / HUB_CHUNK);
-                B.chunk_part[u] = s;
+                B.chunk_part[B.chunk_base[r] + c] = s;
                 __threadfence();
                 if (atomicAdd(&B.row_cnt[r], 1) == nch - 1) {
                     __threadfence();
@@ -273,7 +297,7 @@ __device__ __forceinline__ void bins_run_plain(const BinView &B, const double *_
                 for (int j = 0; j < 32; ++j) {
                     const int64_t row = base + 8 * j;
                     if (row >= d.y) break;
-                    const double s = span_sum_warp<STREAM>(B.csc, B.doff[row], B.doff[row + 1], x);
+                    const double s = span_sum_warp<STREAM, SRC>(B.csc, B.doff[row], B.doff[row + 1], x);
                     if (lane == j) mine = s;
                 }
                 const int64_t row = base + 8 * lane;
@@ -284,12 +308,12 @@ __device__ __forceinline__ void bins_run_plain(const BinView &B, const double *_
             for (int64_t base = d.x; base < d.y; base += 256) {
                 const int64_t row = base + tid;
                 const bool valid = row < d.y;
-                const double s = valid ? row_sum_thread<STREAM>(B.csc, B.doff[row], B.doff[row + 1], x) : 0.0;
+                const double s = valid ? row_sum_thread<STREAM, SRC>(B.csc, B.doff[row], B.doff[row + 1], x) : 0.0;
                 thread_row(valid, row, s);
             }
         }
 #if PR_DYNAMIC_UNITS
-        if (tid == 0) next_unit = (int64_t)gridDim.x + (int64_t)claim;
+        if (tid == 0) next_unit = u_lo + (int64_t)gridDim.x + (int64_t)claim;
         __syncthreads();
         u = next_unit;
         __syncthreads();

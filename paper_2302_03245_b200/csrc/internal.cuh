@@ -11,6 +11,9 @@
 
 namespace pr {
 
+// Gauss-Seidel sections of a dense sweep (rounds.cu): at most this many
+#define PR_MAX_SECTIONS 8
+
 // ---------------------------------------------------------------- errors
 void set_error(const std::string &msg);
 int fail(int code, const std::string &msg);
@@ -62,6 +65,13 @@ struct Ctx {
     DevBuf flush;            // L2 flush buffer (bench)
 };
 
+// Per-block partial statistics of one round (reduced in fixed order).
+struct Partial {
+    double l1, above, nd_above;
+    int64_t conv_all, conv_scan, nact, work, push_ops, push_dang;
+    uint64_t digest;
+};
+
 // Device-side control block of a round loop (one per run workspace).
 struct RunCtl {
     int64_t round;            // index t of the state being drained next
@@ -88,14 +98,13 @@ struct RunCtl {
     uint64_t t_k0;
     double next_bytes;        // algorithmic bytes of that round
     double pull_ns, pull_bytes, sparse_ns;
+    // Gauss-Seidel sections (rounds.cu): statistics of the sections of the
+    // current sweep, and the kind of the next round
+    Partial sec_acc;
+    int32_t gs;               // next pull round is a Gauss-Seidel sweep
+    int32_t push_filter;      // next push round follows a GS sweep
 };
 
-// Per-block partial statistics of one round (reduced in fixed order).
-struct Partial {
-    double l1, above, nd_above;
-    int64_t conv_all, conv_scan, nact, work, push_ops, push_dang;
-    uint64_t digest;
-};
 
 struct Graph {
     Ctx *ctx = nullptr;
@@ -141,6 +150,9 @@ struct Graph {
         DevBuf chunk_base;        // int64 [n_hub+1] first chunk of each hub row
         DevBuf row_cum;           // int64 [|D|+1] exclusive prefix of row costs (edges + ROW_COST)
         int64_t unit_blocks = 0;  // grid size the units below were cut for
+        int nsec = 0;             // Gauss-Seidel sections the units were cut for
+        int64_t sec_row[PR_MAX_SECTIONS + 1] = {};   // section row bounds (equal edges)
+        int64_t sec_unit[PR_MAX_SECTIONS + 1] = {};  // section unit bounds
         int64_t n_units = 0;
         DevBuf units;             // int2 [n_units]: (row_begin, row_end) or hub chunk (row, -(chunk+1))
         DevBuf row_cnt;           // int32 [n_hub] chunk arrival counters
@@ -184,7 +196,7 @@ int count_dangling(Graph &g);
 int ensure_run_layout(Graph &g);
 void invalidate_cache(Graph &g);
 int ensure_sched(Graph &g, int which);
-int ensure_units(Graph &g, int which, int64_t blocks);
+int ensure_units(Graph &g, int which, int64_t blocks, int nsec = 1);
 int build_from_device_edges(Ctx &ctx, int64_t n, const int64_t *d_src, const int64_t *d_dst,
                             int64_t m_raw, Graph **out);
 int classify_device(Graph &g);

@@ -115,7 +115,8 @@ __global__ void __launch_bounds__(256, 4) k_pw_gather(PowArgs A) {
         if (valid) finish(__ldg(&A.T.ids[row]), sum);
     };
     auto single_row = [&](int64_t row, double sum) { finish(__ldg(&A.T.ids[row]), sum); };
-    bins_run_plain<STREAM>(A.T, A.z, thread_row, single_row);
+    const Src src{A.z, A.z, 0, 0};
+    bins_run_plain<STREAM, 0>(A.T, 0, A.T.n_units, src, thread_row, single_row);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.n_zero;
          i += (int64_t)gridDim.x * blockDim.x)
         finish(A.zero_ids[i], 0.0);

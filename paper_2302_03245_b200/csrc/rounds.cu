@@ -27,6 +27,8 @@
 #include <cooperative_groups.h>
 #include <cooperative_groups/scan.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -68,6 +70,11 @@ struct RunArgs {
     double push_work;          // AUTO: push when the next round's work < push_work
     double n_scan;             // scan-set size (bytes model)
     cudaGraphConditionalHandle h_loop, h_pull, h_push;
+    // Gauss-Seidel sections of a dense sweep (ids == rows: the IFP2 run
+    // layout); this launch processes section `sec` of `nsec`
+    int32_t sec, nsec;
+    int64_t sec_row[PR_MAX_SECTIONS + 1];
+    int64_t sec_unit[PR_MAX_SECTIONS + 1];
 };
 
 __device__ __forceinline__ uint64_t digest_term(int64_t v, double r, double h) {
@@ -217,6 +224,16 @@ __device__ void finalize_row(const RunArgs &A, const Partial &tot, int64_t r, bo
         if (A.policy == PR_MODE_PUSH) mode = 1;
         else if (A.policy == PR_MODE_AUTO && (double)tot.work < A.push_work) mode = 1;
     }
+    // Gauss-Seidel state of the next round: after a dense sweep the next one
+    // is a transition sweep (owed shares to every target + new shares of
+    // earlier sections), then GS sweeps; a push round after a GS sweep only
+    // delivers to targets in the source's section or earlier
+    {
+        const bool was_pull = fast && r >= 1 && ctl->next_mode == 0;
+        const int32_t was_gs = ctl->gs;
+        ctl->push_filter = A.nsec > 1 && mode == 1 && was_pull && was_gs != 0;
+        ctl->gs = (A.nsec > 1 && mode == 0 && was_pull) ? 2 - (was_gs == 0 ? 1 : 0) : 0;
+    }
     ctl->mode = mode;
     ctl->next_mode = mode;
     if (!done) {
@@ -241,8 +258,11 @@ __device__ void finalize_row(const RunArgs &A, const Partial &tot, int64_t r, bo
 // Publish this block's partial; the last block to arrive reduces all of
 // them in a fixed order (deterministic) and finalises row r.
 // `p` (and `cst`) must already be the block totals in thread 0.
+// sec_kind: 0 a whole round; 1 a Gauss-Seidel section before the last (its
+// totals are added to ctl->sec_acc, section order); 2 the last section (adds
+// the accumulated sections and finalises the row).
 __device__ void publish_round(const RunArgs &A, const Partial &p, int64_t r, bool fast, bool with_consts,
-                              const Partial &cst) {
+                              const Partial &cst, int sec_kind = 0) {
     __shared__ bool is_last;
     if (threadIdx.x == 0) {
         A.partials[blockIdx.x] = p;
@@ -271,14 +291,29 @@ __device__ void publish_round(const RunArgs &A, const Partial &p, int64_t r, boo
             A.ctl->c_conv_all = cacc.conv_all;
             A.ctl->c_conv_scan = cacc.conv_scan;
         }
+        if (sec_kind == 1) {
+            RunCtl *c = A.ctl;
+            if (A.sec == 0) c->sec_acc = acc;
+            else add(c->sec_acc, acc);
+            c->unit_ctr = 0;
+            c->blocks_done = 0;
+            __threadfence();
+            return;
+        }
+        if (sec_kind == 2) {
+            Partial tot = A.ctl->sec_acc;
+            add(tot, acc);
+            acc = tot;
+        }
         finalize_row(A, acc, r, fast);
     }
 }
 
-__device__ void finish_round(const RunArgs &A, Partial p, int64_t r, bool fast, bool with_consts, Partial cst) {
+__device__ void finish_round(const RunArgs &A, Partial p, int64_t r, bool fast, bool with_consts, Partial cst,
+                             int sec_kind = 0) {
     block_reduce(p);
     if (with_consts) block_reduce(cst);
-    publish_round(A, p, r, fast, with_consts, cst);
+    publish_round(A, p, r, fast, with_consts, cst, sec_kind);
 }
 
 // warp-sum a batch partial and fold it into this warp's shared accumulator
@@ -312,6 +347,8 @@ __global__ void k_reset(RunArgs A) {
     c->t_k0 = 0;
     c->next_bytes = 0.0;
     c->pull_ns = c->pull_bytes = c->sparse_ns = 0.0;
+    c->gs = 0;
+    c->push_filter = 0;
 }
 
 // State 0 (h = 1 everywhere, MassState.fresh engines.py:51-54): trace row 0
@@ -436,7 +473,8 @@ __device__ __forceinline__ bool round_is(const RunArgs &A, int mode) {
     return !c->done && c->mode == mode;
 }
 
-template <bool STREAM, bool PREFETCH>
+// GS: the launch is one Gauss-Seidel section of a sweep
+template <bool STREAM, bool PREFETCH, bool GS>
 __global__ void __launch_bounds__(256, PREFETCH ? PULL_MIN_BLOCKS - 1 : PULL_MIN_BLOCKS) k_pull(RunArgs A) {
     if (A.use_graph && !round_is(A, 0)) return;
     stamp_round_start(A.ctl);
@@ -446,11 +484,21 @@ __global__ void __launch_bounds__(256, PREFETCH ? PULL_MIN_BLOCKS - 1 : PULL_MIN
     const bool app = A.ctl->append != 0;
     long long *F = A.frontier + (r & 1) * A.fcap;
     int64_t *fsize = &A.ctl->fsize[r & 1];
+    // this launch's section and the sweep kind (Src in bins.cuh)
+    const int64_t u_lo = A.sec_unit[A.sec], u_hi = A.sec_unit[A.sec + 1];
+    Src src{s_in, A.s + (r & 1) * A.n, 0, 0};
+    int32_t gs = 0;
+    if constexpr (GS) {
+        gs = A.ctl->gs;
+        if (gs) src.gs_lo = (int)A.sec_row[A.sec];
+    }
     Partial p;
     zero(p);
     if constexpr (PREFETCH) {
         PullRows rows{A, r, app, F, fsize, p};
-        bins_run<STREAM, true>(A.T, s_in, rows);
+        if constexpr (!GS) bins_run<STREAM, true, 0>(A.T, u_lo, u_hi, src, rows);
+        else if (gs == 1) bins_run<STREAM, true, 2>(A.T, u_lo, u_hi, src, rows);
+        else bins_run<STREAM, true, 1>(A.T, u_lo, u_hi, src, rows);
     } else {
         auto thread_row = [&](bool valid, int64_t row, double sum) {
             int items = 0;
@@ -466,9 +514,11 @@ __global__ void __launch_bounds__(256, PREFETCH ? PULL_MIN_BLOCKS - 1 : PULL_MIN
             int it = drain_vertex(A, v, A.h[v] + sum, r, p);
             if (app) append_one(it, v, F, fsize);
         };
-        bins_run_plain<STREAM>(A.T, s_in, thread_row, single_row);
+        if constexpr (!GS) bins_run_plain<STREAM, 0>(A.T, u_lo, u_hi, src, thread_row, single_row);
+        else if (gs == 1) bins_run_plain<STREAM, 2>(A.T, u_lo, u_hi, src, thread_row, single_row);
+        else bins_run_plain<STREAM, 1>(A.T, u_lo, u_hi, src, thread_row, single_row);
     }
-    finish_round(A, p, r, true, false, p);
+    finish_round(A, p, r, true, false, p, A.nsec > 1 ? (A.sec + 1 < A.nsec ? 1 : 2) : 0);
 }
 
 // Sparse round t, step 1: scatter the frontier's shares (red.global.add.f64);
@@ -481,6 +531,7 @@ __global__ void __launch_bounds__(256) k_push(RunArgs A) {
     const double *__restrict__ s_in = A.s + (t & 1) * A.n;
     const long long *F = A.frontier + (t & 1) * A.fcap;
     int64_t cnt = A.ctl->fsize[t & 1];
+    const bool filter = A.ctl->push_filter != 0;
     int lane = threadIdx.x & 31;
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -491,6 +542,15 @@ __global__ void __launch_bounds__(256) k_push(RunArgs A) {
         double sh = s_in[u];
         int64_t lo = A.push_off[u] + c * TILE, hi = A.push_off[u + 1];
         if (hi > lo + TILE) hi = lo + TILE;
+        // after a Gauss-Seidel sweep, targets in later sections than u have
+        // already taken u's share during the sweep
+        int32_t t_hi = 0x7fffffff;
+        if (filter)
+            for (int k = 1; k <= A.nsec; ++k)
+                if (u < A.sec_row[k]) {
+                    t_hi = (int32_t)A.sec_row[k];
+                    break;
+                }
         int32_t tg[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -499,7 +559,7 @@ __global__ void __launch_bounds__(256) k_push(RunArgs A) {
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            if (tg[k] >= 0) atomicAdd(&A.h[tg[k]], sh);
+            if (tg[k] >= 0 && tg[k] < t_hi) atomicAdd(&A.h[tg[k]], sh);
     }
 }
 
@@ -642,7 +702,7 @@ __global__ void k_settle_fast(RunArgs A, const double *__restrict__ w, const int
     if (thread_mode) {
         for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd;
              i += (int64_t)gridDim.x * blockDim.x) {
-            const double acc = row_sum_thread<false>(src_ids, src_off[i], src_off[i + 1], w);
+            const double acc = row_sum_thread<false, 0>(src_ids, src_off[i], src_off[i + 1], Src{w, w, 0, 0});
             const int32_t d = dang_ids[i];
             A.reserved[d] = A.h[d] + acc;
             A.h[d] = 0.0;
@@ -653,7 +713,7 @@ __global__ void k_settle_fast(RunArgs A, const double *__restrict__ w, const int
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t i = lo + warp; i < nd; i += nwarps) {
-        const double acc = span_sum_warp<false>(src_ids, src_off[i], src_off[i + 1], w);
+        const double acc = span_sum_warp<false, 0>(src_ids, src_off[i], src_off[i + 1], Src{w, w, 0, 0});
         if (lane == 0) {
             const int32_t d = dang_ids[i];
             A.reserved[d] = A.h[d] + acc;
@@ -867,11 +927,16 @@ static int build_graph(Plan &P, cudaGraph_t *out_g, cudaGraphExec_t *out_exec) {
         PR_TRY(add_while(body, &w_pull, nullptr, A.h_pull, &b_pull));
         PR_TRY(add_while(body, &w_push, &w_pull, A.h_push, &b_push));
         cudaGraphNode_t prev = nullptr;
-        for (int k = 0; k < PULL_UNROLL; ++k) {
-            PR_TRY(add_kernel(b_pull, &n_a, prev ? &prev : nullptr, prev ? 1 : 0, (void *)P.k_pull_fn, P.g_pull, 256,
-                              args));
-            prev = n_a;
-        }
+        // a slot is one dense sweep: its sections in order
+        const int sweeps = A.nsec > 1 ? (PULL_UNROLL / A.nsec > 2 ? PULL_UNROLL / A.nsec : 2) : PULL_UNROLL;
+        for (int k = 0; k < sweeps; ++k)
+            for (int sec = 0; sec < A.nsec; ++sec) {
+                A.sec = sec;  // the node copies its arguments here
+                PR_TRY(add_kernel(b_pull, &n_a, prev ? &prev : nullptr, prev ? 1 : 0, (void *)P.k_pull_fn, P.g_pull,
+                                  256, args));
+                prev = n_a;
+            }
+        A.sec = 0;
         prev = nullptr;
         for (int k = 0; k < PUSH_UNROLL; ++k) {
             PR_TRY(add_kernel(b_push, &n_a, prev ? &prev : nullptr, prev ? 1 : 0, (void *)k_push, P.g_push, 256, args));
@@ -953,8 +1018,10 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     const double ws = 4.0 * (double)g.sched[which].edges + 8.0 * (double)g.n + 44.0 * (double)g.sched[which].count;
     const double l2 = (double)(ctx.l2_bytes ? ctx.l2_bytes : (size_t)126 << 20);
     const bool stream = ws > 0.6 * l2, prefetch = ws < 1.2 * l2;
-    const void *k_pull_fn = stream ? (prefetch ? (const void *)k_pull<true, true> : (const void *)k_pull<true, false>)
-                                   : (prefetch ? (const void *)k_pull<false, true> : (const void *)k_pull<false, false>);
+    const void *k_pull_fn = stream ? (prefetch ? (const void *)k_pull<true, true, false>
+                                               : (const void *)k_pull<true, false, false>)
+                                   : (prefetch ? (const void *)k_pull<false, true, false>
+                                               : (const void *)k_pull<false, false, false>);
     int per_sm = 0;
     PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pull_fn, 256, 0));
     if (per_sm < 1) per_sm = 1;
@@ -962,8 +1029,32 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     int64_t n = g.n;
     // persistent pull grid, ~UNITS_PER_BLOCK equal-cost units per block
     const int64_t pull_blocks = (int64_t)ctx.sm_count * per_sm;
-    PR_TRY(ensure_units(g, which, pull_blocks));
+    // Gauss-Seidel sections need vertex id == row (the IFP2 run layout's
+    // prefix schedule); PUSHRANK_GS_SECTIONS overrides the default
+    // Sections cut rounds (C2: 174 -> 98 at 4 sections) but each adds a
+    // launch, a ramp and a reduction to the sweep, so they pay only when a
+    // round is long: 2 sections past 1.5x L2 of round working set (C3: 14.8 ->
+    // 11.5 ms), 4 past 16x (C5: 813 -> 598 ms), none below (C2, C4).
+    int nsec = 1;
+    if (algo == PR_ALGO_IFP2 && g.class0_end >= 0) {
+        nsec = ws > 16.0 * l2 ? 4 : ws > 1.5 * l2 ? 2 : 1;
+        if (const char *e = getenv("PUSHRANK_GS_SECTIONS")) nsec = atoi(e);
+        if (nsec < 1) nsec = 1;
+        if (nsec > PR_MAX_SECTIONS) nsec = PR_MAX_SECTIONS;
+    }
+    if (nsec > 1)
+        k_pull_fn = stream ? (prefetch ? (const void *)k_pull<true, true, true> : (const void *)k_pull<true, false, true>)
+                           : (prefetch ? (const void *)k_pull<false, true, true> : (const void *)k_pull<false, false, true>);
+    {
+        const void *before = g.sched[which].units.ptr;
+        const int64_t before_n = g.sched[which].n_units;
+        PR_TRY(ensure_units(g, which, pull_blocks, nsec));
+        if (g.sched[which].units.ptr != before || g.sched[which].n_units != before_n) invalidate_cache(g);
+    }
     const int64_t fcap = n + g.m / TILE + 1;
+    if (getenv("PUSHRANK_TIMING"))
+        fprintf(stderr, "[pushrank] round working set %.1f MB (L2 %.1f MB): stream %d prefetch %d sections %d\n",
+                ws / 1e6, l2 / 1e6, (int)stream, (int)prefetch, nsec);
     phase_mark(ctx.stream, "run: schedule");
     PR_TRY(ws_alloc(g, pull_blocks, fcap));
     phase_mark(ctx.stream, "run: workspace");
@@ -998,6 +1089,12 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     A.T.chunk_part = S.chunk_part.as<double>();
     A.T.units = S.units.as<int2>();
     A.T.n_units = S.n_units;
+    A.nsec = S.nsec;
+    A.sec = 0;
+    for (int k = 0; k <= PR_MAX_SECTIONS; ++k) {
+        A.sec_row[k] = k <= S.nsec ? S.sec_row[k] : S.count;
+        A.sec_unit[k] = k <= S.nsec ? S.sec_unit[k] : S.n_units;
+    }
     A.d_count = S.count;
     A.seeds = S.seed_ids.as<int32_t>();
     A.n_seed = S.n_seed;
@@ -1103,7 +1200,11 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
                 k_ex_prep<<<P.g_all, 256, 0, st>>>(A);
             } else if (hc.mode == 0) {
                 void *kargs[] = {&A};
-                PR_CUDA(cudaLaunchKernel(P.k_pull_fn, dim3(P.g_pull), dim3(256), kargs, 0, st));
+                for (int sec = 0; sec < A.nsec; ++sec) {
+                    A.sec = sec;
+                    PR_CUDA(cudaLaunchKernel(P.k_pull_fn, dim3(P.g_pull), dim3(256), kargs, 0, st));
+                }
+                A.sec = 0;
             } else {
                 k_push<<<P.g_push, 256, 0, st>>>(A);
                 k_scan<<<P.g_scan, 256, 0, st>>>(A);

@@ -82,10 +82,29 @@ __global__ void k_row_cost(const int64_t *__restrict__ doff, int64_t cnt, int64_
 }
 
 // hub chunk units (row, -(chunk+1)) in row/chunk order
-__global__ void k_hub_units(const int64_t *__restrict__ base, int64_t n_hub, int2 *__restrict__ units) {
-    GRID_STRIDE(i, n_hub) {
-        for (int64_t c = base[i]; c < base[i + 1]; ++c) units[c] = make_int2((int)i, (int)(-(c - base[i] + 1)));
+// units of the hub rows [h0, h1), written from `out` on: one per HUB_CHUNK
+// slice, (row, -(slice+1))
+__global__ void k_hub_units(const int64_t *__restrict__ base, int64_t h0, int64_t h1, int2 *__restrict__ out) {
+    GRID_STRIDE(j, h1 - h0) {
+        const int64_t i = h0 + j;
+        for (int64_t c = base[i]; c < base[i + 1]; ++c) out[c - base[h0]] = make_int2((int)i, (int)(-(c - base[i] + 1)));
     }
+}
+
+// section row bounds: b[k] = first row whose CSC offset reaches k*E/K
+__global__ void k_section_bounds(const int64_t *__restrict__ doff, int64_t count, int nsec, int64_t *__restrict__ b) {
+    const int k = threadIdx.x;
+    if (k > nsec) return;
+    if (k == 0) { b[0] = 0; return; }
+    if (k == nsec) { b[k] = count; return; }
+    const int64_t E = doff[count], target = (int64_t)((__int128)E * k / nsec);
+    int64_t lo = 0, hi = count;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (doff[mid] >= target) hi = mid;
+        else lo = mid + 1;
+    }
+    b[k] = lo;
 }
 
 // k equal-cost row ranges over rows [r0, r1): unit j = [first row with
@@ -109,33 +128,90 @@ __global__ void k_range_units(const int64_t *__restrict__ cum, int64_t r0, int64
     }
 }
 
-int ensure_units(Graph &g, int which, int64_t blocks) {
+// Work units of a schedule for a persistent grid of `blocks` blocks, cut into
+// `nsec` Gauss-Seidel sections of equal edge count (rounds.cu).  Units are
+// laid out section by section, each section hub slices, then warp-row ranges,
+// then thread-row ranges, so a section's units are the contiguous range
+// [sec_unit[k], sec_unit[k+1]).
+int ensure_units(Graph &g, int which, int64_t blocks, int nsec) {
     auto &S = g.sched[which];
-    if (S.unit_blocks == blocks) return PR_OK;
+    if (nsec < 1) nsec = 1;
+    if (nsec > PR_MAX_SECTIONS) nsec = PR_MAX_SECTIONS;
+    if (S.unit_blocks == blocks && S.nsec == nsec) return PR_OK;
     Ctx &ctx = *g.ctx;
     cudaStream_t st = ctx.stream;
-    int64_t cum[4];
-    const int64_t marks[4] = {S.n_hub, S.n_hub + S.n_warp, S.count, 0};
-    for (int i = 0; i < 3; ++i)
-        PR_CUDA(cudaMemcpyAsync(&cum[i], S.row_cum.as<int64_t>() + marks[i], 8, cudaMemcpyDeviceToHost, st));
+    // section row bounds
+    int64_t b[PR_MAX_SECTIONS + 1];
+    {
+        DevBuf db;
+        PR_TRY(ensure(db, 8 * (PR_MAX_SECTIONS + 1)));
+        k_section_bounds<<<1, 32, 0, st>>>(S.doff.as<int64_t>(), S.count, nsec, db.as<int64_t>());
+        PR_CUDA(cudaMemcpyAsync(b, db.ptr, 8 * (nsec + 1), cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+    }
+    // segments (section x bin) and the prefix values they need
+    const int64_t bin_lo[3] = {0, S.n_hub, S.n_hub + S.n_warp};
+    const int64_t bin_hi[3] = {S.n_hub, S.n_hub + S.n_warp, S.count};
+    int64_t seg_lo[PR_MAX_SECTIONS][3], seg_hi[PR_MAX_SECTIONS][3];
+    int64_t cum_lo[PR_MAX_SECTIONS][3], cum_hi[PR_MAX_SECTIONS][3], hb_lo[PR_MAX_SECTIONS], hb_hi[PR_MAX_SECTIONS];
+    for (int k = 0; k < nsec; ++k)
+        for (int j = 0; j < 3; ++j) {
+            // section k's rows of bin j, clamped inside the bin
+            int64_t lo = b[k] > bin_lo[j] ? b[k] : bin_lo[j];
+            int64_t hi = b[k + 1] < bin_hi[j] ? b[k + 1] : bin_hi[j];
+            if (lo > bin_hi[j]) lo = bin_hi[j];
+            if (hi < lo) hi = lo;
+            seg_lo[k][j] = lo;
+            seg_hi[k][j] = hi;
+            PR_CUDA(cudaMemcpyAsync(&cum_lo[k][j], S.row_cum.as<int64_t>() + seg_lo[k][j], 8, cudaMemcpyDeviceToHost, st));
+            PR_CUDA(cudaMemcpyAsync(&cum_hi[k][j], S.row_cum.as<int64_t>() + seg_hi[k][j], 8, cudaMemcpyDeviceToHost, st));
+            if (j == 0) {
+                PR_CUDA(cudaMemcpyAsync(&hb_lo[k], S.chunk_base.as<int64_t>() + seg_lo[k][0], 8, cudaMemcpyDeviceToHost,
+                                        st));
+                PR_CUDA(cudaMemcpyAsync(&hb_hi[k], S.chunk_base.as<int64_t>() + seg_hi[k][0], 8, cudaMemcpyDeviceToHost,
+                                        st));
+            }
+        }
     PR_CUDA(cudaStreamSynchronize(st));
-    const int64_t cw = cum[1] - cum[0], ct = cum[2] - cum[1];
-    int64_t T = (cw + ct) / (blocks * UNITS_PER_BLOCK);
+    int64_t total = 0;
+    for (int k = 0; k < nsec; ++k) total += (cum_hi[k][1] - cum_lo[k][1]) + (cum_hi[k][2] - cum_lo[k][2]);
+    int64_t T = total / (blocks * UNITS_PER_BLOCK);
     if (T < 400 * ROW_COST) T = 400 * ROW_COST;  // >= 3200 edge-units per unit
-    const int64_t kw = S.n_warp ? (cw + T - 1) / T : 0, kt = (S.count - S.n_hub - S.n_warp) ? (ct + T - 1) / T : 0;
-    S.n_units = S.n_chunks + kw + kt;
-    PR_TRY(ensure(S.units, 8 * (S.n_units + 1)));
+    int64_t cnt[PR_MAX_SECTIONS][3];
+    int64_t n_units = 0;
+    for (int k = 0; k < nsec; ++k) {
+        S.sec_row[k] = b[k];
+        S.sec_unit[k] = n_units;
+        cnt[k][0] = hb_hi[k] - hb_lo[k];
+        for (int j = 1; j < 3; ++j) {
+            const int64_t c = cum_hi[k][j] - cum_lo[k][j];
+            cnt[k][j] = seg_hi[k][j] > seg_lo[k][j] ? (c + T - 1) / T : 0;
+        }
+        n_units += cnt[k][0] + cnt[k][1] + cnt[k][2];
+    }
+    S.sec_row[nsec] = b[nsec];
+    S.sec_unit[nsec] = n_units;
+    S.n_units = n_units;
+    PR_TRY(ensure(S.units, 8 * (n_units + 1)));
     int2 *U = S.units.as<int2>();
-    if (S.n_hub)
-        k_hub_units<<<grid_for(S.n_hub, 256), 256, 0, st>>>(S.chunk_base.as<int64_t>(), S.n_hub, U);
-    if (kw)
-        k_range_units<<<grid_for(kw, 256), 256, 0, st>>>(S.row_cum.as<int64_t>(), S.n_hub, S.n_hub + S.n_warp, kw,
-                                                        U + S.n_chunks);
-    if (kt)
-        k_range_units<<<grid_for(kt, 256), 256, 0, st>>>(S.row_cum.as<int64_t>(), S.n_hub + S.n_warp, S.count, kt,
-                                                        U + S.n_chunks + kw);
+    for (int k = 0; k < nsec; ++k) {
+        int64_t off = S.sec_unit[k];
+        if (cnt[k][0]) {
+            const int64_t nh = seg_hi[k][0] - seg_lo[k][0];
+            k_hub_units<<<grid_for(nh, 256), 256, 0, st>>>(S.chunk_base.as<int64_t>(), seg_lo[k][0], seg_hi[k][0],
+                                                          U + off);
+        }
+        off += cnt[k][0];
+        for (int j = 1; j < 3; ++j) {
+            if (cnt[k][j])
+                k_range_units<<<grid_for(cnt[k][j], 256), 256, 0, st>>>(S.row_cum.as<int64_t>(), seg_lo[k][j],
+                                                                       seg_hi[k][j], cnt[k][j], U + off);
+            off += cnt[k][j];
+        }
+    }
     PR_CUDA(cudaGetLastError());
     S.unit_blocks = blocks;
+    S.nsec = nsec;
     return PR_OK;
 }
 

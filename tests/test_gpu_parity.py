@@ -262,6 +262,35 @@ def test_c2_full_size_parity(xi):
                 assert tr.final.push_ops_dangling == cls.dangling_edge_count
 
 
+@pytest.mark.parametrize("sections", [2, 3, 8])
+def test_gauss_seidel_sections_parity(sections, monkeypatch, golden_corpus):
+    """IFP2 dense sweeps cut into Gauss-Seidel sections (big graphs use them
+    by default; PUSHRANK_GS_SECTIONS forces them here): same fixed point as
+    the round-synchronous oracle (L1 <= 1e-9, identical top-100), mass 1,
+    every dangling in-edge settled, and fewer rounds than Jacobi."""
+    monkeypatch.setenv("PUSHRANK_GS_SECTIONS", str(sections))
+    n, src, dst = synthetic.make("c2", seed=0)
+    g = P.from_edges(n, src, dst)
+    ref = oracle.from_edges(n, src, dst)
+    cls = P.classify(g)
+    pg = P.preprocess_ifp2(g, cls)
+    o = oracle.sync_simulate(ref, "ifp2", threshold=XI)
+    for mode in MODES:
+        vec, tr = P.ifp2_run(pg, cfg(), mode=mode)
+        assert np.abs(vec.values - o.values).sum() <= 1e-9, mode
+        assert np.array_equal(top100(vec.values), top100(o.values)), mode
+        assert abs(vec.values.sum() - 1.0) <= 1e-12
+        assert tr.final.push_ops_dangling == cls.dangling_edge_count
+        if mode == "pull":
+            assert tr.meta["rounds"] < o.iterations, (tr.meta["rounds"], o.iterations)
+    # and on every corpus graph (tiny ones have a single section)
+    for i in range(int(golden_corpus["count"])):
+        n, src, dst = corpus_graph(golden_corpus, i)
+        pg = P.preprocess_ifp2(P.from_edges(n, src, dst), None)
+        v2, _ = P.ifp2_run(pg, cfg(), mode="auto")
+        assert np.max(np.abs(v2.values - golden_corpus[f"g{i}_ifp2_values"])) <= max(1e-10, 10 * XI * n), i
+
+
 # ------------------------------------------------------------ known answers (reference tests)
 
 def test_known_answers():
