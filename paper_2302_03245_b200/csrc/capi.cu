@@ -145,6 +145,7 @@ int pr_ctx_destroy(pr_ctx *ctx) {
     cudaSetDevice(ctx->c.device);
     alloc_stream() = ctx->c.stream;
     cudaStreamSynchronize(ctx->c.stream);
+    release_execs(ctx->c);
     ctx->c.scratch.release();
     ctx->c.flush.release();
     cudaStreamDestroy(ctx->c.stream);

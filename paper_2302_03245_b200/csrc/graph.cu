@@ -34,13 +34,7 @@ int ensure(DevBuf &b, size_t bytes) {
     return PR_OK;
 }
 
-Graph::~Graph() {
-    for (auto &c : cached) {
-        if (c.exec) cudaGraphExecDestroy(c.exec);
-        if (c.graph) cudaGraphDestroy(c.graph);
-    }
-    delete run;
-}
+Graph::~Graph() { delete run; }
 
 
 static int bit_width_u64(unsigned long long x) {

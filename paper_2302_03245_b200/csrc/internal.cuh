@@ -63,7 +63,19 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     DevBuf scratch;          // CUB temporaries
     DevBuf flush;            // L2 flush buffer (bench)
+    // Instantiated round-loop graphs, keyed by the bytes of their launch plan
+    // (every pointer, size and parameter the kernels receive).  The stream-
+    // ordered pool hands a re-uploaded graph of the same shape the same
+    // addresses, so a new pr_graph usually hits here and skips instantiation.
+    struct ExecSlot {
+        std::vector<unsigned char> key;
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        uint64_t used = 0;
+    } execs[8];
+    uint64_t exec_tick = 0;
 };
+void release_execs(Ctx &ctx);
 
 // Per-block partial statistics of one round (reduced in fixed order).
 struct Partial {
@@ -179,13 +191,6 @@ struct Graph {
     Graph *run = nullptr;
     DevBuf perm;              // int32 [n]: run id -> original id
     DevBuf rank;              // int32 [n]: original id -> run id
-    // cached instantiated round-loop graphs, keyed by run parameters
-    struct Cached {
-        bool valid = false;
-        pr_run_params key{};
-        cudaGraph_t graph = nullptr;
-        cudaGraphExec_t exec = nullptr;
-    } cached[4];
     ~Graph();
 };
 
@@ -194,7 +199,6 @@ int need_csr(const Graph &g, const char *what);
 int attach_out_targets(Graph &g, const int64_t *out_tgt);
 int count_dangling(Graph &g);
 int ensure_run_layout(Graph &g);
-void invalidate_cache(Graph &g);
 int ensure_sched(Graph &g, int which);
 int ensure_units(Graph &g, int which, int64_t blocks, int nsec = 1);
 int build_from_device_edges(Ctx &ctx, int64_t n, const int64_t *d_src, const int64_t *d_dst,

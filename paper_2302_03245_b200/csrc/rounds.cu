@@ -856,18 +856,13 @@ struct Plan {
     const void *k_pull_fn;   // k_pull<STREAM, PREFETCH> chosen by the round's working set
 };
 
-static bool same_key(const pr_run_params &a, const pr_run_params &b) {
-    return a.algorithm == b.algorithm && a.mode == b.mode && a.damping == b.damping && a.threshold == b.threshold &&
-           a.max_rounds == b.max_rounds && a.push_switch == b.push_switch && a.converged_scope == b.converged_scope;
-}
-
-void invalidate_cache(Graph &g) {
-    for (auto &c : g.cached) {
-        if (c.exec) cudaGraphExecDestroy(c.exec);
-        if (c.graph) cudaGraphDestroy(c.graph);
-        c.exec = nullptr;
-        c.graph = nullptr;
-        c.valid = false;
+void release_execs(Ctx &ctx) {
+    for (auto &e : ctx.execs) {
+        if (e.exec) cudaGraphExecDestroy(e.exec);
+        if (e.graph) cudaGraphDestroy(e.graph);
+        e.exec = nullptr;
+        e.graph = nullptr;
+        e.key.clear();
     }
 }
 
@@ -951,12 +946,10 @@ static int build_graph(Plan &P, cudaGraph_t *out_g, cudaGraphExec_t *out_exec) {
     return PR_OK;
 }
 
-// Workspace sized once per graph; any reallocation invalidates the cached
-// executable graphs (they bake the pointers in).
+// Workspace sized once per graph (the executable-graph cache is keyed by the
+// pointers, so a reallocation simply misses it).
 static int ws_alloc(Graph &g, int64_t need_blocks, int64_t fcap) {
     int64_t n = g.n;
-    void *before[9] = {g.h.ptr, g.reserved.ptr, g.s2.ptr, g.act.ptr, g.in_d.ptr,
-                       g.frontier2.ptr, g.partials.ptr, g.ctl.ptr, g.rows.ptr};
     PR_TRY(ensure(g.h, 8 * n));
     PR_TRY(ensure(g.reserved, 8 * n));
     PR_TRY(ensure(g.s2, 16 * n));
@@ -972,9 +965,6 @@ static int ws_alloc(Graph &g, int64_t need_blocks, int64_t fcap) {
         PR_TRY(ensure(g.partials, sizeof(Partial) * 3 * mb));
         g.max_blocks = mb;
     }
-    void *after[9] = {g.h.ptr, g.reserved.ptr, g.s2.ptr, g.act.ptr, g.in_d.ptr,
-                      g.frontier2.ptr, g.partials.ptr, g.ctl.ptr, g.rows.ptr};
-    if (memcmp(before, after, sizeof(before)) != 0) invalidate_cache(g);
     return PR_OK;
 }
 
@@ -1045,12 +1035,7 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     if (nsec > 1)
         k_pull_fn = stream ? (prefetch ? (const void *)k_pull<true, true, true> : (const void *)k_pull<true, false, true>)
                            : (prefetch ? (const void *)k_pull<false, true, true> : (const void *)k_pull<false, false, true>);
-    {
-        const void *before = g.sched[which].units.ptr;
-        const int64_t before_n = g.sched[which].n_units;
-        PR_TRY(ensure_units(g, which, pull_blocks, nsec));
-        if (g.sched[which].units.ptr != before || g.sched[which].n_units != before_n) invalidate_cache(g);
-    }
+    PR_TRY(ensure_units(g, which, pull_blocks, nsec));
     const int64_t fcap = n + g.m / TILE + 1;
     if (getenv("PUSHRANK_TIMING"))
         fprintf(stderr, "[pushrank] round working set %.1f MB (L2 %.1f MB): stream %d prefetch %d sections %d\n",
@@ -1150,23 +1135,31 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     PR_CUDA(cudaEventCreate(&e2));
     PR_CUDA(cudaEventRecord(e0, st));
     if (!host_loop) {
-        Graph::Cached *slot = nullptr;
-        for (auto &c : g.cached)
-            if (c.valid && same_key(c.key, p)) { slot = &c; break; }
+        // the plan's bytes (graph-owned conditional handles still zero) key
+        // the context's executable-graph cache
+        const unsigned char *pb = reinterpret_cast<const unsigned char *>(&P);
+        std::vector<unsigned char> key(pb, pb + sizeof(P));
+        Ctx::ExecSlot *slot = nullptr;
+        for (auto &e : ctx.execs)
+            if (e.exec && e.key == key) { slot = &e; break; }
         if (!slot) {
-            slot = &g.cached[0];
-            for (auto &c : g.cached)
-                if (!c.valid) { slot = &c; break; }
+            slot = &ctx.execs[0];
+            for (auto &e : ctx.execs)
+                if (!e.exec || e.used < slot->used) slot = &e;
+            if (!slot->exec) {
+                for (auto &e : ctx.execs)
+                    if (!e.exec) { slot = &e; break; }
+            }
             if (slot->exec) cudaGraphExecDestroy(slot->exec);
             if (slot->graph) cudaGraphDestroy(slot->graph);
             slot->exec = nullptr;
             slot->graph = nullptr;
-            slot->valid = false;
+            slot->key.clear();
             PR_TRY(build_graph(P, &slot->graph, &slot->exec));
-            slot->key = p;
-            slot->valid = true;
+            slot->key = std::move(key);
             phase_mark(ctx.stream, "run: graph instantiate");
         }
+        slot->used = ++ctx.exec_tick;
         PR_CUDA(cudaGraphLaunch(slot->exec, st));
     } else {
         A.use_graph = 0;
