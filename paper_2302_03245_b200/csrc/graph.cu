@@ -456,9 +456,12 @@ __global__ void k_tail_rows(const int64_t *__restrict__ in_off, int64_t live_end
     }
 }
 
+static int sort_by_source(Ctx &ctx, const DevBuf &in_off, const DevBuf &in_src, int64_t rows, int64_t m_e,
+                          int64_t n, DevBuf &out_tgt);
+
 int preprocess_ifp2_device(Graph &g) {
     if (g.has_ifp2) return PR_OK;
-    PR_TRY(need_csr(g, "the IFP2 live CSR"));
+    if (g.live_end < 0) PR_TRY(need_csr(g, "the IFP2 live CSR"));
     Ctx &ctx = *g.ctx;
     cudaStream_t st = ctx.stream;
     int64_t n = g.n, m = g.m;
@@ -475,9 +478,15 @@ int preprocess_ifp2_device(Graph &g) {
         return cub::DeviceScan::ExclusiveSum(t, b, deg64.as<int64_t>(), g.live_off.as<int64_t>(), (int)(n + 1), st);
     }));
     // live_targets: stable compaction keeps each row's target order (graph.py:353-354)
-    PR_TRY(ensure(g.live_tgt, 4 * (m ? m : 1)));
     int64_t live_m = 0;
-    if (m) {
+    if (g.live_end >= 0) {
+        // run layout: the live edges are the CSC rows of the non-dangling
+        // prefix [0, live_end); sorted by source they are the live CSR
+        PR_CUDA(cudaMemcpyAsync(&live_m, g.in_off.as<int64_t>() + g.live_end, 8, cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+        PR_TRY(sort_by_source(ctx, g.in_off, g.in_src, g.live_end, live_m, n, g.live_tgt));
+    } else if (m) {
+        PR_TRY(ensure(g.live_tgt, 4 * m));
         auto first = thrust::make_counting_iterator<int64_t>(0);
         DevBuf eids;
         PR_TRY(ensure(eids, 8 * m));
@@ -491,6 +500,7 @@ int preprocess_ifp2_device(Graph &g) {
             k_gather_i32<<<gs_grid(ctx, live_m), 256, 0, st>>>(g.out_tgt.as<int32_t>(), eids.as<int64_t>(), live_m,
                                                                g.live_tgt.as<int32_t>());
     }
+    if (!g.live_tgt.ptr) PR_TRY(ensure(g.live_tgt, 4));
     // dangling ids (ascending) and their source CSR (graph.py:363-367)
     int64_t nd = 0, md = 0;
     if (g.live_end >= 0) {
@@ -669,32 +679,42 @@ __global__ void __launch_bounds__(256) k_edge_rows(const int64_t *__restrict__ o
     }
 }
 
-// The out-adjacency of the run layout from its in-adjacency: a stable sort of
-// the CSC's (source, destination) pairs by source.  Destinations come out
-// ascending inside every row, so the result is deterministic.  Used when the
-// graph was uploaded CSC-only (the fast engines never need the original
-// out_targets).
-static int csr_from_csc(Ctx &ctx, const DevBuf &orig_out_off, const DevBuf &perm, int64_t n, int64_t m,
-                        const DevBuf &in_off, const DevBuf &in_src, DevBuf &out_off, DevBuf &out_tgt) {
+// Out-adjacency from in-adjacency: a stable sort of the (source, destination)
+// pairs of the first m_e CSC edges (rows [0, rows)) by source.  Destinations
+// come out ascending inside every row, so the result is deterministic.  The
+// caller provides the out-offsets (the per-source counts of those edges).
+static int sort_by_source(Ctx &ctx, const DevBuf &in_off, const DevBuf &in_src, int64_t rows, int64_t m_e,
+                          int64_t n, DevBuf &out_tgt) {
     cudaStream_t st = ctx.stream;
-    DevBuf len, keys_out, rows;
-    PR_TRY(ensure(len, 8 * (n + 1)));
-    PR_TRY(ensure(out_off, 8 * (n + 1)));
-    PR_TRY(ensure(out_tgt, 4 * (m ? m : 1)));
-    k_perm_len<<<gs_grid(ctx, n + 1), 256, 0, st>>>(orig_out_off.as<int64_t>(), perm.as<int32_t>(), n, len.as<int64_t>());
-    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
-        return cub::DeviceScan::ExclusiveSum(t, b, len.as<int64_t>(), out_off.as<int64_t>(), (int)(n + 1), st);
-    }));
-    if (!m) return PR_OK;
-    PR_TRY(ensure(keys_out, 4 * m));
-    PR_TRY(ensure(rows, 4 * m));
-    k_edge_rows<<<seg_grid(ctx, m), 256, 0, st>>>(in_off.as<int64_t>(), n, m, rows.as<int32_t>());
+    PR_TRY(ensure(out_tgt, 4 * (m_e ? m_e : 1)));
+    if (!m_e) return PR_OK;
+    DevBuf keys_out, row_of;
+    PR_TRY(ensure(keys_out, 4 * m_e));
+    PR_TRY(ensure(row_of, 4 * m_e));
+    k_edge_rows<<<seg_grid(ctx, m_e), 256, 0, st>>>(in_off.as<int64_t>(), rows, m_e, row_of.as<int32_t>());
     int bits = 1;
     while (bits < 31 && ((int64_t)1 << bits) < n) ++bits;
     PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
         return cub::DeviceRadixSort::SortPairs(t, b, (const uint32_t *)in_src.ptr, keys_out.as<uint32_t>(),
-                                               rows.as<int32_t>(), out_tgt.as<int32_t>(), m, 0, bits, st);
+                                               row_of.as<int32_t>(), out_tgt.as<int32_t>(), m_e, 0, bits, st);
     }));
+    return PR_OK;
+}
+
+// The run layout's full out-adjacency, built on first use (IFP1's push
+// rounds): permuted from the original when that has one, else sorted out of
+// the run layout's CSC.  IFP2 never needs it (its live CSR comes from the
+// CSC prefix, preprocess_ifp2_device).
+int ensure_run_csr(Graph &r) {
+    if (r.has_csr) return PR_OK;
+    Ctx &ctx = *r.ctx;
+    Graph &g = *r.orig;
+    if (g.has_csr)
+        PR_TRY(permute_adjacency(ctx, g.out_off, g.out_tgt, g.perm, g.rank, r.n, r.m, r.out_off, r.out_tgt));
+    else
+        PR_TRY(sort_by_source(ctx, r.in_off, r.in_src, r.n, r.m, r.n, r.out_tgt));
+    PR_CUDA(cudaGetLastError());
+    r.has_csr = true;
     return PR_OK;
 }
 
@@ -749,9 +769,19 @@ int ensure_run_layout(Graph &g) {
     r->n = n;
     r->m = m;
     r->raw = g.raw;
+    r->orig = &g;
+    r->has_csr = false;       // out_tgt on demand (ensure_run_csr)
     int rc = permute_adjacency(ctx, g.in_off, g.in_src, g.perm, g.rank, n, m, r->in_off, r->in_src);
-    if (!rc) rc = g.has_csr ? permute_adjacency(ctx, g.out_off, g.out_tgt, g.perm, g.rank, n, m, r->out_off, r->out_tgt)
-                            : csr_from_csc(ctx, g.out_off, g.perm, n, m, r->in_off, r->in_src, r->out_off, r->out_tgt);
+    DevBuf len;
+    if (!rc) rc = ensure(len, 8 * (n + 1));
+    if (!rc) rc = ensure(r->out_off, 8 * (n + 1));
+    if (!rc) {
+        k_perm_len<<<gs_grid(ctx, n + 1), 256, 0, st>>>(g.out_off.as<int64_t>(), g.perm.as<int32_t>(), n,
+                                                        len.as<int64_t>());
+        rc = cub_run(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceScan::ExclusiveSum(t, b, len.as<int64_t>(), r->out_off.as<int64_t>(), (int)(n + 1), st);
+        });
+    }
     if (!rc) rc = ensure(r->out_deg, 4 * n);
     if (!rc) k_degree<<<gs_grid(ctx, n), 256, 0, st>>>(r->out_off.as<int64_t>(), n, r->out_deg.as<int32_t>());
     int64_t bounds[2] = {n, n};

@@ -189,6 +189,7 @@ struct Graph {
     // the IFP2 destination set is a contiguous id range.  Exact mode keeps
     // the original layout (bit-exact summation order).
     Graph *run = nullptr;
+    Graph *orig = nullptr;    // run layout: the graph it was built from (non-owning)
     DevBuf perm;              // int32 [n]: run id -> original id
     DevBuf rank;              // int32 [n]: original id -> run id
     ~Graph();
@@ -199,6 +200,7 @@ int need_csr(const Graph &g, const char *what);
 int attach_out_targets(Graph &g, const int64_t *out_tgt);
 int count_dangling(Graph &g);
 int ensure_run_layout(Graph &g);
+int ensure_run_csr(Graph &r);
 int ensure_sched(Graph &g, int which);
 int ensure_units(Graph &g, int which, int64_t blocks, int nsec = 1);
 int build_from_device_edges(Ctx &ctx, int64_t n, const int64_t *d_src, const int64_t *d_dst,

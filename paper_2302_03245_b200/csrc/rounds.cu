@@ -992,8 +992,12 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     }
     Graph &g = *gp;
     const int32_t *perm = exact ? nullptr : g_in.perm.as<int32_t>();
-    if (algo == PR_ALGO_IFP2) PR_TRY(preprocess_ifp2_device(g));
-    else PR_TRY(ensure_dtc(g));
+    if (algo == PR_ALGO_IFP2) {
+        PR_TRY(preprocess_ifp2_device(g));
+    } else {
+        PR_TRY(ensure_dtc(g));
+        if (!exact) PR_TRY(ensure_run_csr(g));   // IFP1 pushes along the full out-adjacency
+    }
     PR_TRY(count_dangling(g));
     phase_mark(ctx.stream, "run: ifp2 split/dtc");
     const int which = algo == PR_ALGO_IFP2 ? 1 : 0;
