@@ -369,6 +369,12 @@ def e2e_measure(args, g, dev_resident):
             times.append(dt)
             ops = tr.final.push_ops
             h2d = device_graph(obj).h2d_bytes
+        # release this step's graph before the next upload (a user would not
+        # keep two copies alive); the freed pool blocks are then reused at the
+        # same addresses, which also lets the next solve reuse its executable
+        # graph
+        if args.algo == "ifp2":
+            del pg
         del obj
     mean = sum(times) / len(times)
     return {"value": ops / mean / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": int(h2d),

@@ -18,8 +18,10 @@ B="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline"
 if timeout 300 $B > $O/hostloop_c2.json 2>&1; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
     --log-file $O/launches_c2.csv $B > $O/ncu_launches.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_pull|k_scan|k_push" \
-    -s 60 -c 3 -o $O/full_c2 $B > $O/ncu_full_c2.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_pull" \
+    -s 60 -c 2 -o $O/full_c2 $B > $O/ncu_full_c2.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_scan|k_push" \
+    -c 4 -o $O/sparse_c2 $B > $O/ncu_sparse_c2.log 2>&1
 fi
 B5="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --config c5"
 if timeout 600 $B5 > $O/hostloop_c5.json 2>&1; then
