@@ -268,6 +268,8 @@ def run_ours(args):
                          "loop_achieved": r0.bytes_moved / (r0.round_ms * 1e-3) / 1e9,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
             "gpu_launches": int(launches), "clocks": clocks.summary()}
+    if args.algo == "ifp2":
+        line["l1_crossing"] = l1_crossing(args, dev, r0)
     if not args.no_e2e and args.config != "c5":
         line["e2e"] = e2e_measure(args, g, dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config != "c5":
@@ -337,6 +339,26 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
                 "note": "host-driven partitioned rounds; exchange = NCCL all-gather of shares per round"}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
+
+
+def l1_crossing(args, dev, res_timed):
+    """the first round whose non-dangling residual
+    L1_p = sum_{v non-dangling} h_v / n is below 1e-10, from one extra traced
+    solve (untimed).  IFP2 keeps exactly 1.0 pending on every dangling vertex
+    until the settle, so the non-dangling residual is h_l1 - n_dangling.
+    `ms` is that row's device timestamp (globaltimer, from the solve start)
+    plus the settle/normalise time of the timed solves."""
+    from paper_2302_03245_b200 import _lib
+    n_d = int(dev.preprocess_ifp2().dangling)
+    _, rows, res, _, _ = dev.run(args.algo, args.mode, DAMPING, XI, 1_000_000, _lib.CONV_SCAN,
+                                 push_switch=args.push_switch, row_cap=1 << 16)
+    l1p = (rows["h_l1"] - n_d) / dev.n
+    hit = np.nonzero(l1p < 1e-10)[0]
+    if not hit.size:
+        return None
+    r = int(hit[0])
+    return {"round": r, "rounds_total": int(res.rows) - 1, "l1_p": float(max(l1p[r], 0.0)),
+            "ms": float(rows["wall_ms"][r] + (res_timed.push_ms - res_timed.round_ms))}
 
 
 def e2e_measure(args, g, dev_resident):

@@ -320,6 +320,12 @@ def test_known_answers():
     single = P.from_edges(1, [], [])
     v, _ = P.ifp1_run(single, P.classify(single), cfg())
     assert v.values.tolist() == [1.0]
+    # star4, fp-full sync: a quarter of the mass on the only scanned vertex,
+    # first decay 0.85 * 0.25 (test_engines.py:192-197)
+    star = P.from_edges(4, [0, 0, 0], [1, 2, 3])
+    _, ts = P.sync_simulate(star, cfg(), variant="fp-full")
+    assert ts.samples[0].alpha == 0.25
+    assert ts.samples[1].h_l1 / ts.samples[0].h_l1 == pytest.approx(0.85 * 0.25, abs=1e-12)
 
 
 def test_power_matches_reference(golden_corpus, golden_c1):
