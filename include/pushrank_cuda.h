@@ -42,6 +42,7 @@ extern "C" {
 #define PR_ERR_STATE (-3)       /* missing prerequisite (e.g. preprocess before IFP2) */
 #define PR_ERR_NOT_SETTLED (-4) /* max_rounds exhausted (engines.py:455-456 RuntimeError) */
 #define PR_ERR_NOMEM (-5)       /* device allocation failed */
+#define PR_ERR_FORMAT (-6)      /* edge-list text the device parser does not accept (graph.py:180-233) */
 
 #define PR_ABI_VERSION 2
 
@@ -141,6 +142,20 @@ int pr_graph_upload(pr_ctx *ctx, int64_t n, int64_t m, const int64_t *out_offset
                     const int64_t *out_targets, const int64_t *in_offsets,
                     const int64_t *in_sources, pr_graph **out);
 int pr_graph_attach_out_targets(pr_graph *g, const int64_t *out_targets);
+/* graph.py:201-259 load_edge_list, on the device: `text` is the raw bytes of
+ * a whitespace-separated "src dst" edge list ('#' comments, blank lines).
+ * Ids are remapped densely in order of first appearance (interleaved
+ * src/dst), duplicates dropped, self-loops kept.  Returns PR_ERR_FORMAT for
+ * text outside that grammar (a third column, a non-digit, a negative id, an
+ * int64 overflow, no edges): the caller re-parses it on the host to report
+ * the reference's line-numbered error, then calls pr_graph_from_raw_ids. */
+int pr_graph_load_edge_list(pr_ctx *ctx, const char *text, int64_t len, pr_graph **out,
+                            int64_t *raw_edges);
+/* graph.py:243-257 on already-parsed raw ids (int64[m] each, non-negative). */
+int pr_graph_from_raw_ids(pr_ctx *ctx, const int64_t *src, const int64_t *dst, int64_t m,
+                          pr_graph **out);
+/* Graph.original_ids -> int64[n] (identity for graphs not built from raw ids). */
+int pr_graph_original_ids(pr_graph *g, int64_t *out);
 int pr_graph_destroy(pr_graph *g);
 int pr_graph_info(const pr_graph *g, int64_t *n, int64_t *m);
 /* Graph arrays back to the host (int64, reference layout); NULL skips one. */

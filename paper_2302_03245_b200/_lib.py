@@ -22,7 +22,7 @@ c_f64 = ctypes.c_double
 c_i32 = ctypes.c_int32
 c_vp = ctypes.c_void_p
 
-PR_OK, PR_ERR_ARG, PR_ERR_CUDA, PR_ERR_STATE, PR_ERR_NOT_SETTLED, PR_ERR_NOMEM = 0, -1, -2, -3, -4, -5
+PR_OK, PR_ERR_ARG, PR_ERR_CUDA, PR_ERR_STATE, PR_ERR_NOT_SETTLED, PR_ERR_NOMEM, PR_ERR_FORMAT = 0, -1, -2, -3, -4, -5, -6
 ALGO = {"ifp1": 0, "ifp2": 1, "fp-full": 2}
 MODE = {"auto": 0, "pull": 1, "push": 2, "exact": 3}
 CONV_SCAN, CONV_ALL = 0, 1
@@ -83,6 +83,9 @@ SIGNATURES = {
     "pr_graph_upload": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, _PP]),
     "pr_graph_attach_out_targets": (ctypes.c_int, [c_vp, c_vp]),
     "pr_host_alloc": (ctypes.c_int, [c_i64, _PP]),
+    "pr_graph_load_edge_list": (ctypes.c_int, [c_vp, ctypes.c_char_p, c_i64, _PP, c_vp]),
+    "pr_graph_from_raw_ids": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, _PP]),
+    "pr_graph_original_ids": (ctypes.c_int, [c_vp, c_vp]),
     "pr_host_free": (ctypes.c_int, [c_vp]),
     "pr_graph_destroy": (ctypes.c_int, [c_vp]),
     "pr_graph_info": (ctypes.c_int, [c_vp, _PI64, _PI64]),

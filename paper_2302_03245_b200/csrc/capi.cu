@@ -193,6 +193,45 @@ int pr_graph_from_device_edges(pr_ctx *ctx, int64_t n, const int64_t *d_src, con
     return PR_OK;
 }
 
+int pr_graph_load_edge_list(pr_ctx *ctx, const char *text, int64_t len, pr_graph **out, int64_t *raw_edges) {
+    CHECK_PTR(ctx, "ctx");
+    CHECK_PTR(out, "out");
+    if (len > 0) CHECK_PTR(text, "text");
+    PR_TRY(set_device(ctx->c));
+    Graph *g = nullptr;
+    PR_TRY(load_edge_list_device(ctx->c, text, len, &g));
+    if (raw_edges) *raw_edges = g->raw;
+    *out = new pr_graph{g};
+    return PR_OK;
+}
+
+int pr_graph_from_raw_ids(pr_ctx *ctx, const int64_t *src, const int64_t *dst, int64_t m, pr_graph **out) {
+    CHECK_PTR(ctx, "ctx");
+    CHECK_PTR(out, "out");
+    if (m > 0) {
+        CHECK_PTR(src, "src");
+        CHECK_PTR(dst, "dst");
+    }
+    PR_TRY(set_device(ctx->c));
+    Graph *g = nullptr;
+    PR_TRY(graph_from_raw_ids(ctx->c, src, dst, m, &g));
+    *out = new pr_graph{g};
+    return PR_OK;
+}
+
+int pr_graph_original_ids(pr_graph *g, int64_t *out) {
+    CHECK_PTR(g, "graph");
+    CHECK_PTR(out, "out");
+    Graph &G = *g->g;
+    PR_TRY(set_device(*G.ctx));
+    if (G.orig_ids.ptr) {
+        PR_CUDA(cudaMemcpy(out, G.orig_ids.ptr, 8 * G.n, cudaMemcpyDeviceToHost));
+    } else {
+        for (int64_t i = 0; i < G.n; ++i) out[i] = i;
+    }
+    return PR_OK;
+}
+
 int pr_graph_upload(pr_ctx *ctx, int64_t n, int64_t m, const int64_t *out_offsets, const int64_t *out_targets,
                     const int64_t *in_offsets, const int64_t *in_sources, pr_graph **out) {
     CHECK_PTR(ctx, "ctx");

@@ -121,6 +121,7 @@ struct RunCtl {
 struct Graph {
     Ctx *ctx = nullptr;
     int64_t n = 0, m = 0, raw = 0;
+    DevBuf orig_ids;  // int64 [n] first-appearance id table (ingest.cu); empty = identity
     // run layout only: vertices [live_end, n) are the dangling ones (classes
     // out=0&in>0, isolated), so their in-edges are the CSC tail
     int64_t live_end = -1;
@@ -203,6 +204,8 @@ int ensure_run_layout(Graph &g);
 int ensure_run_csr(Graph &r);
 int ensure_sched(Graph &g, int which);
 int ensure_units(Graph &g, int which, int64_t blocks, int nsec = 1);
+int load_edge_list_device(Ctx &ctx, const char *text, int64_t len, Graph **out);
+int graph_from_raw_ids(Ctx &ctx, const int64_t *src, const int64_t *dst, int64_t m, Graph **out);
 int build_from_device_edges(Ctx &ctx, int64_t n, const int64_t *d_src, const int64_t *d_dst,
                             int64_t m_raw, Graph **out);
 int classify_device(Graph &g);

@@ -233,6 +233,7 @@ class Graph:
         self.raw_edge_count = int(raw_edge_count)
         self.name = name
         self._orig = None if original_ids is None else np.asarray(original_ids, np.int64)
+        self._orig_on_device = False   # load_edge_list keeps the id table on the device
         self._arrays = None
 
     def _export(self) -> dict:
@@ -252,6 +253,10 @@ class Graph:
 
     @property
     def original_ids(self) -> np.ndarray:
+        if self._orig is None and self._orig_on_device:
+            out = np.empty(self.n, np.int64)
+            _lib.check(_lib.load().pr_graph_original_ids(self.dev.handle, _lib.ptr(out)), "original_ids")
+            self._orig = out
         return self._orig if self._orig is not None else np.arange(self.n, dtype=np.int64)
 
     def out_neighbors(self, v: int) -> np.ndarray:

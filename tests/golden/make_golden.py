@@ -20,6 +20,11 @@ Fixtures
               sha256 digests of the integer arrays, full float vectors.
   synth42.npz the reference acceptance graph synth.generate(10_000, 100_000,
               0.2, seed=42) (test_acceptance.py:41-45): edges + outputs.
+  edge_lists.npz  load_edge_list (graph.py:201-259) on edge-list texts: the
+              cases of test_graph.py:20-68 plus tabs, CRLF, inline comments,
+              blank lines, '+' signs, 43-bit ids, no trailing newline, a
+              seeded 20k-edge list; and malformed texts with the exception
+              class and message.  ``--only edge_lists`` regenerates just this.
 """
 
 from __future__ import annotations
@@ -107,14 +112,59 @@ def reference_outputs(P, g, prefix: str, out: dict, full_ints: bool, dense: bool
         out[f"{prefix}dense_values"] = P.dense_oracle(g, P.SolverConfig()).values
 
 
+def edge_list_texts() -> tuple[list[bytes], list[bytes]]:
+    ok = [b"0 1\n1 2\n", b"# c\n5 9\n5 9\n", b"7 3\n3 1\n", b"0\t1\n1\t0\n",
+          b"10 20\r\n20 30\r\n30 10\r\n", b"1 2 # note\n2 3\n", b"\n  4   5\n\n5 4\n   \n",
+          b"9000000000000 1\n1 42\n42 9000000000000\n", b"0 0\n0 1\n0 1\n", b"+1 2\n2 +3\n",
+          b"1 2\n2 3", b"3 3\n"]
+    rng = np.random.default_rng(20261019)
+    ids = rng.integers(0, 1 << 40, size=3000)
+    e = rng.integers(0, ids.size, size=(20000, 2))
+    lines = [f"{ids[a]} {ids[b]}" for a, b in e]
+    for k in range(0, len(lines), 997):
+        lines.insert(k, "# block")
+    ok.append(("\n".join(lines) + "\n").encode())
+    bad = [b"0 1\nx 2\n", b"# head\n0 1\n4\n", b"", b"# only comments\n", b"0 1\n-2 1\n", b"0 1 2\n",
+           b"0 1\n1 2 3\n", b"5#c 6\n", b"1 99999999999999999999\n", b"0 1\n\xff 2\n"]
+    return ok, bad
+
+
+def edge_lists(P) -> None:
+    ok, bad = edge_list_texts()
+    out = {"n_ok": np.int64(len(ok)), "n_bad": np.int64(len(bad))}
+    for i, t in enumerate(ok):
+        g = P.load_edge_list(t)
+        out[f"ok{i}_text"] = np.frombuffer(t, np.uint8)
+        out[f"ok{i}_n"] = np.int64(g.n)
+        out[f"ok{i}_raw"] = np.int64(g.raw_edge_count)
+        for k in ("original_ids", "out_offsets", "out_targets", "in_offsets", "in_sources"):
+            out[f"ok{i}_{k}"] = np.asarray(getattr(g, k), np.int64)
+    for i, t in enumerate(bad):
+        out[f"bad{i}_text"] = np.frombuffer(t, np.uint8)
+        try:
+            P.load_edge_list(t)
+            raise SystemExit(f"bad case {i} did not raise")
+        except Exception as exc:  # noqa: BLE001 -- record whatever the reference raises
+            out[f"bad{i}_type"] = np.array(type(exc).__name__)
+            out[f"bad{i}_msg"] = np.array(str(exc))
+    np.savez_compressed(os.path.join(HERE, "edge_lists.npz"), **out)
+    print("edge_lists.npz:", len(ok), "ok,", len(bad), "malformed")
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref-src", default="/tmp/refpkg/src")
+    ap.add_argument("--only", default=None, choices=["edge_lists"])
     args = ap.parse_args()
     ensure_reference(args.ref_src)
     import pushrank as P
     import corpus
     from pushrank import synth
+
+    if args.only == "edge_lists":
+        edge_lists(P)
+        return
+    edge_lists(P)
 
     sys.path.insert(0, REPO)
     from paper_2302_03245_b200 import synthetic

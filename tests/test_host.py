@@ -100,3 +100,28 @@ def test_rmat_numpy_generator_is_deterministic_and_sane():
     assert n == 4096 and s1.max() < n and d1.max() < n
     # quadrant a dominates: the low half of the id range holds ~76% of sources
     assert 0.70 < np.mean(s1 < n // 2) < 0.82
+
+
+# ------------------------------------------------------------ edge-list ingest (host part)
+
+def test_edge_list_host_parse_matches_reference_errors():
+    """The host re-parse that load_edge_list falls back to for text the
+    device parser refuses reports the reference's exceptions (graph.py:
+    180-236); pinned by tests/golden/edge_lists.npz (made by the reference)."""
+    import os
+    from paper_2302_03245_b200.ingest import GraphFormatError, _host_parse
+    d = np.load(os.path.join(os.path.dirname(__file__), "golden", "edge_lists.npz"))
+    for i in range(int(d["n_bad"])):
+        text = d[f"bad{i}_text"].tobytes()
+        want_type, want_msg = str(d[f"bad{i}_type"]), str(d[f"bad{i}_msg"])
+        try:
+            src, dst = _host_parse(text)
+        except Exception as exc:  # noqa: BLE001
+            assert type(exc).__name__ == want_type, (i, exc)
+            assert str(exc) == want_msg, (i, exc)
+            continue
+        # no exception: only the empty streams get here (load_edge_list raises)
+        assert src.size == 0 and "empty graph" in want_msg, i
+    for i in range(int(d["n_ok"])):
+        src, dst = _host_parse(d[f"ok{i}_text"].tobytes())
+        assert src.size == int(d[f"ok{i}_raw"]), i
