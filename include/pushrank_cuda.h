@@ -156,6 +156,19 @@ int pr_graph_from_raw_ids(pr_ctx *ctx, const int64_t *src, const int64_t *dst, i
                           pr_graph **out);
 /* Graph.original_ids -> int64[n] (identity for graphs not built from raw ids). */
 int pr_graph_original_ids(pr_graph *g, int64_t *out);
+
+/* ---- output formats (serialize.py) ----------------------------------------
+ * serialize.py:16 ranking order: indices of `values` by score descending,
+ * ties by original id ascending (np.lexsort((original_ids, -values))); the
+ * first k of them.  original_ids NULL = identity. */
+int pr_rank_order(pr_ctx *ctx, const double *values, const int64_t *original_ids, int64_t n, int64_t k,
+                  int64_t *order);
+/* serialize.py:14-21 write_ranking_csv: byte-identical to the reference's
+ * csv.writer output (scores formatted as Python repr(float)). */
+int pr_write_ranking_csv(pr_ctx *ctx, const double *values, const int64_t *original_ids, int64_t n,
+                         const char *path);
+/* repr(float) of one finite double into out[32]; returns the length. */
+int pr_format_score(double value, char *out);
 int pr_graph_destroy(pr_graph *g);
 int pr_graph_info(const pr_graph *g, int64_t *n, int64_t *m);
 /* Graph arrays back to the host (int64, reference layout); NULL skips one. */

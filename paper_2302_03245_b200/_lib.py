@@ -86,6 +86,9 @@ SIGNATURES = {
     "pr_graph_load_edge_list": (ctypes.c_int, [c_vp, ctypes.c_char_p, c_i64, _PP, c_vp]),
     "pr_graph_from_raw_ids": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, _PP]),
     "pr_graph_original_ids": (ctypes.c_int, [c_vp, c_vp]),
+    "pr_rank_order": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_vp]),
+    "pr_write_ranking_csv": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, ctypes.c_char_p]),
+    "pr_format_score": (ctypes.c_int, [ctypes.c_double, ctypes.c_char_p]),
     "pr_host_free": (ctypes.c_int, [c_vp]),
     "pr_graph_destroy": (ctypes.c_int, [c_vp]),
     "pr_graph_info": (ctypes.c_int, [c_vp, _PI64, _PI64]),

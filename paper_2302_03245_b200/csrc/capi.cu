@@ -232,6 +232,32 @@ int pr_graph_original_ids(pr_graph *g, int64_t *out) {
     return PR_OK;
 }
 
+int pr_rank_order(pr_ctx *ctx, const double *values, const int64_t *original_ids, int64_t n, int64_t k,
+                  int64_t *order) {
+    CHECK_PTR(ctx, "ctx");
+    if (n > 0) {
+        CHECK_PTR(values, "values");
+        CHECK_PTR(order, "order");
+    }
+    if (n < 0 || k < 0) return fail(PR_ERR_ARG, "n and k must be non-negative");
+    PR_TRY(set_device(ctx->c));
+    return rank_order(ctx->c, values, original_ids, n, k, order);
+}
+
+int pr_write_ranking_csv(pr_ctx *ctx, const double *values, const int64_t *original_ids, int64_t n,
+                         const char *path) {
+    CHECK_PTR(ctx, "ctx");
+    CHECK_PTR(path, "path");
+    if (n > 0) CHECK_PTR(values, "values");
+    PR_TRY(set_device(ctx->c));
+    return write_ranking_csv(ctx->c, values, original_ids, n, path);
+}
+
+int pr_format_score(double value, char *out) {
+    CHECK_PTR(out, "out");
+    return format_score(value, out);
+}
+
 int pr_graph_upload(pr_ctx *ctx, int64_t n, int64_t m, const int64_t *out_offsets, const int64_t *out_targets,
                     const int64_t *in_offsets, const int64_t *in_sources, pr_graph **out) {
     CHECK_PTR(ctx, "ctx");

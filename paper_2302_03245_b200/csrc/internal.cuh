@@ -205,6 +205,9 @@ int ensure_run_csr(Graph &r);
 int ensure_sched(Graph &g, int which);
 int ensure_units(Graph &g, int which, int64_t blocks, int nsec = 1);
 int load_edge_list_device(Ctx &ctx, const char *text, int64_t len, Graph **out);
+int rank_order(Ctx &ctx, const double *h_values, const int64_t *h_ids, int64_t n, int64_t k, int64_t *h_order);
+int write_ranking_csv(Ctx &ctx, const double *values, const int64_t *ids, int64_t n, const char *path);
+int format_score(double x, char *out);
 int graph_from_raw_ids(Ctx &ctx, const int64_t *src, const int64_t *dst, int64_t m, Graph **out);
 int build_from_device_edges(Ctx &ctx, int64_t n, const int64_t *d_src, const int64_t *d_dst,
                             int64_t m_raw, Graph **out);

@@ -25,6 +25,10 @@ Fixtures
               blank lines, '+' signs, 43-bit ids, no trailing newline, a
               seeded 20k-edge list; and malformed texts with the exception
               class and message.  ``--only edge_lists`` regenerates just this.
+  serialize.npz  write_ranking_csv (serialize.py:14-21) output bytes for
+              reference vectors on edge-list graphs with sparse original ids,
+              a uniform vector (all ties) and the C1 power vector.
+              ``--only serialize``.
 """
 
 from __future__ import annotations
@@ -151,10 +155,40 @@ def edge_lists(P) -> None:
     print("edge_lists.npz:", len(ok), "ok,", len(bad), "malformed")
 
 
+def serialize_cases(P) -> None:
+    import tempfile
+    from pushrank.serialize import write_ranking_csv
+    ok, _ = edge_list_texts()
+    cases = []
+    g = P.load_edge_list(ok[-1])                       # 3000 vertices, 40-bit ids
+    cfg = P.SolverConfig(threshold=1e-12)
+    cases.append((g, P.ifp1_run(g, P.classify(g), cfg)[0]))
+    cases.append((g, P.PageRankVector(values=np.full(g.n, 1.0 / g.n), algorithm="uniform", damping=0.85)))
+    g2 = P.load_edge_list(b"7 3\n3 1\n1 7\n9 9\n")
+    cases.append((g2, P.power_method(g2, cfg)[0]))
+    sys.path.insert(0, REPO)
+    from paper_2302_03245_b200 import synthetic
+    n, src, dst = synthetic.make("c1", seed=0)
+    g3 = P.from_edges(n, src, dst)
+    cases.append((g3, P.power_method(g3, P.SolverConfig(max_iterations=210))[0]))
+    out = {"count": np.int64(len(cases))}
+    for i, (graph, vec) in enumerate(cases):
+        with tempfile.NamedTemporaryFile(suffix=".csv", delete=False) as fh:
+            path = fh.name
+        write_ranking_csv(vec, graph, path)
+        with open(path, "rb") as fh:
+            out[f"c{i}_csv"] = np.frombuffer(fh.read(), np.uint8)
+        os.unlink(path)
+        out[f"c{i}_values"] = np.asarray(vec.values, np.float64)
+        out[f"c{i}_ids"] = np.asarray(graph.original_ids, np.int64)
+    np.savez_compressed(os.path.join(HERE, "serialize.npz"), **out)
+    print("serialize.npz:", len(cases), "cases")
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref-src", default="/tmp/refpkg/src")
-    ap.add_argument("--only", default=None, choices=["edge_lists"])
+    ap.add_argument("--only", default=None, choices=["edge_lists", "serialize"])
     args = ap.parse_args()
     ensure_reference(args.ref_src)
     import pushrank as P
@@ -164,7 +198,11 @@ def main() -> None:
     if args.only == "edge_lists":
         edge_lists(P)
         return
+    if args.only == "serialize":
+        serialize_cases(P)
+        return
     edge_lists(P)
+    serialize_cases(P)
 
     sys.path.insert(0, REPO)
     from paper_2302_03245_b200 import synthetic

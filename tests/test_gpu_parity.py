@@ -158,6 +158,29 @@ def test_load_edge_list_matches_reference():
     assert vec.values == pytest.approx([0.5, 0.5], abs=1e-10)
 
 
+def test_ranking_csv_matches_reference(tmp_path):
+    """write_ranking_csv (serialize.py:14-21): device ordering (score desc,
+    ties by original id) and native row writing, byte-identical to the
+    reference's file; ranking_order equals np.lexsort((ids, -values))."""
+    import os
+    from types import SimpleNamespace
+    from paper_2302_03245_b200 import serialize
+    d = np.load(os.path.join(os.path.dirname(__file__), "golden", "serialize.npz"))
+    for i in range(int(d["count"])):
+        vals, ids = d[f"c{i}_values"], d[f"c{i}_ids"]
+        g = SimpleNamespace(original_ids=ids)
+        vec = P.PageRankVector(values=vals, algorithm="x", damping=0.85)
+        path = tmp_path / f"r{i}.csv"
+        serialize.write_ranking_csv(vec, g, path)
+        assert path.read_bytes() == d[f"c{i}_csv"].tobytes(), i
+        assert np.array_equal(serialize.ranking_order(vals, g), np.lexsort((ids, -vals))), i
+        assert np.array_equal(serialize.ranking_order(vals, g, k=10), np.lexsort((ids, -vals))[:10]), i
+    # binary vector round trip (serialize.py:24-38)
+    vec = P.PageRankVector(values=d["c0_values"], algorithm="x", damping=0.85)
+    serialize.write_vector_binary(vec, tmp_path / "v.bin")
+    assert np.array_equal(serialize.read_vector_binary(tmp_path / "v.bin"), d["c0_values"])
+
+
 def test_rmat_device_generator_matches_numpy():
     from paper_2302_03245_b200 import _lib
     import ctypes

@@ -125,3 +125,18 @@ def test_edge_list_host_parse_matches_reference_errors():
     for i in range(int(d["n_ok"])):
         src, dst = _host_parse(d[f"ok{i}_text"].tobytes())
         assert src.size == int(d[f"ok{i}_raw"]), i
+
+
+def test_score_format_is_python_repr():
+    """Ranking CSV scores are written natively as Python repr(float)
+    (serialize.py:21): shortest round-trip digits, fixed notation for decimal
+    exponents -4..15, scientific otherwise."""
+    from paper_2302_03245_b200.serialize import format_score
+    rng = np.random.default_rng(7)
+    special = [0.0, -0.0, 1.0, -1.0, 0.1, 0.0001, 0.00001, 1e15, 1e16, 1.5e16, 123456789012345.0,
+               1234567890123456.0, 12345678901234567.0, 5e-324, 2.2250738585072014e-308, 1.7976931348623157e308,
+               1 / 3, 2 / 3, 0.15, 0.3, 1e-10, 9.999999999999999e-05, 0.00010000000000000009, 100.0, 1e22]
+    vals = special + list(rng.random(2000)) + list(rng.random(1000) * 1e-12) \
+        + list(10.0 ** rng.uniform(-300, 300, 2000)) + list(-(10.0 ** rng.uniform(-20, 20, 500)))
+    for v in vals:
+        assert format_score(v) == repr(float(v)), v
