@@ -1008,10 +1008,12 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     // round is bandwidth-bound: k_pull<true> streams the CSC (evict-first)
     // at 4 blocks/SM.  Otherwise it is latency-bound: k_pull<false> issues
     // each row's drain loads before its gathers, at 3 blocks/SM (the extra
-    // live registers).  Measured: C2 -9%, C4 -11%; C3 prefers the former.
+    // live registers).  Measured: C2 -9%, C4 -11%, C3 -1.4%; C5 prefers the former.
     const double ws = 4.0 * (double)g.sched[which].edges + 8.0 * (double)g.n + 44.0 * (double)g.sched[which].count;
     const double l2 = (double)(ctx.l2_bytes ? ctx.l2_bytes : (size_t)126 << 20);
-    const bool stream = ws > 0.6 * l2, prefetch = ws < 1.2 * l2;
+    const bool stream = ws > 0.6 * l2;
+    bool prefetch = ws < 4.0 * l2;   // C3 (1.9x L2) -1.4% with it, C5 (55x) +6%
+    if (const char *e = getenv("PUSHRANK_PREFETCH")) prefetch = atoi(e) != 0;
     const void *k_pull_fn = stream ? (prefetch ? (const void *)k_pull<true, true, false>
                                                : (const void *)k_pull<true, false, false>)
                                    : (prefetch ? (const void *)k_pull<false, true, false>
