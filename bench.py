@@ -176,9 +176,18 @@ def run_ours(args):
     from paper_2302_03245_b200 import _lib
     from paper_2302_03245_b200.graph import DeviceGraph
 
+    # PUSHRANK_DIST_BACKEND=gloo (functional check of the N > 1 path on a
+    # single-GPU box: host collectives, every rank on device 0); nccl otherwise
+    backend = os.environ.get("PUSHRANK_DIST_BACKEND", "nccl")
+    if world > 1 and backend == "gloo":
+        local = local % max(torch.cuda.device_count(), 1)
+        os.environ["PUSHRANK_DEVICE"] = str(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     t0 = time.perf_counter()
     if args.config == "c5":
@@ -302,38 +311,57 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
     from paper_2302_03245_b200 import distributed as D
     host = __import__("oracle").graph_arrays(g)
     part = D.partition_graph(host, world, rank, args.algo)
-    comm = D.Comm(device=torch.device("cuda", local))
+    comm = D.Comm(device=torch.device("cpu") if dist.get_backend() == "gloo" else torch.device("cuda", local))
+    # the partition is uploaded once (inputs resident in HBM for `value`);
+    # pr_part_init resets the round state of every solve
+    step = D.CudaLocalStep(part, DAMPING, XI, args.algo, device=local)
 
-    def solve():
-        step = D.CudaLocalStep(part, DAMPING, XI, args.algo, device=local)
-        vals, rows, info = D.run_partitioned(step, comm, part, args.algo, DAMPING, XI)
+    def solve(s):
+        vals, rows, info = D.run_partitioned(s, comm, part, args.algo, DAMPING, XI)
         return vals, info
 
     for _ in range(args.warmup):
-        solve()
-    times, info = [], None
+        solve(step)
+    # device time per rank (CUDA events on torch's stream, which also orders
+    # the library calls: each returns with its stream synchronised), max over
+    # ranks
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    info = None
     with ClockSampler(local) as clocks:
+        dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record()
         for _ in range(args.steps):
-            dist.barrier()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            vals, info = solve()
-            torch.cuda.synchronize()
-            dist.barrier()
-            times.append(time.perf_counter() - t0)
-    t = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
+            vals, info = solve(step)
+        ev1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    red_dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([ev0.elapsed_time(ev1) * 1e-3], dtype=torch.float64, device=red_dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_s = float(t.item())
     value = info["push_ops"] * args.steps / total_s / 1e9
+    # e2e: partition upload + solve + owned values back, every step
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(2):
+        s2 = D.CudaLocalStep(part, DAMPING, XI, args.algo, device=local)
+        solve(s2)
+        del s2
+    torch.cuda.synchronize()
+    te = torch.tensor([(time.perf_counter() - t0) / 2], dtype=torch.float64, device=red_dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_s = float(te.item())
     if rank == 0:
         line = {"metric": "GTEPS", "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": dict(config_desc(args, g.n, g.m), parallelism=f"vertex-range x{world}"),
                 "rounds": info["rounds"], "push_ops_per_step": info["push_ops"], "preprocess_s": preprocess_s,
-                "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": int(part.in_sources.nbytes +
-                                                                                  part.in_offsets.nbytes),
-                        "d2h_bytes_per_step": int(8 * part.owned),
+                "e2e": {"value": info["push_ops"] / e2e_s / 1e9, "unit": "GTEPS",
+                        "h2d_bytes_per_step": int(part.in_sources.nbytes + part.in_offsets.nbytes),
+                        "d2h_bytes_per_step": int(8 * part.owned), "ms_per_step": 1e3 * e2e_s,
                         "path": "per step: partition upload (pr_part_create) + rounds + owned values D2H"},
                 "gpu_launches": int(2 * (info["rounds"] + 2)), "clocks": clocks.summary(),
                 "note": "host-driven partitioned rounds; exchange = NCCL all-gather of shares per round"}

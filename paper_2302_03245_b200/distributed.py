@@ -132,12 +132,15 @@ class Comm:
         self.dist.all_gather_into_tensor(full, mine_view.clone() if full.device.type == "cpu" else mine_view)
 
     def allreduce_stats(self, ints: np.ndarray, floats: np.ndarray):
+        # one all-reduce per round: the integer counters ride in a float64
+        # tensor (exact below 2**53) after the float statistics
         t = self.torch
-        ti = t.tensor(ints, dtype=t.int64, device=self.device)
-        tf = t.tensor(floats, dtype=t.float64, device=self.device)
-        self.dist.all_reduce(ti)
-        self.dist.all_reduce(tf)
-        return ti.cpu().numpy(), tf.cpu().numpy()
+        buf = np.concatenate([np.asarray(floats, np.float64), np.asarray(ints, np.float64)])
+        tb = t.tensor(buf, dtype=t.float64, device=self.device)
+        self.dist.all_reduce(tb)
+        out = tb.cpu().numpy()
+        k = len(floats)
+        return np.rint(out[k:]).astype(np.int64), out[:k]
 
 
 def run_partitioned(step, comm, part: Partition, algorithm: str, damping: float, threshold: float,
