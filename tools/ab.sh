@@ -1,5 +1,5 @@
 #!/bin/bash
-# A/B of library variants on one box: tools_ab.sh "v1 v2 ..." "c2 c3" [extra bench args]
+# A/B of library variants on one box: tools/ab.sh "v1 v2 ..." "c2 c3" [extra bench args]
 # variant "base" = the in-tree library; others = build/var/lib_<v>.so
 for v in $1; do
   if [ "$v" = base ]; then L=""; else L=$PWD/build/var/lib_$v.so; fi

@@ -1,11 +1,12 @@
 """Phase timing of the e2e path (host graph -> upload -> preprocess -> solve -> D2H)."""
+import os
 import sys
 import time
 from types import SimpleNamespace
 
 import numpy as np
 
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2302_03245_b200 as P
 from paper_2302_03245_b200 import _lib, synthetic
 from paper_2302_03245_b200.graph import DeviceGraph

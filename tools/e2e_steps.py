@@ -1,7 +1,8 @@
 """Wall-clock breakdown of bench.py's e2e step (pinned host graph -> ifp2_run)."""
+import os
 import sys, time
 from types import SimpleNamespace
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 import paper_2302_03245_b200 as P

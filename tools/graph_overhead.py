@@ -1,8 +1,9 @@
 """Per-round launch overhead of the round-loop structures (pr_debug_graph)."""
 import ctypes
+import os
 import sys
 
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2302_03245_b200 import _lib
 
 L = _lib.load()

@@ -1,7 +1,8 @@
 """Edge-list ingest timing: device load_edge_list vs the host path the
 reference takes (pandas parse + numpy first-appearance remap), on C2 as text."""
+import os
 import sys, time
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2302_03245_b200 as P
 from paper_2302_03245_b200 import synthetic, _lib

@@ -1,5 +1,5 @@
 """Stall samples of one kernel per CUDA source line (needs -lineinfo and
---import-source on at capture): tools_ncu_src.py REP KERNEL [TOP]."""
+--import-source on at capture): tools/ncu_src.py REP KERNEL [TOP]."""
 import csv
 import subprocess
 import sys

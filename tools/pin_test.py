@@ -1,5 +1,6 @@
+import os
 import sys, time, gc
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_2302_03245_b200 import _lib
 _lib.context()

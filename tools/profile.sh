@@ -3,7 +3,7 @@
 #   bench lines (C2 default with e2e + cpu_baseline, reference arm, C3, C5),
 #   the ncu launch list of one C2 solve, --set full captures of the round
 #   kernels (C2) and of one C5 k_pull.  Each ncu command runs only after the
-#   same command exited 0 without ncu.  Usage: bash tools_profile.sh TAG
+#   same command exited 0 without ncu.  Usage: bash tools/profile.sh TAG
 set -u
 T=${1:-r01}
 O=gpurun_out/prof_$T

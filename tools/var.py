@@ -1,15 +1,15 @@
-"""Build a variant library with extra -D flags: tools_var.py NAME "-DX=1 -DY=2"
--> build/var/lib_NAME.so (used by tools_ab.sh through PUSHRANK_LIB)."""
+"""Build a variant library with extra -D flags: tools/var.py NAME "-DX=1 -DY=2"
+-> build/var/lib_NAME.so (used by tools/ab.sh through PUSHRANK_LIB)."""
 import os
 import subprocess
 import sys
 from concurrent.futures import ThreadPoolExecutor
 
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2302_03245_b200 import build as B  # noqa: E402
 
 name, defs = sys.argv[1], sys.argv[2].split()
-root = os.path.dirname(os.path.abspath(__file__))
+root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 odir = os.path.join(root, "build", "var", name)
 os.makedirs(odir, exist_ok=True)
 objs = [os.path.join(odir, os.path.basename(s)[:-3] + ".o") for s in B.SOURCES]
