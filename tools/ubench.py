@@ -1,5 +1,5 @@
 """Gather microbenchmarks on the C2 run layout (pr_debug_gather)."""
-import ctypes, sys
+import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2302_03245_b200 as P
 from paper_2302_03245_b200 import _lib, synthetic
