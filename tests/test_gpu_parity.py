@@ -347,6 +347,41 @@ def test_gauss_seidel_sections_parity(sections, monkeypatch, golden_corpus):
         assert np.max(np.abs(v2.values - golden_corpus[f"g{i}_ifp2_values"])) <= max(1e-10, 10 * XI * n), i
 
 
+def test_c3_full_size_parity():
+    """C3 (52 M edges): the fast IFP2 engine, which runs 2 Gauss-Seidel
+    sections per dense sweep at this size, against the round-synchronous
+    oracle -- L1 <= 1e-9, identical top-100, every dangling in-edge settled."""
+    n, src, dst = synthetic.make("c3", seed=0)
+    g = P.from_edges(n, src, dst)
+    ref = oracle.from_edges(n, src, dst)
+    cls = P.classify(g)
+    o = oracle.sync_simulate(ref, "ifp2", threshold=XI)
+    vec, tr = P.ifp2_run(P.preprocess_ifp2(g, cls), cfg())
+    assert np.abs(vec.values - o.values).sum() <= 1e-9
+    assert np.array_equal(top100(vec.values), top100(o.values))
+    assert tr.final.push_ops_dangling == cls.dangling_edge_count
+    assert tr.meta["rounds"] < o.iterations          # the sections cut rounds
+
+
+def test_c5_full_size_properties():
+    """C5 (R-MAT scale 26, 1.06 B edges; too large for the oracle): size-
+    independent properties of the fast IFP2 engine (4 Gauss-Seidel sections):
+    mass 1, m_d dangling pushes, agreement with 210 power iterations (L1 and
+    top-100), and the ranking order against numpy."""
+    from paper_2302_03245_b200 import serialize
+    dev = P.graph.DeviceGraph.rmat(26, 16, seed=0)
+    g = P.graph.Graph(dev, raw_edge_count=16 << 26, name="c5")
+    cls = P.classify(g)
+    vec, tr = P.ifp2_run(P.preprocess_ifp2(g, cls), cfg())
+    assert abs(vec.values.sum() - 1.0) <= 1e-12
+    assert tr.final.push_ops_dangling == cls.dangling_edge_count
+    pw, _ = P.power_method(g, P.SolverConfig(max_iterations=210))
+    assert np.abs(vec.values - pw.values).sum() <= 1e-8
+    assert np.array_equal(top100(vec.values), top100(pw.values))
+    order = serialize.ranking_order(vec.values, None, k=1000)
+    assert np.array_equal(order, np.lexsort((np.arange(g.n), -vec.values))[:1000])
+
+
 # ------------------------------------------------------------ known answers (reference tests)
 
 def test_known_answers():
