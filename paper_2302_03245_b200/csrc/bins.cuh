@@ -10,8 +10,11 @@
 //   * thread unit -- rows with d <= THREAD_DEG; thread t takes rows t, t+256,
 //                    ... (coalesced drains), 8 index loads then 8 gathers.
 // Rows of a unit have near-equal degree (sorted), so warps carry uniform
-// work; units are dealt round-robin to a persistent grid.  Every summation
-// order is fixed by the schedule: results are run-to-run deterministic.
+// work.  Blocks of a persistent grid claim units dynamically (an atomic per
+// unit, issued at the start of the previous one); a launch covers the unit
+// range of one Gauss-Seidel section.  Every summation order is fixed by the
+// schedule (row sums do not depend on which block claims a unit): the vector
+// results are run-to-run deterministic.
 #pragma once
 
 #include "internal.cuh"

@@ -9,18 +9,23 @@
 // the dangling vertices once at the end (engines.py:269-289); fp-full (sync
 // twin only) scans everything and reserves 1-c.
 //
-// Fast engine (PR_MODE_AUTO/PULL/PUSH): one launch per round.
+// Fast engine (PR_MODE_AUTO/PULL/PUSH), on the run layout (graph.cu):
 //   * pull round (dense): CSC gather over the destination set D (vertices
-//     that can receive mass), degree-binned thread / 8-lane / warp / CTA per
-//     destination, fixed-order group reductions (deterministic, no
-//     atomics), double-buffered shares s, the next state's drain fused into
-//     the epilogue;
+//     that can receive mass), degree bins (bins.cuh: hub slices per block,
+//     warp rows, thread rows) dealt as equal-cost units to a persistent grid,
+//     fixed-order reductions (deterministic, no atomics), double-buffered
+//     shares s, the next state's drain fused into the epilogue.  k_pull<
+//     STREAM, PREFETCH, GS>: evict-first index loads when the round overflows
+//     L2; drain inputs loaded ahead of the gathers when it is latency-bound;
+//     on large IFP2 graphs a sweep is cut into Gauss-Seidel sections (one
+//     launch each) that read the new shares of earlier sections;
 //   * push round (sparse tail): frontier scatter with red.global.add.f64,
 //     then a scan kernel over D that fuses the drain;
 //   * every round kernel ends with a last-block reduction of per-block
 //     statistics (trace row, convergence test, next-mode choice) that also
-//     drives the CUDA-graph conditional WHILE/SWITCH nodes, so the whole
-//     solve is one graph launch with no host round trips.
+//     drives the CUDA-graph conditionals (nested WHILE loops over unrolled
+//     kernel slots), so the whole solve is one graph launch with no host
+//     round trips.
 // Exact engine (PR_MODE_EXACT): thread per vertex, sequential ascending
 // source sums with explicit _rn intrinsics -- bit-identical reserved/h to
 // sync_simulate's np.bincount order.
