@@ -216,6 +216,19 @@ int pr_power_observed(pr_graph *g, double damping, int64_t iterations, double to
                       int64_t *converged, int (*on_iterate)(void *user, int64_t k, const double *pi),
                       void *user, pr_run_result *result);
 
+/* ---- ERR harness (bench.py:90-112, 255-275) ------
+ * max_relative_error: ERR = max_v |est_v - ref_v| / ref_v, its first argmax
+ * (worst vertex), the L1 error, and the number of ref_v <= 0 (the reference
+ * raises ValueError on any; the caller does).  d_est / d_ref are device
+ * vectors of n doubles. */
+int pr_error_report(pr_ctx *ctx, const double *d_est, const double *d_ref, int64_t n,
+                    double *max_rel, double *l1, int64_t *worst, int64_t *nonpositive);
+/* _power_iterations_to_target (bench.py:255-275): power iterations (limit at
+ * most) with the ERR of every iterate against d_ref checked on the device;
+ * *hit = the first k+1 whose iterate has ERR < target_err, or 0 if none. */
+int pr_power_to_target(pr_graph *g, double damping, int64_t limit, const double *personalization,
+                       const double *d_ref, double target_err, int64_t *hit);
+
 /* ---- synthetic inputs ---------------------------------------------------
  * Device R-MAT sampler, bit-identical to synthetic.rmat_edges (counter
  * based splitmix64): samples first..first+count into device int64 arrays. */

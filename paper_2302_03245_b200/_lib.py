@@ -106,6 +106,9 @@ SIGNATURES = {
                                 ctypes.POINTER(RunResult)]),
     "pr_power_observed": (ctypes.c_int, [c_vp, c_f64, c_i64, c_f64, c_f64, c_vp, c_vp, c_vp, c_vp,
                                          POWER_CB, c_vp, ctypes.POINTER(RunResult)]),
+    "pr_error_report": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, ctypes.POINTER(c_f64), ctypes.POINTER(c_f64),
+                                       _PI64, _PI64]),
+    "pr_power_to_target": (ctypes.c_int, [c_vp, c_f64, c_i64, c_vp, c_vp, c_f64, _PI64]),
     "pr_rmat_generate": (ctypes.c_int, [c_vp, ctypes.c_int, c_i64, c_f64, c_f64, c_f64,
                                         ctypes.c_uint64, c_i64, c_i64, c_vp, c_vp]),
     "pr_graph_rmat": (ctypes.c_int, [c_vp, ctypes.c_int, c_i64, c_f64, c_f64, c_f64, ctypes.c_uint64,
@@ -143,7 +146,10 @@ def load():
                     f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
             L = ctypes.CDLL(LIB_PATH)
             for name, (res, args) in SIGNATURES.items():
-                fn = getattr(L, name)
+                # an A/B variant library (PUSHRANK_LIB) may predate newer entry points
+                fn = getattr(L, name, None) if os.environ.get("PUSHRANK_LIB") else getattr(L, name)
+                if fn is None:
+                    continue
                 fn.restype = res
                 fn.argtypes = args
             _lib = L

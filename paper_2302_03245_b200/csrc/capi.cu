@@ -412,6 +412,27 @@ int pr_power_observed(pr_graph *g, double damping, int64_t iterations, double to
                         on_iterate, user, result);
 }
 
+int pr_error_report(pr_ctx *ctx, const double *d_est, const double *d_ref, int64_t n, double *max_rel, double *l1,
+                    int64_t *worst, int64_t *nonpositive) {
+    CHECK_PTR(ctx, "ctx");
+    CHECK_PTR(d_est, "est");
+    CHECK_PTR(d_ref, "ref");
+    PR_TRY(set_device(ctx->c));
+    return error_report(ctx->c, d_est, d_ref, n, max_rel, l1, worst, nonpositive);
+}
+
+int pr_power_to_target(pr_graph *g, double damping, int64_t limit, const double *personalization,
+                       const double *d_ref, double target_err, int64_t *hit) {
+    CHECK_PTR(g, "graph");
+    CHECK_PTR(d_ref, "ref");
+    CHECK_PTR(hit, "hit");
+    PR_TRY(set_device(*g->g->ctx));
+    *hit = 0;
+    if (limit <= 0) return PR_OK;
+    return power_device(*g->g, damping, limit, 0.0, 1e-10, personalization, nullptr, nullptr, nullptr, nullptr,
+                        nullptr, nullptr, d_ref, target_err, hit);
+}
+
 int pr_rmat_generate(pr_ctx *ctx, int scale, int64_t edge_factor, double a, double b, double c, uint64_t seed,
                      int64_t first, int64_t count, int64_t *d_src, int64_t *d_dst) {
     CHECK_PTR(ctx, "ctx");

@@ -219,7 +219,10 @@ int run_rounds(Graph &g, const pr_run_params &p, double *d_values, double *d_res
                int64_t row_cap, pr_run_result *res);
 int power_device(Graph &g, double damping, int64_t iterations, double tolerance, double threshold,
                  const double *h_personalization, double *h_pi, double *h_deltas, int64_t *h_converged,
-                 int (*on_iterate)(void *, int64_t, const double *), void *user, pr_run_result *res);
+                 int (*on_iterate)(void *, int64_t, const double *), void *user, pr_run_result *res,
+                 const double *d_ref = nullptr, double target_err = 0.0, int64_t *hit = nullptr);
+int error_report(Ctx &ctx, const double *d_est, const double *d_ref, int64_t n, double *max_rel, double *l1,
+                 int64_t *worst, int64_t *nonpositive);
 
 constexpr int TILE = 256;   // edges per warp tile (long rows are cut into TILE chunks)
 constexpr int CSC_PAD = 1024;  // int32 padding past the compacted CSC for vector loads

@@ -9,6 +9,8 @@
 // Two launches per iteration: gather (+ sum of nxt) and normalise (+ delta,
 // converged count, next z, next dangling sum); both end with a
 // deterministic last-block reduction that also drives the graph's WHILE node.
+#include <algorithm>
+#include <climits>
 #include <cstring>
 #include <vector>
 
@@ -26,6 +28,8 @@ struct PowCtl {
     double restart;          // restart coefficient for the current iteration
     double delta;
     unsigned long long unit_ctr;  // gather-unit dispatch counter (bins.cuh)
+    unsigned long long err_bits;  // max relative error vs ref of this iteration (bits of a double >= 0)
+    int64_t hit;                  // first k+1 whose iterate beat target_err (0: none)
 };
 
 struct PowArgs {
@@ -43,6 +47,8 @@ struct PowArgs {
     Partial *partials;
     PowCtl *ctl;
     double c, tolerance, threshold, uniform_p;
+    const double *ref;       // target mode (bench.py:255-275): reference vector or null
+    double target_err;
     int64_t iterations;
     int32_t use_graph;
     cudaGraphConditionalHandle h_loop;
@@ -132,6 +138,7 @@ __global__ void __launch_bounds__(256) k_pw_norm(PowArgs A) {
     double total = A.ctl->total;
     Partial p;
     zero(p);
+    double err = 0.0;                                   // max |pi - ref| / ref (bench.py:266)
     // grid-stride over one resident wave (few partials for the last block)
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < A.n; v += (int64_t)gridDim.x * blockDim.x) {
         double x = __ddiv_rn(A.nxt[v], total);
@@ -141,6 +148,16 @@ __global__ void __launch_bounds__(256) k_pw_norm(PowArgs A) {
         A.pi[v] = x;
         A.z[v] = z_of(A, v, x);
         if (A.deg[v] == 0) p.above += x;                // dangling mass for the next restart
+        if (A.ref) {
+            const double r = A.ref[v];
+            err = fmax(err, __ddiv_rn(fabs(x - r), r));
+        }
+    }
+    if (A.ref) {
+        // max is order-free: non-negative doubles order as their bit patterns
+        for (int o = 16; o > 0; o >>= 1) err = fmax(err, __shfl_xor_sync(0xffffffffu, err, o));
+        if ((threadIdx.x & 31) == 0 && err > 0.0)
+            atomicMax(&A.ctl->err_bits, (unsigned long long)__double_as_longlong(err));
     }
     pow_finish(A, p, [&](const Partial &acc) {
         PowCtl *c = A.ctl;
@@ -151,6 +168,15 @@ __global__ void __launch_bounds__(256) k_pw_norm(PowArgs A) {
         c->restart = __dadd_rn(__dmul_rn(A.c, acc.above), 1.0 - A.c);
         c->k = k + 1;
         bool stop = (k + 1 >= A.iterations) || (A.tolerance > 0.0 && acc.l1 < A.tolerance);
+        if (A.ref) {
+            // bench.py:263-268: the probe stops at the first iterate below the target
+            const double e = __longlong_as_double((long long)__ldcg(&c->err_bits));
+            c->err_bits = 0;
+            if (e < A.target_err) {
+                c->hit = k + 1;
+                stop = true;
+            }
+        }
         c->done = stop;
         if (A.use_graph) cudaGraphSetConditional(A.h_loop, stop ? 0u : 1u);
     });
@@ -171,7 +197,8 @@ static int add_node(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t 
 
 int power_device(Graph &g, double damping, int64_t iterations, double tolerance, double threshold,
                  const double *h_p, double *h_pi, double *h_deltas, int64_t *h_conv,
-                 int (*on_iterate)(void *, int64_t, const double *), void *user, pr_run_result *res) {
+                 int (*on_iterate)(void *, int64_t, const double *), void *user, pr_run_result *res,
+                 const double *d_ref, double target_err, int64_t *hit) {
     if (!(damping > 0.0 && damping < 1.0)) return fail(PR_ERR_ARG, "damping must be in (0,1)");
     if (iterations < 0) return fail(PR_ERR_ARG, "max_iterations must be non-negative");
     Ctx &ctx = *g.ctx;
@@ -230,6 +257,8 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
     A.threshold = threshold;
     A.uniform_p = 1.0 / (double)n;
     A.iterations = iterations;
+    A.ref = d_ref;
+    A.target_err = target_err;
     if (h_p) PR_CUDA(cudaMemcpyAsync((void *)A.p, h_p, 8 * n, cudaMemcpyHostToDevice, st));
     PR_CUDA(cudaMemsetAsync(A.ctl, 0, sizeof(PowCtl), st));
     unsigned g_all = grid_for(n, 256), g_gather = (unsigned)blk;
@@ -302,6 +331,7 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
     PowCtl hc;
     PR_CUDA(cudaMemcpy(&hc, A.ctl, sizeof(hc), cudaMemcpyDeviceToHost));
     int64_t k = hc.k;
+    if (hit) *hit = hc.hit;
     if (h_pi) PR_CUDA(cudaMemcpy(h_pi, A.pi, 8 * n, cudaMemcpyDeviceToHost));
     if (h_deltas && k) PR_CUDA(cudaMemcpy(h_deltas, A.deltas, 8 * k, cudaMemcpyDeviceToHost));
     if (h_conv && k) PR_CUDA(cudaMemcpy(h_conv, A.conv, 8 * k, cudaMemcpyDeviceToHost));
@@ -316,6 +346,88 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
         res->round_ms = ms;
         res->bytes_moved = (double)k * (12.0 * (double)g.m + 32.0 * (double)n);
     }
+    return PR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// max_relative_error (bench.py:90-112): ERR = max_v |est_v - ref_v| / ref_v,
+// its first argmax (np.argmax), the L1 error, and the count of ref_v <= 0
+// (the reference raises on any).  Per-element arithmetic is the reference's
+// (one subtraction, fabs, one division), so ERR and the worst vertex are
+// bit-identical for equal inputs; the L1 sum runs in a fixed order (a fixed
+// grid, then one block over the block partials), not numpy's pairwise order.
+struct ErrPart {
+    double rel, l1;
+    int64_t worst, nonpos;
+};
+
+__device__ __forceinline__ void err_merge(ErrPart &a, const ErrPart &b) {
+    // larger error wins; ties go to the smaller index (np.argmax is the first)
+    if (b.rel > a.rel || (b.rel == a.rel && b.worst < a.worst)) {
+        a.rel = b.rel;
+        a.worst = b.worst;
+    }
+    a.l1 += b.l1;
+    a.nonpos += b.nonpos;
+}
+
+__device__ void err_block(ErrPart &p) {
+    __shared__ ErrPart wp[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) {
+        ErrPart q;
+        q.rel = __shfl_down_sync(0xffffffffu, p.rel, o);
+        q.l1 = __shfl_down_sync(0xffffffffu, p.l1, o);
+        q.worst = __shfl_down_sync(0xffffffffu, p.worst, o);
+        q.nonpos = __shfl_down_sync(0xffffffffu, p.nonpos, o);
+        if (lane + o < 32) err_merge(p, q);
+    }
+    __syncthreads();
+    if (lane == 0) wp[wid] = p;
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) err_merge(p, wp[w]);
+}
+
+__global__ void __launch_bounds__(256) k_err(const double *est, const double *ref, int64_t n, ErrPart *parts) {
+    ErrPart p{0.0, 0.0, INT64_MAX, 0};
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const double r = ref[v], d = fabs(est[v] - r);
+        const double rel = __ddiv_rn(d, r);
+        if (rel > p.rel || p.worst == INT64_MAX) {
+            p.rel = rel;
+            p.worst = v;
+        }
+        p.l1 += d;
+        p.nonpos += r <= 0.0 ? 1 : 0;
+    }
+    err_block(p);
+    if (threadIdx.x == 0) parts[blockIdx.x] = p;
+}
+
+__global__ void __launch_bounds__(256) k_err_final(ErrPart *parts, int nb) {
+    ErrPart p{0.0, 0.0, INT64_MAX, 0};
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) err_merge(p, parts[b]);
+    err_block(p);
+    if (threadIdx.x == 0) parts[nb] = p;
+}
+
+int error_report(Ctx &ctx, const double *d_est, const double *d_ref, int64_t n, double *max_rel, double *l1,
+                 int64_t *worst, int64_t *nonpositive) {
+    if (n <= 0) return fail(PR_ERR_ARG, "empty vectors");
+    const int nb = (int)std::min<int64_t>((int64_t)ctx.sm_count * 4, (n + 255) / 256);
+    PR_TRY(ensure(ctx.scratch, sizeof(ErrPart) * (nb + 1)));
+    ErrPart *parts = ctx.scratch.as<ErrPart>();
+    k_err<<<nb, 256, 0, ctx.stream>>>(d_est, d_ref, n, parts);
+    k_err_final<<<1, 256, 0, ctx.stream>>>(parts, nb);
+    PR_CUDA(cudaGetLastError());
+    ErrPart h;
+    PR_CUDA(cudaMemcpyAsync(&h, parts + nb, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
+    PR_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (max_rel) *max_rel = h.rel;
+    if (l1) *l1 = h.l1;
+    if (worst) *worst = h.worst;
+    if (nonpositive) *nonpositive = h.nonpos;
     return PR_OK;
 }
 

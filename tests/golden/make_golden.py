@@ -25,6 +25,11 @@ Fixtures
               blank lines, '+' signs, 43-bit ids, no trailing newline, a
               seeded 20k-edge list; and malformed texts with the exception
               class and message.  ``--only edge_lists`` regenerates just this.
+  harness.npz the ERR harness (bench.py:90-329) on C1 and the acceptance
+              graph: the 210-iteration reference vector, ERR reports of
+              fixed estimates, _power_iterations_to_target hits, sweep_xi
+              errors of the deterministic engines, compare_algorithms
+              settings, and formatted CSV rows.  ``--only harness``.
   serialize.npz  write_ranking_csv (serialize.py:14-21) output bytes for
               reference vectors on edge-list graphs with sparse original ids,
               a uniform vector (all ties) and the C1 power vector.
@@ -185,10 +190,61 @@ def serialize_cases(P) -> None:
     print("serialize.npz:", len(cases), "cases")
 
 
+HARNESS_TARGETS = (1e-2, 1e-3, 1e-4, 1e-6, 1e-8, 1e-10, 1e-13)
+HARNESS_XIS = (1e-4, 1e-6, 1e-8)
+
+
+def harness_cases(P) -> None:
+    from pushrank import bench as B
+    sys.path.insert(0, REPO)
+    from paper_2302_03245_b200 import synthetic
+
+    out = {}
+    n, src, dst = synthetic.make("c1", seed=0)
+    graphs = [("c1", P.from_edges(n, src, dst, name="c1"))]
+    from pushrank import synth
+    graphs.append(("synth42", synth.generate(10_000, 100_000, dangling_fraction=0.2, seed=42)))
+    for name, g in graphs:
+        pre = f"{name}_"
+        cfg = P.SolverConfig()
+        ref = B.reference_vector(g, cfg)
+        out[pre + "ref"] = ref.values
+        if name == "synth42":
+            out[pre + "src"] = np.repeat(np.arange(g.n), np.diff(g.out_offsets)).astype(np.int32)
+            out[pre + "dst"] = np.asarray(g.out_targets, np.int32)
+            out[pre + "n"] = np.int64(g.n)
+        # ERR of fixed estimates (the reference's own ifp1 / spi-20 vectors)
+        cls = P.classify(g)
+        est1, _ = P.ifp1_run(g, cls, cfg.with_threshold(1e-6), sample_every=float("inf"))
+        est2, _ = P.power_method(g, P.SolverConfig(max_iterations=20))
+        for k, est in (("ifp1", est1), ("spi20", est2)):
+            r = B.max_relative_error(est, ref)
+            out[pre + k + "_est"] = est.values
+            out[pre + k + "_err"] = np.array([r.max_relative_error, r.l1_error])
+            out[pre + k + "_worst"] = np.int64(r.worst_vertex)
+        hits = [B._power_iterations_to_target(g, cfg, ref, t) for t in HARNESS_TARGETS]
+        out[pre + "targets"] = np.array(HARNESS_TARGETS)
+        out[pre + "hits"] = np.array([-1 if h is None else h for h in hits], np.int64)
+        rows = B.sweep_xi(g, ["sync-ifp1", "sync-ifp2", "spi"], HARNESS_XIS, workers=1, reps=1)
+        out[pre + "sweep_err"] = np.array([r.err for r in rows])
+        out[pre + "sweep_samples"] = np.array([r.samples for r in rows], np.int64)
+        cmp_rows = B.compare_algorithms(g, 1e-4, workers=2, reps=1,
+                                        algorithms=("spi", "mpi", "sync-ifp1", "sync-ifp2"))
+        out[pre + "compare_setting"] = np.array([r.setting for r in cmp_rows])
+        out[pre + "compare_qualified"] = np.array([r.qualified for r in cmp_rows])
+    row = B.SweepRow("d", "ifp2", 1e-6, 4, 1.2345678901234567e-05, 0.1234567, 0.5, 12, True)
+    crow = B.ComparisonRow("d", "spi", 1e-4, 3.3e-05, 0.25, 0.125, "iterations=42", True, 2)
+    urow = B.ComparisonRow("d", "ifp1", 1e-4, float("nan"), float("nan"), 0.1, "unreached", False)
+    out["csv_rows"] = np.array([repr(row.as_csv_row()), repr(crow.as_csv_row()), repr(urow.as_csv_row())])
+    out["slope"] = np.float64(B.fit_loglog_slope([1e-4, 1e-6, 1e-8], [0.01, 0.1, 0.9]))
+    np.savez_compressed(os.path.join(HERE, "harness.npz"), **out)
+    print("harness.npz")
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref-src", default="/tmp/refpkg/src")
-    ap.add_argument("--only", default=None, choices=["edge_lists", "serialize"])
+    ap.add_argument("--only", default=None, choices=["edge_lists", "serialize", "harness"])
     args = ap.parse_args()
     ensure_reference(args.ref_src)
     import pushrank as P
@@ -201,8 +257,12 @@ def main() -> None:
     if args.only == "serialize":
         serialize_cases(P)
         return
+    if args.only == "harness":
+        harness_cases(P)
+        return
     edge_lists(P)
     serialize_cases(P)
+    harness_cases(P)
 
     sys.path.insert(0, REPO)
     from paper_2302_03245_b200 import synthetic
