@@ -182,7 +182,10 @@ def run_ours(args):
     if world > 1 and backend == "gloo":
         local = local % max(torch.cuda.device_count(), 1)
         os.environ["PUSHRANK_DEVICE"] = str(local)
-    if world > 1:
+    # PUSHRANK_PARTITIONED=1 (under torchrun) runs the partitioned path even
+    # at one rank: the cost of the partitioned rounds against the engine
+    partitioned = world > 1 or os.environ.get("PUSHRANK_PARTITIONED", "0") == "1"
+    if partitioned:
         import torch.distributed as dist
         if backend == "gloo":
             dist.init_process_group("gloo")
@@ -201,7 +204,7 @@ def run_ours(args):
     cls = P.classify(g)
     pg = P.preprocess_ifp2(g, cls)
     preprocess_s = time.perf_counter() - t0
-    if world > 1:
+    if partitioned:
         return run_partitioned_bench(args, g, rank, world, local, preprocess_s)
     dev = g.dev
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -309,32 +312,36 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
     import torch
     import torch.distributed as dist
     from paper_2302_03245_b200 import distributed as D
-    host = __import__("oracle").graph_arrays(g)
-    part = D.partition_graph(host, world, rank, args.algo)
+    # partitions of the engines' run layout (hot sources at low ids)
+    order = D.run_order(np.diff(g.out_offsets), np.diff(g.in_offsets))
+    part = D.partition_graph(g, world, rank, args.algo, order=order)
     comm = D.Comm(device=torch.device("cpu") if dist.get_backend() == "gloo" else torch.device("cuda", local))
     # the partition is uploaded once (inputs resident in HBM for `value`);
-    # pr_part_init resets the round state of every solve
-    step = D.CudaLocalStep(part, DAMPING, XI, args.algo, device=local)
+    # pr_part_init resets the round state of every solve.  Fast local step
+    # (binned gather) with the rounds, all-gathers and statistics all-reduces
+    # queued on the library stream (statistics read back every 8 rounds)
+    step = D.CudaLocalStep(part, DAMPING, XI, args.algo, device=local, fast=True)
 
-    def solve(s):
-        vals, rows, info = D.run_partitioned(s, comm, part, args.algo, DAMPING, XI)
+    def solve(s, host_values=False):
+        vals, rows, info = D.run_partitioned_queued(s, comm, part, args.algo, DAMPING, XI, batch=8,
+                                                    host_values=host_values)
         return vals, info
 
     for _ in range(args.warmup):
         solve(step)
-    # device time per rank (CUDA events on torch's stream, which also orders
-    # the library calls: each returns with its stream synchronised), max over
-    # ranks
+    # device time per rank: CUDA events on the library stream, where the
+    # rounds and their collectives are queued; max over ranks
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    lib_stream = step.stream
     info = None
     with ClockSampler(local) as clocks:
         dist.barrier()
         torch.cuda.synchronize()
-        ev0.record()
+        ev0.record(lib_stream)
         for _ in range(args.steps):
             vals, info = solve(step)
-        ev1.record()
+        ev1.record(lib_stream)
         torch.cuda.synchronize()
         dist.barrier()
     red_dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
@@ -346,8 +353,8 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
     dist.barrier()
     t0 = time.perf_counter()
     for _ in range(2):
-        s2 = D.CudaLocalStep(part, DAMPING, XI, args.algo, device=local)
-        solve(s2)
+        s2 = D.CudaLocalStep(part, DAMPING, XI, args.algo, device=local, fast=True)
+        solve(s2, host_values=True)
         del s2
     torch.cuda.synchronize()
     te = torch.tensor([(time.perf_counter() - t0) / 2], dtype=torch.float64, device=red_dev)
@@ -364,7 +371,9 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
                         "d2h_bytes_per_step": int(8 * part.owned), "ms_per_step": 1e3 * e2e_s,
                         "path": "per step: partition upload (pr_part_create) + rounds + owned values D2H"},
                 "gpu_launches": int(2 * (info["rounds"] + 2)), "clocks": clocks.summary(),
-                "note": "host-driven partitioned rounds; exchange = NCCL all-gather of shares per round"}
+                "note": ("partitioned rounds queued on the device (statistics read back every 8 rounds); "
+                         "local step = binned dense-round gather (k_part_pull); exchange = all-gather of "
+                         "shares + all-reduce of 9 statistics per round")}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 

@@ -258,6 +258,19 @@ int pr_part_create(pr_ctx *ctx, int64_t owned, int64_t slot, const int64_t *in_o
 int pr_part_init(pr_part *p, double *d_shares_mine, int64_t *ints, double *floats);
 int pr_part_round(pr_part *p, const double *d_shares_full, double *d_shares_mine, int64_t *ints,
                   double *floats);
+/* Device-resident forms for a queued round loop (no host synchronisation):
+ * d_stats receives the 9 statistics as doubles {h_l1, active_mass,
+ * nd_active_mass, active, work, push_ops, push_ops_dangling, converged_all,
+ * converged_scan}, ready for an in-place device all-reduce.  fast = 1 runs
+ * the single-GPU dense-round gather (degree-binned schedule of the
+ * receiving rows, deterministic but not ascending-source order); fast = 0
+ * the exact ascending-source sums of pr_part_round.  Work is queued on the
+ * library stream (pr_part_stream), which the caller orders its collectives
+ * on. */
+int pr_part_init_device(pr_part *p, double *d_shares_mine, double *d_stats);
+int pr_part_round_device(pr_part *p, const double *d_shares_full, double *d_shares_mine, int32_t fast,
+                         double *d_stats);
+int pr_part_stream(pr_part *p, void **stream);
 int pr_part_settle_shares(pr_part *p, double *d_x_mine);
 int pr_part_settle(pr_part *p, const double *d_x_full, int64_t *settled, int64_t *ints, double *floats);
 int pr_part_total(pr_part *p, int32_t include_pending, double *total);

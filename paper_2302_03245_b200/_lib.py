@@ -117,6 +117,9 @@ SIGNATURES = {
                                        c_i32, c_f64, c_f64, _PP]),
     "pr_part_init": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "pr_part_round": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "pr_part_init_device": (ctypes.c_int, [c_vp, c_vp, c_vp]),
+    "pr_part_round_device": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_vp]),
+    "pr_part_stream": (ctypes.c_int, [c_vp, _PP]),
     "pr_part_settle_shares": (ctypes.c_int, [c_vp, c_vp]),
     "pr_part_settle": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pr_part_total": (ctypes.c_int, [c_vp, c_i32, ctypes.POINTER(c_f64)]),

@@ -57,6 +57,9 @@ int part_total(Part &P, int include_h, double *total);
 int part_export(Part &P, double *reserved, double *pending);
 void part_destroy(Part *P);
 Ctx &part_ctx(Part &P);
+void *part_stream(Part &P);
+int part_init_device(Part &P, double *d_s_mine, double *d_stats9);
+int part_round_device(Part &P, const double *d_s_full, double *d_s_mine, int fast, double *d_stats9);
 
 static int set_device(Ctx &ctx) {
     PR_CUDA(cudaSetDevice(ctx.device));
@@ -548,6 +551,23 @@ int pr_part_init(pr_part *p, double *d_shares_mine, int64_t *ints, double *float
 int pr_part_round(pr_part *p, const double *d_shares_full, double *d_shares_mine, int64_t *ints, double *floats) {
     PART_ENTER(p);
     return part_round(*p->p, d_shares_full, d_shares_mine, ints, floats);
+}
+int pr_part_init_device(pr_part *p, double *d_shares_mine, double *d_stats) {
+    PART_ENTER(p);
+    CHECK_PTR(d_stats, "stats");
+    return part_init_device(*p->p, d_shares_mine, d_stats);
+}
+int pr_part_round_device(pr_part *p, const double *d_shares_full, double *d_shares_mine, int32_t fast,
+                         double *d_stats) {
+    PART_ENTER(p);
+    CHECK_PTR(d_stats, "stats");
+    return part_round_device(*p->p, d_shares_full, d_shares_mine, fast, d_stats);
+}
+int pr_part_stream(pr_part *p, void **stream) {
+    PART_ENTER(p);
+    CHECK_PTR(stream, "stream");
+    *stream = part_stream(*p->p);
+    return PR_OK;
 }
 int pr_part_settle_shares(pr_part *p, double *d_x_mine) {
     PART_ENTER(p);

@@ -203,6 +203,8 @@ int count_dangling(Graph &g);
 int ensure_run_layout(Graph &g);
 int ensure_run_csr(Graph &r);
 int ensure_sched(Graph &g, int which);
+// sort the sources of every CSC row ascending (in place; segmented radix sort)
+int sort_csc_rows(Ctx &ctx, const DevBuf &in_off, DevBuf &in_src, int64_t n, int64_t m);
 int ensure_units(Graph &g, int which, int64_t blocks, int nsec = 1);
 int load_edge_list_device(Ctx &ctx, const char *text, int64_t len, Graph **out);
 int rank_order(Ctx &ctx, const double *h_values, const int64_t *h_ids, int64_t n, int64_t k, int64_t *h_order);

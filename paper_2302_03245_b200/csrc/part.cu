@@ -11,13 +11,40 @@
 //   settle -- IFP2: reserved_d = h_d + sum x_full[u] over d's sources
 // Statistics are reduced per block and then by one block in fixed order
 // (deterministic) and returned to the host, which all-reduces them.
+//
+// Two forms of the round:
+//   exact -- thread per owned vertex, sequential ascending-source sums: the
+//            summation order of the single-GPU exact engine and np.bincount,
+//            so partitions are bit-identical to sync_simulate (tests);
+//   fast  -- the single-GPU dense-round gather (bins.cuh) over a pull
+//            schedule of the partition's receiving rows (sched.cu: rows by
+//            descending in-degree, hub chunks / warp rows / thread rows,
+//            equal-cost units for a persistent grid), then the owned
+//            vertices outside it.  Summation order is fixed by the schedule
+//            (deterministic run to run), not ascending.
+// The *_device entry points leave the statistics on the device (9 doubles:
+// l1, above, nd_above, nact, work, push_ops, push_dang, conv_all,
+// conv_scan) and never synchronise, so the caller can queue rounds and
+// their collectives back to back on the library stream.
 #include <cstring>
 #include <vector>
 
 #include "internal.cuh"
 #include "reduce.cuh"
+#include "bins.cuh"
+#include "cubutil.cuh"
+
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 namespace pr {
+
+// an owned vertex that is not a row of the pull schedule
+struct OutsideRow {
+    const int64_t *in_off;
+    const uint8_t *recv;
+    __host__ __device__ bool operator()(int32_t v) const { return !(recv[v] && in_off[v + 1] > in_off[v]); }
+};
 
 struct Part {
     Ctx *ctx;
@@ -26,6 +53,17 @@ struct Part {
     double c, xi;
     DevBuf in_off, in_src, deg, row_len, dtc, dang, recv;   // int64 offsets, int32 ids/degrees, uint8 flags
     DevBuf h, reserved, act, partials, stats;
+    // fast form: the partition as a Graph of `owned` rows (local ids) whose
+    // sources are padded global ids, and its pull schedule
+    Graph *sg = nullptr;
+    int which = 0;            // schedule: 0 in-degree > 0 (IFP1), 1 and non-dangling (IFP2)
+    int64_t blocks = 0;       // persistent pull grid
+    bool stream_csc = false;  // evict-first index loads (round working set > 0.6 L2)
+    bool prefetch = false;    // drain inputs ahead of the gathers (round working set < 4 L2)
+    DevBuf outside;           // int32: owned vertices outside the schedule
+    int64_t n_outside = 0;
+    unsigned long long *unit_ctr = nullptr;
+    ~Part() { delete sg; }
 };
 
 struct PartArgs {
@@ -42,6 +80,56 @@ struct PartArgs {
 
 // per-block statistics of the drain (ints: nact, work, push_ops, push_dang,
 // conv_all, conv_scan; floats in l1/above/nd_above)
+// per-vertex inputs of the drain, loadable ahead of a row's gathers
+struct PartIn {
+    int32_t v, dv;
+    double h, rv;
+    bool act, dang;
+};
+
+__device__ __forceinline__ PartIn part_load(const PartArgs &A, int32_t v) {
+    PartIn q;
+    q.v = v;
+    q.dv = __ldg(&A.deg[v]);
+    q.h = A.h[v];
+    q.rv = A.reserved[v];
+    q.act = A.act[v] != 0;
+    q.dang = __ldg(&A.dang[v]) != 0;
+    return q;
+}
+
+// h_v = (drained last state ? 0 : h_v) + inflow, then the drain
+__device__ __forceinline__ void part_finish(const PartArgs &A, const PartIn &q, double sum, double *s_mine,
+                                            Partial &p) {
+    const int64_t v = q.v;
+    const double hv = __dadd_rn(q.act ? 0.0 : q.h, sum);
+    const bool scan = !q.dang;
+    const bool above = hv > A.xi;
+    p.l1 += hv;
+    if (above) {
+        p.above += hv;
+        if (scan) p.nd_above += hv;
+    } else {
+        p.conv_all += 1;
+        if (scan) p.conv_scan += 1;
+    }
+    const bool active = above && scan;
+    A.act[v] = active;
+    if (active) {
+        const int32_t len = __ldg(&A.row_len[v]);
+        A.reserved[v] = __dadd_rn(q.rv, hv);
+        A.h[v] = hv;
+        s_mine[v] = len > 0 ? __ddiv_rn(__dmul_rn(A.c, hv), (double)q.dv) : 0.0;
+        p.nact += 1;
+        p.work += (int64_t)q.dv + 1;
+        p.push_ops += len;
+        p.push_dang += __ldg(&A.dtc[v]);
+    } else {
+        A.h[v] = hv;
+        s_mine[v] = 0.0;
+    }
+}
+
 __device__ __forceinline__ void part_drain(const PartArgs &A, int64_t v, double *s_mine, Partial &p) {
     const double hv = A.h[v];
     const int32_t dv = A.deg[v];
@@ -98,6 +186,55 @@ __global__ void __launch_bounds__(256) k_part_round(PartArgs A, const double *__
     if (threadIdx.x == 0) A.partials[blockIdx.x] = p;
 }
 
+// fast round: binned gather over the receiving rows (drain inputs loaded
+// before each row's gathers when the round is L2-resident), then the owned
+// vertices outside the schedule (no inflow)
+struct PartRows {
+    const PartArgs &A;
+    const int32_t *ids;
+    double *s_mine;
+    Partial &p;
+    __device__ __forceinline__ PartIn pre(bool valid, int64_t row) const {
+        if (valid) return part_load(A, __ldg(&ids[row]));
+        PartIn q;
+        q.v = 0;
+        q.dv = 0;
+        q.h = q.rv = 0.0;
+        q.act = q.dang = false;
+        return q;
+    }
+    __device__ __forceinline__ void fin(bool valid, const PartIn &q, double sum) {
+        if (valid) part_finish(A, q, sum, s_mine, p);
+    }
+    __device__ __forceinline__ void single(int64_t row, double sum) {
+        part_finish(A, part_load(A, __ldg(&ids[row])), sum, s_mine, p);
+    }
+};
+
+template <bool STREAM, bool PREFETCH>
+__global__ void __launch_bounds__(256, PREFETCH ? 3 : 4) k_part_pull(PartArgs A, BinView T, const int32_t *outside,
+                                                                    int64_t n_outside, const double *__restrict__ s_full,
+                                                                    double *s_mine) {
+    Partial p;
+    zero(p);
+    const Src src{s_full, s_full, 0, 0};
+    PartRows rows{A, T.ids, s_mine, p};
+    if constexpr (PREFETCH) {
+        bins_run<STREAM, true, 0>(T, 0, T.n_units, src, rows);
+    } else {
+        auto thread_row = [&](bool valid, int64_t row, double sum) {
+            if (valid) part_finish(A, part_load(A, __ldg(&T.ids[row])), sum, s_mine, p);
+        };
+        auto single_row = [&](int64_t row, double sum) { rows.single(row, sum); };
+        bins_run_plain<STREAM, 0>(T, 0, T.n_units, src, thread_row, single_row);
+    }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_outside;
+         i += (int64_t)gridDim.x * blockDim.x)
+        part_finish(A, part_load(A, __ldg(&outside[i])), 0.0, s_mine, p);
+    block_reduce(p);
+    if (threadIdx.x == 0) A.partials[blockIdx.x] = p;
+}
+
 __global__ void k_part_shares(PartArgs A, double *x_mine) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < A.owned; v += (int64_t)gridDim.x * blockDim.x)
         x_mine[v] = A.deg[v] > 0 ? __ddiv_rn(__dmul_rn(A.c, A.reserved[v]), (double)A.deg[v]) : 0.0;
@@ -139,13 +276,29 @@ __global__ void __launch_bounds__(256) k_part_total(PartArgs A, int include_h) {
     if (threadIdx.x == 0) A.partials[blockIdx.x] = p;
 }
 
-// one block: fixed-order reduction of the block partials
-__global__ void k_part_reduce(const Partial *partials, int64_t blocks, Partial *out) {
+// one block: fixed-order reduction of the block partials; optionally the 9
+// statistics as doubles for a device all-reduce, and the unit counter reset
+__global__ void k_part_reduce(const Partial *partials, int64_t blocks, Partial *out, double *out9,
+                              unsigned long long *unit_ctr) {
     Partial acc;
     zero(acc);
     for (int64_t b = threadIdx.x; b < blocks; b += blockDim.x) add(acc, partials[b]);
     block_reduce(acc);
-    if (threadIdx.x == 0) *out = acc;
+    if (threadIdx.x == 0) {
+        *out = acc;
+        if (out9) {
+            out9[0] = acc.l1;
+            out9[1] = acc.above;
+            out9[2] = acc.nd_above;
+            out9[3] = (double)acc.nact;
+            out9[4] = (double)acc.work;
+            out9[5] = (double)acc.push_ops;
+            out9[6] = (double)acc.push_dang;
+            out9[7] = (double)acc.conv_all;
+            out9[8] = (double)acc.conv_scan;
+        }
+        if (unit_ctr) *unit_ctr = 0;
+    }
 }
 
 static PartArgs args_of(Part &P) {
@@ -169,7 +322,7 @@ static PartArgs args_of(Part &P) {
 
 static int finish_stats(Part &P, unsigned blocks, int64_t *ints, double *floats) {
     cudaStream_t st = P.ctx->stream;
-    k_part_reduce<<<1, 256, 0, st>>>(P.partials.as<Partial>(), blocks, P.stats.as<Partial>());
+    k_part_reduce<<<1, 256, 0, st>>>(P.partials.as<Partial>(), blocks, P.stats.as<Partial>(), nullptr, P.unit_ctr);
     Partial h;
     PR_CUDA(cudaMemcpyAsync(&h, P.stats.ptr, sizeof(h), cudaMemcpyDeviceToHost, st));
     PR_CUDA(cudaStreamSynchronize(st));
@@ -234,12 +387,116 @@ int part_create(Ctx &ctx, int64_t owned, int64_t slot, const int64_t *in_off, co
         if ((rc = ensure(P->h, 8 * (owned ? owned : 1)))) break;
         if ((rc = ensure(P->reserved, 8 * (owned ? owned : 1)))) break;
         if ((rc = ensure(P->act, owned ? owned : 1))) break;
-        if ((rc = ensure(P->partials, sizeof(Partial) * (grid_for(owned, 256) + 1)))) break;
-        if ((rc = ensure(P->stats, sizeof(Partial)))) break;
+        if ((rc = ensure(P->partials, sizeof(Partial) * (grid_for(owned, 256) + (int64_t)ctx.sm_count * 8 + 1)))) break;
+        if ((rc = ensure(P->stats, sizeof(Partial) + 64))) break;
+        P->unit_ctr = (unsigned long long *)(P->stats.as<char>() + sizeof(Partial) + 32);
+        cudaMemsetAsync(P->unit_ctr, 0, 8, ctx.stream);
         if (cudaStreamSynchronize(ctx.stream) != cudaSuccess) rc = fail(PR_ERR_CUDA, "partition upload");
     } while (0);
     if (rc) { delete P; return rc; }
     *out = P;
+    return PR_OK;
+}
+
+// the fast form's pull schedule, built on first use
+static int ensure_part_sched(Part &P) {
+    if (P.sg) return PR_OK;
+    Ctx &ctx = *P.ctx;
+    cudaStream_t st = ctx.stream;
+    Graph *g = new Graph();
+    g->ctx = &ctx;
+    g->n = P.owned;
+    g->m = P.edges;
+    int rc = PR_OK;
+    do {
+        if ((rc = ensure(g->in_off, 8 * (P.owned + 1)))) break;
+        if ((rc = ensure(g->in_src, 4 * (P.edges > 0 ? P.edges : 1)))) break;
+        if ((rc = ensure(g->out_deg, 4 * (P.owned > 0 ? P.owned : 1)))) break;
+        cudaMemcpyAsync(g->in_off.ptr, P.in_off.ptr, 8 * (P.owned + 1), cudaMemcpyDeviceToDevice, st);
+        if (P.edges) cudaMemcpyAsync(g->in_src.ptr, P.in_src.ptr, 4 * P.edges, cudaMemcpyDeviceToDevice, st);
+        if (P.owned) cudaMemcpyAsync(g->out_deg.ptr, P.deg.ptr, 4 * P.owned, cudaMemcpyDeviceToDevice, st);
+        // IFP2 pulls into non-dangling rows only (receives = !dangling), IFP1 into all
+        P.which = P.algorithm == PR_ALGO_IFP2 ? 1 : 0;
+        if ((rc = ensure_sched(*g, P.which))) break;
+        // the same working-set rules as the engine's k_pull (rounds.cu)
+        const double ws = 4.0 * (double)g->sched[P.which].edges + 8.0 * (double)P.slot + 44.0 * (double)P.owned;
+        const double l2 = (double)(ctx.l2_bytes ? ctx.l2_bytes : (size_t)126 << 20);
+        P.stream_csc = ws > 0.6 * l2;
+        P.prefetch = ws < 4.0 * l2;
+        P.blocks = (int64_t)ctx.sm_count * (P.prefetch ? 3 : 4);
+        if ((rc = ensure_units(*g, P.which, P.blocks, 1))) break;
+        // owned vertices outside the schedule: no inflow, drained alone
+        {
+            DevBuf cnt;
+            if ((rc = ensure(cnt, 8))) break;
+            if ((rc = ensure(P.outside, 4 * (P.owned > 0 ? P.owned : 1)))) break;
+            auto first = thrust::make_counting_iterator<int32_t>(0);
+            OutsideRow pred{P.in_off.as<int64_t>(), P.recv.as<uint8_t>()};
+            if ((rc = cub_run(ctx, [&](void *t, size_t &b) {
+                     return cub::DeviceSelect::If(t, b, first, P.outside.as<int32_t>(), cnt.as<int64_t>(),
+                                                  (int)P.owned, pred, st);
+                 })))
+                break;
+            cudaMemcpyAsync(&P.n_outside, cnt.ptr, 8, cudaMemcpyDeviceToHost, st);
+        }
+        if (cudaStreamSynchronize(st) != cudaSuccess) rc = fail(PR_ERR_CUDA, "partition schedule");
+    } while (0);
+    if (rc) {
+        delete g;
+        return rc;
+    }
+    P.sg = g;
+    return PR_OK;
+}
+
+static BinView part_view(Part &P) {
+    auto &S = P.sg->sched[P.which];
+    BinView T;
+    T.ids = S.ids.as<int32_t>();
+    T.doff = S.doff.as<int64_t>();
+    T.csc = S.csc.as<int32_t>();
+    T.count = S.count;
+    T.n_hub = S.n_hub;
+    T.n_warp = S.n_warp;
+    T.chunk_base = S.chunk_base.as<int64_t>();
+    T.units = S.units.as<int2>();
+    T.n_units = S.n_units;
+    T.row_cnt = S.row_cnt.as<int32_t>();
+    T.chunk_part = S.chunk_part.as<double>();
+    T.unit_ctr = P.unit_ctr;
+    return T;
+}
+
+int part_init_device(Part &P, double *d_s_mine, double *d_stats9) {
+    unsigned g = grid_for(P.owned, 256);
+    cudaStream_t st = P.ctx->stream;
+    k_part_init<<<g, 256, 0, st>>>(args_of(P), d_s_mine);
+    k_part_reduce<<<1, 256, 0, st>>>(P.partials.as<Partial>(), g, P.stats.as<Partial>(), d_stats9, P.unit_ctr);
+    PR_CUDA(cudaGetLastError());
+    return PR_OK;
+}
+
+int part_round_device(Part &P, const double *d_s_full, double *d_s_mine, int fast, double *d_stats9) {
+    cudaStream_t st = P.ctx->stream;
+    unsigned g;
+    if (fast) {
+        PR_TRY(ensure_part_sched(P));
+        g = (unsigned)P.blocks;
+        const int32_t *out = P.outside.as<int32_t>();
+        const int64_t no = P.n_outside;
+        if (P.stream_csc) {
+            if (P.prefetch) k_part_pull<true, true><<<g, 256, 0, st>>>(args_of(P), part_view(P), out, no, d_s_full, d_s_mine);
+            else k_part_pull<true, false><<<g, 256, 0, st>>>(args_of(P), part_view(P), out, no, d_s_full, d_s_mine);
+        } else {
+            if (P.prefetch) k_part_pull<false, true><<<g, 256, 0, st>>>(args_of(P), part_view(P), out, no, d_s_full, d_s_mine);
+            else k_part_pull<false, false><<<g, 256, 0, st>>>(args_of(P), part_view(P), out, no, d_s_full, d_s_mine);
+        }
+    } else {
+        g = grid_for(P.owned, 256);
+        k_part_round<<<g, 256, 0, st>>>(args_of(P), d_s_full, d_s_mine);
+    }
+    k_part_reduce<<<1, 256, 0, st>>>(P.partials.as<Partial>(), g, P.stats.as<Partial>(), d_stats9, P.unit_ctr);
+    PR_CUDA(cudaGetLastError());
     return PR_OK;
 }
 
@@ -296,5 +553,6 @@ void part_destroy(Part *P) {
 }
 
 Ctx &part_ctx(Part &P) { return *P.ctx; }
+void *part_stream(Part &P) { return (void *)P.ctx->stream; }
 
 }  // namespace pr

@@ -15,7 +15,10 @@ padded space (rank p's vertices at [p*S, p*S + hi_p - lo_p)), so every
 exchange is one equal-sized ``all_gather_into_tensor`` (in place, NCCL over
 NVLink on the GPU; gloo in the CPU tests).  The local step is pluggable:
 ``CudaLocalStep`` (libpushrank_cuda ``pr_part_*``) in production, a numpy step
-in tests/test_distributed.py.
+in tests/test_distributed.py.  ``run_partitioned`` synchronises with the host
+every round (any backend); ``run_partitioned_queued`` keeps the rounds, their
+all-gathers and statistics all-reduces on the device and reads the
+statistics back every few rounds (NCCL).
 """
 
 from __future__ import annotations
@@ -72,41 +75,77 @@ class Partition:
         return r * self.slot + (ids - self.bounds[r])
 
 
-def partition_graph(g, parts: int, rank: int, algorithm: str = "ifp1") -> Partition:
+def run_order(out_deg: np.ndarray, in_deg: np.ndarray) -> np.ndarray:
+    """The engines' run layout (csrc/graph.cu k_relabel_keys): vertices by
+    class (in>0 & out>0 | out>0 & in=0 | out=0 & in>0 | isolated), then by
+    descending in-degree inside the receiving classes, ties by id.  Returns
+    order[new id] = original id."""
+    cls = np.where(out_deg > 0, np.where(in_deg > 0, 0, 1), np.where(in_deg > 0, 2, 3))
+    key = np.where((cls == 0) | (cls == 2), -np.minimum(in_deg, 0x3FFFFFFF), 0)
+    return np.lexsort((np.arange(out_deg.size), key, cls)).astype(np.int64)
+
+
+def partition_graph(g, parts: int, rank: int, algorithm: str = "ifp1", order: np.ndarray | None = None) -> Partition:
     """Rank `rank`'s partition of a graph with the reference arrays
-    (out_offsets/out_targets/in_offsets/in_sources, int64)."""
+    (out_offsets/out_targets/in_offsets/in_sources, int64).
+
+    ``order`` (order[new id] = original id, e.g. ``run_order``) partitions
+    the renumbered graph instead: vertex ids, ranges and source ids are the
+    new ones (what the fast local step wants: hot sources at low ids), and a
+    row's sources keep their original CSC order.  Only this rank's rows are
+    gathered."""
     n = int(g.n)
     out_off = np.asarray(g.out_offsets, np.int64)
     out_tgt = np.asarray(g.out_targets, np.int64)
     in_off = np.asarray(g.in_offsets, np.int64)
     in_src = np.asarray(g.in_sources, np.int64)
     out_deg = np.diff(out_off)
-    in_deg = np.diff(in_off)
     dang = out_deg == 0
+    # per-vertex push-row data in original ids
+    if algorithm == "ifp2":
+        # live push row length: out-edges into non-dangling targets (graph.py:353-356)
+        kept = np.concatenate(([0], np.cumsum((~dang[out_tgt]).astype(np.int64))))
+        row_len_all = kept[out_off[1:]] - kept[out_off[:-1]]
+        dtc_all = None
+    else:
+        cum = np.concatenate(([0], np.cumsum(dang[out_tgt].astype(np.int64))))
+        dtc_all = cum[out_off[1:]] - cum[out_off[:-1]]
+        row_len_all = out_deg
+    if order is None:
+        order = None
+        rank_of = None
+        in_deg = np.diff(in_off)
+    else:
+        order = np.asarray(order, np.int64)
+        rank_of = np.empty(n, np.int64)
+        rank_of[order] = np.arange(n, dtype=np.int64)
+        in_deg = np.diff(in_off)[order]
     bounds = edge_balanced_ranges(in_deg, parts)
     slot = int(np.max(np.diff(bounds))) if parts else n
     slot = max(slot, 1)
     lo, hi = int(bounds[rank]), int(bounds[rank + 1])
-    rows = in_off[lo:hi + 1] - in_off[lo]
-    src = in_src[in_off[lo]:in_off[hi]]
+    if order is None:
+        verts = np.arange(lo, hi, dtype=np.int64)
+        rows = in_off[lo:hi + 1] - in_off[lo]
+        src = in_src[in_off[lo]:in_off[hi]]
+    else:
+        verts = order[lo:hi]
+        d = in_deg[lo:hi]
+        rows = np.concatenate(([0], np.cumsum(d)))
+        starts = np.repeat(in_off[verts] - rows[:-1], d)
+        src = rank_of[in_src[starts + np.arange(rows[-1], dtype=np.int64)]]
     r = np.searchsorted(bounds, src, side="right") - 1
     src_pad = r * slot + (src - bounds[r])
+    row_len = row_len_all[verts]
     if algorithm == "ifp2":
-        # live push row length: out-edges into non-dangling targets (graph.py:353-356)
-        keep = ~dang[out_tgt]
-        kept = np.concatenate(([0], np.cumsum(keep.astype(np.int64))))
-        row_len = (kept[out_off[1:]] - kept[out_off[:-1]])[lo:hi]
         dtc = np.zeros(hi - lo, np.int64)
-        receives = ~dang[lo:hi]
+        receives = ~dang[verts]
     else:
-        isd = dang[out_tgt].astype(np.int64)
-        cum = np.concatenate(([0], np.cumsum(isd)))
-        dtc = (cum[out_off[1:]] - cum[out_off[:-1]])[lo:hi]
-        row_len = out_deg[lo:hi].copy()
+        dtc = dtc_all[verts]
         receives = np.ones(hi - lo, bool)
     return Partition(rank=rank, parts=parts, n=n, bounds=bounds, slot=slot, lo=lo, hi=hi,
-                     in_offsets=rows, in_sources=src_pad, out_degree=out_deg[lo:hi].copy(),
-                     row_len=row_len, dtc=dtc, dangling=dang[lo:hi].copy(), receives=receives)
+                     in_offsets=rows, in_sources=src_pad, out_degree=out_deg[verts].copy(),
+                     row_len=row_len, dtc=dtc, dangling=dang[verts].copy(), receives=receives)
 
 
 @dataclass
@@ -127,9 +166,27 @@ class Comm:
         self.torch, self.dist = torch, dist
         self.device = device
 
+    def _staged(self, t) -> bool:
+        # gloo has no CUDA all-gather: device tensors go through host copies
+        return t.is_cuda and self.dist.get_backend() == "gloo"
+
     def allgather_slots(self, full, mine_view) -> None:
         # `mine_view` aliases this rank's slice of `full`: in-place all-gather
+        if self._staged(full):
+            host = full.cpu()
+            self.dist.all_gather_into_tensor(host, mine_view.cpu())
+            full.copy_(host)
+            return
         self.dist.all_gather_into_tensor(full, mine_view.clone() if full.device.type == "cpu" else mine_view)
+
+    def allreduce_row(self, row) -> None:
+        """In-place sum of a statistics row (device or host tensor)."""
+        if self._staged(row):
+            host = row.cpu()
+            self.dist.all_reduce(host)
+            row.copy_(host)
+            return
+        self.dist.all_reduce(row)
 
     def allreduce_stats(self, ints: np.ndarray, floats: np.ndarray):
         # one all-reduce per round: the integer counters ride in a float64
@@ -202,6 +259,127 @@ def run_partitioned(step, comm, part: Partition, algorithm: str, damping: float,
                                       "push_ops_dangling": push_dang, "settled": settled}
 
 
+def run_partitioned_queued(step, comm, part: Partition, algorithm: str, damping: float, threshold: float,
+                           max_rounds: int = 1_000_000, conv_scope_all: bool = False, batch: int = 8,
+                           graph: bool | None = None, host_values: bool = True):
+    """``run_partitioned`` with the rounds queued on the device: each round
+    is the local step, the all-gather of its shares and an in-place
+    all-reduce of its 9 statistics (a row of a device buffer), all issued on
+    the library stream without host synchronisation; the host reads the
+    statistics of ``batch`` rounds at a time and stops at the first state
+    with no active vertex.  Rounds queued past that state are no-ops (no
+    vertex above the threshold: zero shares, unchanged mass), so the result
+    and the trace equal run_partitioned's.  Needs a step with
+    ``init_device`` / ``round_device`` (CudaLocalStep, whose ``stream`` the
+    collectives are ordered on; NumpyLocalStep for the CPU tests).
+
+    ``graph`` (default: on with NCCL): a batch of rounds -- the local
+    kernels and the NCCL collectives -- is captured once into a CUDA graph
+    on the library stream and replayed for every later batch (and solve), so
+    a round costs no host launches.  Batches start at even rounds, so the
+    share-buffer parities of a replay are those of the capture.
+
+    ``host_values=False`` leaves the owned result on the device (the step's
+    reserved/pending buffers) and returns None for it: the timed solve of
+    bench.py, like the single-GPU engine's device time, excludes the D2H."""
+    import contextlib
+    torch = comm.torch
+    S, P = part.slot, part.parts
+    dev = getattr(step, "dev", None) or comm.device or torch.device("cpu")
+    stream = getattr(step, "stream", None)
+    ctx = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+    if graph is None:
+        graph = stream is not None and comm.dist.get_backend() == "nccl"
+    batch += batch & 1
+    rows = []
+    push_ops = push_dang = 0
+
+    def record(r):
+        nonlocal push_ops, push_dang
+        l1, above, nd_above = float(r[0]), float(r[1]), float(r[2])
+        nact, work, pops, pdang, conv_all, conv_scan = (int(round(x)) for x in r[3:9])
+        rows.append({"h_l1": l1, "converged": conv_all if conv_scope_all else conv_scan,
+                     "alpha": nd_above / above if above > 0 else 1.0, "work": work, "push_ops": push_ops,
+                     "push_ops_dangling": push_dang, "active_mass": above, "carry_mass": l1 - above})
+        push_ops += pops
+        push_dang += pdang
+        return nact
+
+    with ctx:
+        cache = getattr(step, "_queued", None) if graph else None
+        if cache is None or cache["batch"] != batch:
+            full = [torch.zeros(S * P, dtype=torch.float64, device=dev) for _ in range(2)]
+            cache = {"batch": batch, "full": full, "mine": [f[part.rank * S:(part.rank + 1) * S] for f in full],
+                     "stats": torch.zeros((batch, 9), dtype=torch.float64, device=dev), "graph": None}
+            if graph:
+                step._queued = cache
+        full, mine, stats = cache["full"], cache["mine"], cache["stats"]
+
+        def queue_batch(nb, t0):
+            for j in range(nb):
+                tt = t0 + j
+                step.round_device(full[tt & 1], mine[(tt + 1) & 1], stats[j])
+                comm.allgather_slots(full[(tt + 1) & 1], mine[(tt + 1) & 1])
+                comm.allreduce_row(stats[j])
+
+        def run_batch(t0):
+            if not graph:
+                nb = max(1, min(batch, max_rounds - t0))
+                queue_batch(nb, t0)
+                return nb
+            if cache["graph"] is None and t0 > 0:
+                # capture once the schedule exists (built by the first, eager batch)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    queue_batch(batch, 0)
+                cache["graph"] = g
+            if cache["graph"] is None:
+                queue_batch(batch, t0)
+            else:
+                cache["graph"].replay()
+            return batch
+
+        step.init_device(mine[0], stats[0])
+        comm.allgather_slots(full[0], mine[0])
+        comm.allreduce_row(stats[0])
+        nact = record(stats[0].cpu().numpy())
+        t = 0
+        while nact > 0:
+            if t >= max_rounds:
+                raise RuntimeError(f"sync simulation did not settle in {max_rounds} iterations")
+            nb = run_batch(t)
+            host = stats[:nb].cpu().numpy()
+            for j in range(nb):
+                nact = record(host[j])
+                t += 1
+                if nact == 0:
+                    break
+        settled = 0
+        if algorithm == "ifp2":
+            step.settle_shares(mine[0])
+            comm.allgather_slots(full[0], mine[0])
+            settled, ints, floats = step.settle(full[0])
+            gi, gf = comm.allreduce_stats(np.array([settled, 0, 0, 0, ints[4], ints[5]], np.int64), floats)
+            settled = int(gi[0])
+            push_ops += settled
+            push_dang += settled
+            rows.append({"h_l1": float(gf[0]), "converged": int(gi[4] if conv_scope_all else gi[5]),
+                         "alpha": float(gf[2] / gf[1]) if gf[1] > 0 else 1.0, "work": 0, "push_ops": push_ops,
+                         "push_ops_dangling": push_dang, "active_mass": float(gf[1]),
+                         "carry_mass": float(gf[0] - gf[1])})
+        total_local = step.local_total()
+        _, gt = comm.allreduce_stats(np.zeros(6, np.int64), np.array([total_local, 0.0, 0.0]))
+        total = float(gt[0])
+        values = step.values(total) if host_values else None
+    return values, rows, {"rounds": t, "mass_total": total, "push_ops": push_ops,
+                          "push_ops_dangling": push_dang, "settled": settled}
+
+
+def _stats_row(row, ints, floats) -> None:
+    import torch
+    row.copy_(torch.from_numpy(np.concatenate([np.asarray(floats, np.float64), np.asarray(ints, np.float64)])))
+
+
 class NumpyLocalStep:
     """CPU local step (reference semantics, sequential ascending-source sums in
     bincount order).  Test double for tests/test_distributed.py; never used by
@@ -247,6 +425,13 @@ class NumpyLocalStep:
         self.h = np.where(self.act, 0.0, self.h) + inflow
         return self._drain(s_mine)
 
+    # queued form (run_partitioned_queued)
+    def init_device(self, s_mine, stats_row):
+        _stats_row(stats_row, *self.init(s_mine))
+
+    def round_device(self, s_in, s_mine, stats_row):
+        _stats_row(stats_row, *self.round(None, s_in, s_mine))
+
     def settle_shares(self, x_mine):
         p = self.p
         x = np.zeros(p.slot)
@@ -288,7 +473,8 @@ class CudaLocalStep:
     reads torch-written data.
     """
 
-    def __init__(self, part: Partition, damping: float, threshold: float, algorithm: str, device=None):
+    def __init__(self, part: Partition, damping: float, threshold: float, algorithm: str, device=None,
+                 fast: bool = False):
         import ctypes
 
         import torch
@@ -296,6 +482,9 @@ class CudaLocalStep:
         from . import _lib
         self._lib, self._ct, self.torch = _lib, ctypes, torch
         self.part, self.algo = part, algorithm
+        # fast: the binned dense-round gather (run_partitioned_queued); else the
+        # exact ascending-source sums (bit-identical to sync_simulate)
+        self.fast = bool(fast)
         ctx = _lib.context(device)
         self.dev = torch.device("cuda", ctx.device)
         L = _lib.load()
@@ -362,6 +551,23 @@ class CudaLocalStep:
                                              self._lib.ptr(floats)), "pr_part_round")
         self._back(s_mine)
         return ints, floats
+
+    # -- queued form (run_partitioned_queued): device tensors, no host sync
+    @property
+    def stream(self):
+        p = self._ct.c_void_p()
+        self._lib.check(self.L.pr_part_stream(self.h, self._ct.byref(p)), "pr_part_stream")
+        return self.torch.cuda.ExternalStream(p.value or 0, device=self.dev)
+
+    def init_device(self, s_mine, stats_row):
+        self._lib.check(self.L.pr_part_init_device(self.h, self._ct.c_void_p(s_mine.data_ptr()),
+                                                   self._ct.c_void_p(stats_row.data_ptr())), "pr_part_init_device")
+
+    def round_device(self, s_in, s_mine, stats_row):
+        self._lib.check(self.L.pr_part_round_device(self.h, self._ct.c_void_p(s_in.data_ptr()),
+                                                    self._ct.c_void_p(s_mine.data_ptr()), int(self.fast),
+                                                    self._ct.c_void_p(stats_row.data_ptr())),
+                        "pr_part_round_device")
 
     def settle_shares(self, x_mine):
         out = self._out(x_mine)

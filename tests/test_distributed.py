@@ -29,27 +29,33 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, config, algorithm, out_q):
+def _worker(rank, world, port, config, algorithm, out_q, queued=False, relabel=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         n, src, dst = synthetic.make(config, seed=0)
         g = oracle.from_edges(n, src, dst)
-        part = D.partition_graph(g, world, rank, algorithm)
+        order = D.run_order(np.diff(g.out_offsets), np.diff(g.in_offsets)) if relabel else None
+        part = D.partition_graph(g, world, rank, algorithm, order=order)
         step = D.NumpyLocalStep(part, 0.85, 1e-10, algorithm)
         comm = D.Comm()
-        vals, rows, info = D.run_partitioned(step, comm, part, algorithm, 0.85, 1e-10, conv_scope_all=True)
+        if queued:
+            # rounds queued in batches of 5 (partial last batch, no-op rounds past the end)
+            vals, rows, info = D.run_partitioned_queued(step, comm, part, algorithm, 0.85, 1e-10,
+                                                        conv_scope_all=True, batch=5)
+        else:
+            vals, rows, info = D.run_partitioned(step, comm, part, algorithm, 0.85, 1e-10, conv_scope_all=True)
         out_q.put((rank, part.lo, part.hi, step.reserved, step.h, vals, rows, info))
     finally:
         dist.destroy_process_group()
 
 
-def _run(world, config, algorithm):
+def _run(world, config, algorithm, queued=False, relabel=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, config, algorithm, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, config, algorithm, q, queued, relabel)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in range(world)]
@@ -83,9 +89,12 @@ def test_partition_covers_graph():
     assert np.array_equal(back, g.in_sources[g.in_offsets[p.lo]:g.in_offsets[p.hi]])
 
 
+@pytest.mark.parametrize("queued", [False, True])
 @pytest.mark.parametrize("algorithm", ["ifp1", "ifp2"])
-def test_two_ranks_match_sync_twin_bit_exact(algorithm):
-    res = _run(2, "c1", algorithm)
+def test_two_ranks_match_sync_twin_bit_exact(algorithm, queued):
+    """Host-synchronised rounds and rounds queued in batches (statistics read
+    back every 5 rounds) give the same state, trace and round count."""
+    res = _run(2, "c1", algorithm, queued)
     n, src, dst = synthetic.make("c1", seed=0)
     g = oracle.from_edges(n, src, dst)
     o = oracle.sync_simulate(g, algorithm, threshold=1e-10)
@@ -102,3 +111,30 @@ def test_two_ranks_match_sync_twin_bit_exact(algorithm):
     np.testing.assert_allclose(vals, o.values, rtol=1e-13, atol=0)
     if algorithm == "ifp2":
         assert res[0][7]["settled"] == int((g.out_degree == 0)[g.out_targets].sum())
+
+
+def test_run_order_partitions_bit_exact():
+    """Partitions of the run layout (vertices renumbered as the engines do,
+    csrc/graph.cu k_relabel_keys): each row keeps its sources' original
+    order, so the sequential sums -- and the state, trace and values, once
+    un-permuted -- still equal the sync twin bit for bit."""
+    n, src, dst = synthetic.make("c1", seed=0)
+    g = oracle.from_edges(n, src, dst)
+    order = D.run_order(np.diff(g.out_offsets), np.diff(g.in_offsets))
+    assert np.array_equal(np.sort(order), np.arange(n))
+    indeg = np.diff(g.in_offsets)[order]
+    outdeg = np.diff(g.out_offsets)[order]
+    cls = np.where(outdeg > 0, np.where(indeg > 0, 0, 1), np.where(indeg > 0, 2, 3))
+    assert np.all(np.diff(cls) >= 0)
+    first = cls == 0
+    assert np.all(np.diff(indeg[first]) <= 0)
+    for algorithm in ("ifp1", "ifp2"):
+        res = _run(2, "c1", algorithm, queued=True, relabel=True)
+        o = oracle.sync_simulate(g, algorithm, threshold=1e-10)
+        reserved = np.empty(n)
+        reserved[order] = np.concatenate([r[3] for r in res])
+        assert np.array_equal(reserved, o.reserved)
+        vals = np.empty(n)
+        vals[order] = np.concatenate([r[5] for r in res])
+        np.testing.assert_allclose(vals, o.values, rtol=1e-13, atol=0)
+        assert [r["push_ops"] for r in res[0][6]] == o.rows["push_ops"].tolist()
