@@ -321,10 +321,15 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
     # (binned gather) with the rounds, all-gathers and statistics all-reduces
     # queued on the library stream (statistics read back every 8 rounds)
     step = D.CudaLocalStep(part, DAMPING, XI, args.algo, device=local, fast=True)
+    # fused exchange (shares stored into every rank's replica by the round
+    # kernel, peer memory over NVLink) unless PUSHRANK_FUSED=0 or the peer
+    # mapping fails on any rank (then the NCCL all-gather form)
+    want_fused = dist.get_backend() == "nccl" and os.environ.get("PUSHRANK_FUSED", "1") != "0"
+    fused = want_fused and step.setup_fused(comm)
 
-    def solve(s, host_values=False):
+    def solve(s, host_values=False, fused=fused):
         vals, rows, info = D.run_partitioned_queued(s, comm, part, args.algo, DAMPING, XI, batch=8,
-                                                    host_values=host_values)
+                                                    host_values=host_values, fused=fused)
         return vals, info
 
     for _ in range(args.warmup):
@@ -354,7 +359,7 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
     t0 = time.perf_counter()
     for _ in range(2):
         s2 = D.CudaLocalStep(part, DAMPING, XI, args.algo, device=local, fast=True)
-        solve(s2, host_values=True)
+        solve(s2, host_values=True, fused=fused and s2.setup_fused(comm))
         del s2
     torch.cuda.synchronize()
     te = torch.tensor([(time.perf_counter() - t0) / 2], dtype=torch.float64, device=red_dev)
@@ -371,9 +376,11 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
                         "d2h_bytes_per_step": int(8 * part.owned), "ms_per_step": 1e3 * e2e_s,
                         "path": "per step: partition upload (pr_part_create) + rounds + owned values D2H"},
                 "gpu_launches": int(2 * (info["rounds"] + 2)), "clocks": clocks.summary(),
-                "note": ("partitioned rounds queued on the device (statistics read back every 8 rounds); "
-                         "local step = binned dense-round gather (k_part_pull); exchange = all-gather of "
-                         "shares + all-reduce of 9 statistics per round")}
+                "exchange": ("fused: round kernel stores shares into every rank's replica (peer memory)"
+                             if fused else "NCCL all-gather of shares per round"),
+                "note": ("partitioned rounds queued on the device and graph-captured (statistics read back "
+                         "every 8 rounds); local step = binned dense-round gather (k_part_pull); "
+                         "all-reduce of 9 statistics per round (the round barrier)")}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 

@@ -271,6 +271,24 @@ int pr_part_init_device(pr_part *p, double *d_shares_mine, double *d_stats);
 int pr_part_round_device(pr_part *p, const double *d_shares_full, double *d_shares_mine, int32_t fast,
                          double *d_stats);
 int pr_part_stream(pr_part *p, void **stream);
+/* Fused exchange (one process per GPU over NVLink/NVSwitch): the round
+ * kernel stores every drained share straight into every rank's replica of
+ * the full share vector, so no all-gather follows it; the caller's
+ * statistics all-reduce is the round's barrier.
+ *   pr_part_share_buffers: allocates this rank's two replicas (parity 0/1,
+ *     slot*parts doubles, cudaMalloc) -> d_full[2] and their CUDA IPC
+ *     handles (2 x 64 bytes at ipc_handles, may be NULL);
+ *   pr_part_set_peers: opens the other ranks' handles (parts x 2 x 64 bytes,
+ *     rank-major, as gathered from every rank);
+ *   pr_part_set_peer_ptrs: the same from device pointers (2 per rank) -- the
+ *     ranks emulated in one process on one device (tests);
+ *   pr_part_init_fused / pr_part_round_fused(parity): state 0 into replicas
+ *     0; a round reading replica `parity`, writing replicas 1-parity. */
+int pr_part_share_buffers(pr_part *p, int32_t parts, int32_t rank, void **d_full, void *ipc_handles);
+int pr_part_set_peers(pr_part *p, const void *ipc_handles);
+int pr_part_set_peer_ptrs(pr_part *p, int32_t parts, int32_t rank, void *const *d_full);
+int pr_part_init_fused(pr_part *p, double *d_stats);
+int pr_part_round_fused(pr_part *p, int32_t parity, double *d_stats);
 int pr_part_settle_shares(pr_part *p, double *d_x_mine);
 int pr_part_settle(pr_part *p, const double *d_x_full, int64_t *settled, int64_t *ints, double *floats);
 int pr_part_total(pr_part *p, int32_t include_pending, double *total);

@@ -60,6 +60,11 @@ Ctx &part_ctx(Part &P);
 void *part_stream(Part &P);
 int part_init_device(Part &P, double *d_s_mine, double *d_stats9);
 int part_round_device(Part &P, const double *d_s_full, double *d_s_mine, int fast, double *d_stats9);
+int part_share_buffers(Part &P, int parts, int rank, void **d_full, void *ipc);
+int part_set_peers(Part &P, const void *handles);
+int part_set_peer_ptrs(Part &P, int parts, int rank, void *const *ptrs);
+int part_init_fused(Part &P, double *d_stats9);
+int part_round_fused(Part &P, int parity, double *d_stats9);
 
 static int set_device(Ctx &ctx) {
     PR_CUDA(cudaSetDevice(ctx.device));
@@ -562,6 +567,31 @@ int pr_part_round_device(pr_part *p, const double *d_shares_full, double *d_shar
     PART_ENTER(p);
     CHECK_PTR(d_stats, "stats");
     return part_round_device(*p->p, d_shares_full, d_shares_mine, fast, d_stats);
+}
+int pr_part_share_buffers(pr_part *p, int32_t parts, int32_t rank, void **d_full, void *ipc_handles) {
+    PART_ENTER(p);
+    CHECK_PTR(d_full, "d_full");
+    return part_share_buffers(*p->p, parts, rank, d_full, ipc_handles);
+}
+int pr_part_set_peers(pr_part *p, const void *ipc_handles) {
+    PART_ENTER(p);
+    CHECK_PTR(ipc_handles, "ipc_handles");
+    return part_set_peers(*p->p, ipc_handles);
+}
+int pr_part_set_peer_ptrs(pr_part *p, int32_t parts, int32_t rank, void *const *d_full) {
+    PART_ENTER(p);
+    CHECK_PTR(d_full, "d_full");
+    return part_set_peer_ptrs(*p->p, parts, rank, d_full);
+}
+int pr_part_init_fused(pr_part *p, double *d_stats) {
+    PART_ENTER(p);
+    CHECK_PTR(d_stats, "stats");
+    return part_init_fused(*p->p, d_stats);
+}
+int pr_part_round_fused(pr_part *p, int32_t parity, double *d_stats) {
+    PART_ENTER(p);
+    CHECK_PTR(d_stats, "stats");
+    return part_round_fused(*p->p, parity, d_stats);
 }
 int pr_part_stream(pr_part *p, void **stream) {
     PART_ENTER(p);

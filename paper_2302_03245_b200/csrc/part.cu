@@ -39,6 +39,8 @@
 
 namespace pr {
 
+#define PR_MAX_PEERS 8   // fused exchange: ranks whose replicas a round stores into
+
 // an owned vertex that is not a row of the pull schedule
 struct OutsideRow {
     const int64_t *in_off;
@@ -62,8 +64,19 @@ struct Part {
     bool prefetch = false;    // drain inputs ahead of the gathers (round working set < 4 L2)
     DevBuf outside;           // int32: owned vertices outside the schedule
     int64_t n_outside = 0;
+    // fused exchange: replicas of the full share vector (parity 0/1) of
+    // every rank; own ones allocated here, peers' opened through CUDA IPC
+    int parts = 0, rank = 0;
+    void *own_full[2] = {nullptr, nullptr};
+    double *peer[2][PR_MAX_PEERS] = {};
+    std::vector<void *> opened;
     unsigned long long *unit_ctr = nullptr;
-    ~Part() { delete sg; }
+    ~Part() {
+        delete sg;
+        for (void *p : opened) cudaIpcCloseMemHandle(p);
+        for (void *p : own_full)
+            if (p) cudaFree(p);
+    }
 };
 
 struct PartArgs {
@@ -76,6 +89,28 @@ struct PartArgs {
     uint8_t *act;
     Partial *partials;
     double c, xi;
+};
+
+// Where a drained share goes.  peers.n == 0: this rank's slice `mine` (the
+// caller all-gathers it).  peers.n > 0: the fused exchange -- the share is
+// stored straight into every rank's replica of the full share vector at
+// this rank's slot (peer pointers mapped over NVLink through CUDA IPC; own
+// replica included), so the all-gather happens inside the round kernel,
+// overlapped with the gathers of the rows still running.
+struct ShareOut {
+    double *mine;
+    double *peer[PR_MAX_PEERS];
+    int n;
+    int64_t off;   // rank * slot
+    __device__ __forceinline__ void store(int64_t v, double x) const {
+        if (n == 0) {
+            mine[v] = x;
+            return;
+        }
+#pragma unroll
+        for (int k = 0; k < PR_MAX_PEERS; ++k)
+            if (k < n) peer[k][off + v] = x;
+    }
 };
 
 // per-block statistics of the drain (ints: nact, work, push_ops, push_dang,
@@ -99,7 +134,7 @@ __device__ __forceinline__ PartIn part_load(const PartArgs &A, int32_t v) {
 }
 
 // h_v = (drained last state ? 0 : h_v) + inflow, then the drain
-__device__ __forceinline__ void part_finish(const PartArgs &A, const PartIn &q, double sum, double *s_mine,
+__device__ __forceinline__ void part_finish(const PartArgs &A, const PartIn &q, double sum, const ShareOut &out,
                                             Partial &p) {
     const int64_t v = q.v;
     const double hv = __dadd_rn(q.act ? 0.0 : q.h, sum);
@@ -119,14 +154,14 @@ __device__ __forceinline__ void part_finish(const PartArgs &A, const PartIn &q, 
         const int32_t len = __ldg(&A.row_len[v]);
         A.reserved[v] = __dadd_rn(q.rv, hv);
         A.h[v] = hv;
-        s_mine[v] = len > 0 ? __ddiv_rn(__dmul_rn(A.c, hv), (double)q.dv) : 0.0;
+        out.store(v, len > 0 ? __ddiv_rn(__dmul_rn(A.c, hv), (double)q.dv) : 0.0);
         p.nact += 1;
         p.work += (int64_t)q.dv + 1;
         p.push_ops += len;
         p.push_dang += __ldg(&A.dtc[v]);
     } else {
         A.h[v] = hv;
-        s_mine[v] = 0.0;
+        out.store(v, 0.0);
     }
 }
 
@@ -192,7 +227,7 @@ __global__ void __launch_bounds__(256) k_part_round(PartArgs A, const double *__
 struct PartRows {
     const PartArgs &A;
     const int32_t *ids;
-    double *s_mine;
+    const ShareOut &s_mine;
     Partial &p;
     __device__ __forceinline__ PartIn pre(bool valid, int64_t row) const {
         if (valid) return part_load(A, __ldg(&ids[row]));
@@ -214,7 +249,7 @@ struct PartRows {
 template <bool STREAM, bool PREFETCH>
 __global__ void __launch_bounds__(256, PREFETCH ? 3 : 4) k_part_pull(PartArgs A, BinView T, const int32_t *outside,
                                                                     int64_t n_outside, const double *__restrict__ s_full,
-                                                                    double *s_mine) {
+                                                                    const ShareOut s_mine) {
     Partial p;
     zero(p);
     const Src src{s_full, s_full, 0, 0};
@@ -231,6 +266,26 @@ __global__ void __launch_bounds__(256, PREFETCH ? 3 : 4) k_part_pull(PartArgs A,
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_outside;
          i += (int64_t)gridDim.x * blockDim.x)
         part_finish(A, part_load(A, __ldg(&outside[i])), 0.0, s_mine, p);
+    if (s_mine.n) __threadfence_system();   // peer stores performed before the round's barrier
+    block_reduce(p);
+    if (threadIdx.x == 0) A.partials[blockIdx.x] = p;
+}
+
+// state 0 (h = 1) of the fast form: shares through the ShareOut
+__global__ void __launch_bounds__(256) k_part_init_fast(PartArgs A, const ShareOut out) {
+    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    Partial p;
+    zero(p);
+    if (v < A.owned) {
+        A.reserved[v] = 0.0;
+        PartIn q = part_load(A, (int32_t)v);
+        q.h = 1.0;
+        q.rv = 0.0;
+        q.act = false;
+        A.h[v] = 1.0;
+        part_finish(A, q, 0.0, out, p);
+    }
+    if (out.n) __threadfence_system();
     block_reduce(p);
     if (threadIdx.x == 0) A.partials[blockIdx.x] = p;
 }
@@ -467,6 +522,102 @@ static BinView part_view(Part &P) {
     return T;
 }
 
+static void launch_part_pull(Part &P, const double *s_full, const ShareOut &so) {
+    cudaStream_t st = P.ctx->stream;
+    const unsigned g = (unsigned)P.blocks;
+    const int32_t *out = P.outside.as<int32_t>();
+    const int64_t no = P.n_outside;
+    if (P.stream_csc) {
+        if (P.prefetch) k_part_pull<true, true><<<g, 256, 0, st>>>(args_of(P), part_view(P), out, no, s_full, so);
+        else k_part_pull<true, false><<<g, 256, 0, st>>>(args_of(P), part_view(P), out, no, s_full, so);
+    } else {
+        if (P.prefetch) k_part_pull<false, true><<<g, 256, 0, st>>>(args_of(P), part_view(P), out, no, s_full, so);
+        else k_part_pull<false, false><<<g, 256, 0, st>>>(args_of(P), part_view(P), out, no, s_full, so);
+    }
+}
+
+// ---- fused exchange: share replicas in peer memory ----------------------
+
+int part_share_buffers(Part &P, int parts, int rank, void **d_full, void *ipc) {
+    if (parts < 1 || parts > PR_MAX_PEERS || rank < 0 || rank >= parts)
+        return fail(PR_ERR_ARG, "fused exchange: need 1 <= parts <= 8 and 0 <= rank < parts");
+    P.parts = parts;
+    P.rank = rank;
+    const size_t bytes = 8 * (size_t)P.slot * (size_t)parts;
+    for (int k = 0; k < 2; ++k) {
+        if (!P.own_full[k]) {
+            // plain cudaMalloc: IPC handles need it (pool allocations are not exportable this way)
+            PR_CUDA(cudaMalloc(&P.own_full[k], bytes));
+            PR_CUDA(cudaMemset(P.own_full[k], 0, bytes));
+        }
+        d_full[k] = P.own_full[k];
+        if (ipc) PR_CUDA(cudaIpcGetMemHandle((cudaIpcMemHandle_t *)ipc + k, P.own_full[k]));
+    }
+    for (int r = 0; r < PR_MAX_PEERS; ++r) P.peer[0][r] = P.peer[1][r] = nullptr;
+    P.peer[0][rank] = (double *)P.own_full[0];
+    P.peer[1][rank] = (double *)P.own_full[1];
+    return PR_OK;
+}
+
+int part_set_peers(Part &P, const void *handles) {
+    if (P.parts < 1) return fail(PR_ERR_STATE, "fused exchange: call pr_part_share_buffers first");
+    const cudaIpcMemHandle_t *h = (const cudaIpcMemHandle_t *)handles;
+    for (int r = 0; r < P.parts; ++r) {
+        if (r == P.rank) continue;
+        for (int k = 0; k < 2; ++k) {
+            void *ptr = nullptr;
+            PR_CUDA(cudaIpcOpenMemHandle(&ptr, h[2 * r + k], cudaIpcMemLazyEnablePeerAccess));
+            P.peer[k][r] = (double *)ptr;
+            P.opened.push_back(ptr);
+        }
+    }
+    return PR_OK;
+}
+
+// same-process emulation (tests): the ranks' replicas are device pointers
+int part_set_peer_ptrs(Part &P, int parts, int rank, void *const *ptrs) {
+    if (parts < 1 || parts > PR_MAX_PEERS || rank < 0 || rank >= parts)
+        return fail(PR_ERR_ARG, "fused exchange: need 1 <= parts <= 8 and 0 <= rank < parts");
+    P.parts = parts;
+    P.rank = rank;
+    for (int r = 0; r < parts; ++r) {
+        P.peer[0][r] = (double *)ptrs[2 * r];
+        P.peer[1][r] = (double *)ptrs[2 * r + 1];
+    }
+    return PR_OK;
+}
+
+static ShareOut fused_out(Part &P, int parity) {
+    ShareOut so;
+    memset(&so, 0, sizeof(so));
+    so.n = P.parts;
+    so.off = (int64_t)P.rank * P.slot;
+    for (int r = 0; r < P.parts; ++r) so.peer[r] = P.peer[parity][r];
+    return so;
+}
+
+int part_init_fused(Part &P, double *d_stats9) {
+    if (P.parts < 1 || !P.peer[0][P.rank]) return fail(PR_ERR_STATE, "fused exchange not set up");
+    PR_TRY(ensure_part_sched(P));
+    cudaStream_t st = P.ctx->stream;
+    const unsigned g = grid_for(P.owned, 256);
+    k_part_init_fast<<<g, 256, 0, st>>>(args_of(P), fused_out(P, 0));
+    k_part_reduce<<<1, 256, 0, st>>>(P.partials.as<Partial>(), g, P.stats.as<Partial>(), d_stats9, P.unit_ctr);
+    PR_CUDA(cudaGetLastError());
+    return PR_OK;
+}
+
+// round reading this rank's replica `parity`, writing every replica 1-parity
+int part_round_fused(Part &P, int parity, double *d_stats9) {
+    if (P.parts < 1 || !P.peer[0][P.rank]) return fail(PR_ERR_STATE, "fused exchange not set up");
+    PR_TRY(ensure_part_sched(P));
+    launch_part_pull(P, P.peer[parity & 1][P.rank], fused_out(P, 1 - (parity & 1)));
+    k_part_reduce<<<1, 256, 0, P.ctx->stream>>>(P.partials.as<Partial>(), (unsigned)P.blocks, P.stats.as<Partial>(),
+                                                d_stats9, P.unit_ctr);
+    PR_CUDA(cudaGetLastError());
+    return PR_OK;
+}
+
 int part_init_device(Part &P, double *d_s_mine, double *d_stats9) {
     unsigned g = grid_for(P.owned, 256);
     cudaStream_t st = P.ctx->stream;
@@ -482,15 +633,10 @@ int part_round_device(Part &P, const double *d_s_full, double *d_s_mine, int fas
     if (fast) {
         PR_TRY(ensure_part_sched(P));
         g = (unsigned)P.blocks;
-        const int32_t *out = P.outside.as<int32_t>();
-        const int64_t no = P.n_outside;
-        if (P.stream_csc) {
-            if (P.prefetch) k_part_pull<true, true><<<g, 256, 0, st>>>(args_of(P), part_view(P), out, no, d_s_full, d_s_mine);
-            else k_part_pull<true, false><<<g, 256, 0, st>>>(args_of(P), part_view(P), out, no, d_s_full, d_s_mine);
-        } else {
-            if (P.prefetch) k_part_pull<false, true><<<g, 256, 0, st>>>(args_of(P), part_view(P), out, no, d_s_full, d_s_mine);
-            else k_part_pull<false, false><<<g, 256, 0, st>>>(args_of(P), part_view(P), out, no, d_s_full, d_s_mine);
-        }
+        ShareOut so;
+        memset(&so, 0, sizeof(so));
+        so.mine = d_s_mine;
+        launch_part_pull(P, d_s_full, so);
     } else {
         g = grid_for(P.owned, 256);
         k_part_round<<<g, 256, 0, st>>>(args_of(P), d_s_full, d_s_mine);

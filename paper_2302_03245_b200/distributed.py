@@ -261,7 +261,7 @@ def run_partitioned(step, comm, part: Partition, algorithm: str, damping: float,
 
 def run_partitioned_queued(step, comm, part: Partition, algorithm: str, damping: float, threshold: float,
                            max_rounds: int = 1_000_000, conv_scope_all: bool = False, batch: int = 8,
-                           graph: bool | None = None, host_values: bool = True):
+                           graph: bool | None = None, host_values: bool = True, fused: bool = False):
     """``run_partitioned`` with the rounds queued on the device: each round
     is the local step, the all-gather of its shares and an in-place
     all-reduce of its 9 statistics (a row of a device buffer), all issued on
@@ -278,6 +278,12 @@ def run_partitioned_queued(step, comm, part: Partition, algorithm: str, damping:
     on the library stream and replayed for every later batch (and solve), so
     a round costs no host launches.  Batches start at even rounds, so the
     share-buffer parities of a replay are those of the capture.
+
+    ``fused=True`` (CudaLocalStep after ``setup_fused``): no all-gather --
+    the round kernel stores its shares into every rank's replica through
+    peer memory, and the statistics all-reduce is the round's barrier
+    (no rank starts round t+1, which overwrites the replicas round t reads,
+    before every rank has finished round t).
 
     ``host_values=False`` leaves the owned result on the device (the step's
     reserved/pending buffers) and returns None for it: the timed solve of
@@ -307,9 +313,9 @@ def run_partitioned_queued(step, comm, part: Partition, algorithm: str, damping:
 
     with ctx:
         cache = getattr(step, "_queued", None) if graph else None
-        if cache is None or cache["batch"] != batch:
+        if cache is None or cache["batch"] != batch or cache["fused"] != fused:
             full = [torch.zeros(S * P, dtype=torch.float64, device=dev) for _ in range(2)]
-            cache = {"batch": batch, "full": full, "mine": [f[part.rank * S:(part.rank + 1) * S] for f in full],
+            cache = {"batch": batch, "fused": fused, "full": full, "mine": [f[part.rank * S:(part.rank + 1) * S] for f in full],
                      "stats": torch.zeros((batch, 9), dtype=torch.float64, device=dev), "graph": None}
             if graph:
                 step._queued = cache
@@ -318,8 +324,11 @@ def run_partitioned_queued(step, comm, part: Partition, algorithm: str, damping:
         def queue_batch(nb, t0):
             for j in range(nb):
                 tt = t0 + j
-                step.round_device(full[tt & 1], mine[(tt + 1) & 1], stats[j])
-                comm.allgather_slots(full[(tt + 1) & 1], mine[(tt + 1) & 1])
+                if fused:
+                    step.round_fused(tt & 1, stats[j])
+                else:
+                    step.round_device(full[tt & 1], mine[(tt + 1) & 1], stats[j])
+                    comm.allgather_slots(full[(tt + 1) & 1], mine[(tt + 1) & 1])
                 comm.allreduce_row(stats[j])
 
         def run_batch(t0):
@@ -339,8 +348,11 @@ def run_partitioned_queued(step, comm, part: Partition, algorithm: str, damping:
                 cache["graph"].replay()
             return batch
 
-        step.init_device(mine[0], stats[0])
-        comm.allgather_slots(full[0], mine[0])
+        if fused:
+            step.init_fused(stats[0])
+        else:
+            step.init_device(mine[0], stats[0])
+            comm.allgather_slots(full[0], mine[0])
         comm.allreduce_row(stats[0])
         nact = record(stats[0].cpu().numpy())
         t = 0
@@ -568,6 +580,49 @@ class CudaLocalStep:
                                                     self._ct.c_void_p(s_mine.data_ptr()), int(self.fast),
                                                     self._ct.c_void_p(stats_row.data_ptr())),
                         "pr_part_round_device")
+
+    # -- fused exchange (run_partitioned_queued(fused=True)): replicas of the
+    # full share vector in peer memory, written by the round kernel itself
+    def share_buffers(self, parts: int, rank: int, ipc=None):
+        full = (self._ct.c_void_p * 2)()
+        self._lib.check(self.L.pr_part_share_buffers(self.h, int(parts), int(rank), full, ipc),
+                        "pr_part_share_buffers")
+        return full[0], full[1]
+
+    def setup_fused(self, comm) -> bool:
+        """Allocate this rank's replicas and map every other rank's (CUDA IPC
+        handles exchanged over the process group).  Collective: every rank
+        calls it, and it returns True on all ranks or False on all (then the
+        caller keeps the all-gather form)."""
+        parts, rank = self.part.parts, self.part.rank
+        ipc = self._ct.create_string_buffer(128)
+        try:
+            self.share_buffers(parts, rank, ipc)
+            mine = ipc.raw
+        except Exception:   # noqa: BLE001 -- reported through the collective decision
+            mine = None
+        handles = [None] * parts
+        comm.dist.all_gather_object(handles, mine)
+        ok = all(h is not None for h in handles)
+        if ok:
+            blob = self._ct.create_string_buffer(b"".join(handles), 128 * parts)
+            ok = self.L.pr_part_set_peers(self.h, blob) == self._lib.PR_OK
+        flag = self.torch.tensor([1.0 if ok else 0.0], dtype=self.torch.float64,
+                                 device=self.dev if comm.dist.get_backend() == "nccl" else "cpu")
+        comm.dist.all_reduce(flag, op=comm.dist.ReduceOp.MIN)
+        return bool(flag.item() > 0.5)
+
+    def set_peer_ptrs(self, parts: int, rank: int, ptrs) -> None:
+        arr = (self._ct.c_void_p * len(ptrs))(*ptrs)
+        self._lib.check(self.L.pr_part_set_peer_ptrs(self.h, int(parts), int(rank), arr), "pr_part_set_peer_ptrs")
+
+    def init_fused(self, stats_row):
+        self._lib.check(self.L.pr_part_init_fused(self.h, self._ct.c_void_p(stats_row.data_ptr())),
+                        "pr_part_init_fused")
+
+    def round_fused(self, parity: int, stats_row):
+        self._lib.check(self.L.pr_part_round_fused(self.h, int(parity), self._ct.c_void_p(stats_row.data_ptr())),
+                        "pr_part_round_fused")
 
     def settle_shares(self, x_mine):
         out = self._out(x_mine)

@@ -7,3 +7,4 @@ PUSHRANK_PARTITIONED=1 timeout 600 python -m torch.distributed.run --nnodes=1 --
 done
 PUSHRANK_DIST_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --steps 3 --warmup 3 > ${OUT:-gpurun_out/part}/gloo2_c2.json 2> ${OUT:-gpurun_out/part}/gloo2_c2.err
 PUSHRANK_PARTITIONED=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29513 bench.py --steps 2 --warmup 3 --config c5 > ${OUT:-gpurun_out/part}/part1_c5.json 2> ${OUT:-gpurun_out/part}/part1_c5.err
+PUSHRANK_FUSED=0 PUSHRANK_PARTITIONED=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29514 bench.py --steps 5 --warmup 3 --config c3 > ${OUT:-gpurun_out/part}/part1_c3_gathered.json 2> ${OUT:-gpurun_out/part}/part1_c3_gathered.err
