@@ -264,12 +264,20 @@ int pr_part_round(pr_part *p, const double *d_shares_full, double *d_shares_mine
  * converged_scan}, ready for an in-place device all-reduce.  fast = 1 runs
  * the single-GPU dense-round gather (degree-binned schedule of the
  * receiving rows, deterministic but not ascending-source order); fast = 0
- * the exact ascending-source sums of pr_part_round.  Work is queued on the
+ * the exact ascending-source sums of pr_part_round.  kind (fast form):
+ * 0 Jacobi, 1 transition, 2 Gauss-Seidel -- the sweep kinds of rank-local
+ * sections on large IFP2 partitions (round 0 after init is Jacobi, round 1
+ * the transition, later rounds GS; without sections kind is ignored).
+ * Work is queued on the
  * library stream (pr_part_stream), which the caller orders its collectives
  * on. */
+/* The partition's rank among `parts` (its padded slot rank*slot): needed by
+ * the fast form before the first round (rank-local Gauss-Seidel sections);
+ * the fused-exchange setup sets it too. */
+int pr_part_set_rank(pr_part *p, int32_t parts, int32_t rank);
 int pr_part_init_device(pr_part *p, double *d_shares_mine, double *d_stats);
 int pr_part_round_device(pr_part *p, const double *d_shares_full, double *d_shares_mine, int32_t fast,
-                         double *d_stats);
+                         int32_t kind, double *d_stats);
 int pr_part_stream(pr_part *p, void **stream);
 /* Fused exchange (one process per GPU over NVLink/NVSwitch): the round
  * kernel stores every drained share straight into every rank's replica of
@@ -288,7 +296,7 @@ int pr_part_share_buffers(pr_part *p, int32_t parts, int32_t rank, void **d_full
 int pr_part_set_peers(pr_part *p, const void *ipc_handles);
 int pr_part_set_peer_ptrs(pr_part *p, int32_t parts, int32_t rank, void *const *d_full);
 int pr_part_init_fused(pr_part *p, double *d_stats);
-int pr_part_round_fused(pr_part *p, int32_t parity, double *d_stats);
+int pr_part_round_fused(pr_part *p, int32_t parity, int32_t kind, double *d_stats);
 int pr_part_settle_shares(pr_part *p, double *d_x_mine);
 int pr_part_settle(pr_part *p, const double *d_x_full, int64_t *settled, int64_t *ints, double *floats);
 int pr_part_total(pr_part *p, int32_t include_pending, double *total);

@@ -118,13 +118,14 @@ SIGNATURES = {
     "pr_part_init": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "pr_part_round": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pr_part_init_device": (ctypes.c_int, [c_vp, c_vp, c_vp]),
-    "pr_part_round_device": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_vp]),
+    "pr_part_round_device": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
     "pr_part_stream": (ctypes.c_int, [c_vp, _PP]),
     "pr_part_share_buffers": (ctypes.c_int, [c_vp, c_i32, c_i32, c_vp, c_vp]),
     "pr_part_set_peers": (ctypes.c_int, [c_vp, c_vp]),
     "pr_part_set_peer_ptrs": (ctypes.c_int, [c_vp, c_i32, c_i32, c_vp]),
+    "pr_part_set_rank": (ctypes.c_int, [c_vp, c_i32, c_i32]),
     "pr_part_init_fused": (ctypes.c_int, [c_vp, c_vp]),
-    "pr_part_round_fused": (ctypes.c_int, [c_vp, c_i32, c_vp]),
+    "pr_part_round_fused": (ctypes.c_int, [c_vp, c_i32, c_i32, c_vp]),
     "pr_part_settle_shares": (ctypes.c_int, [c_vp, c_vp]),
     "pr_part_settle": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pr_part_total": (ctypes.c_int, [c_vp, c_i32, ctypes.POINTER(c_f64)]),

@@ -34,15 +34,20 @@ __device__ __forceinline__ int ld_idx(const int32_t *p) {
 __device__ __forceinline__ double ld_share(const double *p) { return __ldg(p); }
 
 // Share sources of a dense round (rounds.cu, Gauss-Seidel sections):
-//   Jacobi      gs_lo = tr_lo = 0:      x[u]
-//   GS sweep    gs_lo = section start:  u < gs_lo ? x_new[u] : x[u]
-//   transition  tr_lo = gs_lo:          x[u] + (u < gs_lo ? x_new[u] : 0)
+//   Jacobi      gs_lo = 0:              x[u]
+//   GS sweep    gs_lo = section start:  early(u) ? x_new[u] : x[u]
+//   transition                          x[u] + (early(u) ? x_new[u] : 0)
 // x holds the shares still owed to this row, x_new the shares drained
-// earlier in the same sweep (sources of earlier sections).
+// earlier in the same sweep (sources of earlier sections):
+// early(u) = base <= u < base + gs_lo, with base = 0 on one GPU and the
+// rank's first padded id in a partition (part.cu: sections are rank-local,
+// other ranks' sources always read x).
 struct Src {
     const double *x, *x_new;
-    int gs_lo, tr_lo;
+    int gs_lo, base;
 };
+
+__device__ __forceinline__ bool early(const Src &S, int idx) { return (unsigned)(idx - S.base) < (unsigned)S.gs_lo; }
 
 // SRC: 0 Jacobi only (plain x), 1 section sweep (select), 2 transition
 template <int SRC>
@@ -50,9 +55,9 @@ __device__ __forceinline__ double ld_src(const Src S, int idx) {
     if constexpr (SRC == 0) {
         return ld_share(S.x + idx);
     } else if constexpr (SRC == 1) {
-        return ld_share((idx < S.gs_lo ? S.x_new : S.x) + idx);
+        return ld_share((early(S, idx) ? S.x_new : S.x) + idx);
     } else {
-        return ld_share(S.x + idx) + (idx < S.gs_lo ? ld_share(S.x_new + idx) : 0.0);
+        return ld_share(S.x + idx) + (early(S, idx) ? ld_share(S.x_new + idx) : 0.0);
     }
 }
 

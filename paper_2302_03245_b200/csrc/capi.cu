@@ -59,12 +59,13 @@ void part_destroy(Part *P);
 Ctx &part_ctx(Part &P);
 void *part_stream(Part &P);
 int part_init_device(Part &P, double *d_s_mine, double *d_stats9);
-int part_round_device(Part &P, const double *d_s_full, double *d_s_mine, int fast, double *d_stats9);
+int part_round_device(Part &P, const double *d_s_full, double *d_s_mine, int fast, int kind, double *d_stats9);
 int part_share_buffers(Part &P, int parts, int rank, void **d_full, void *ipc);
 int part_set_peers(Part &P, const void *handles);
 int part_set_peer_ptrs(Part &P, int parts, int rank, void *const *ptrs);
+int part_set_rank(Part &P, int parts, int rank);
 int part_init_fused(Part &P, double *d_stats9);
-int part_round_fused(Part &P, int parity, double *d_stats9);
+int part_round_fused(Part &P, int parity, int kind, double *d_stats9);
 
 static int set_device(Ctx &ctx) {
     PR_CUDA(cudaSetDevice(ctx.device));
@@ -563,10 +564,10 @@ int pr_part_init_device(pr_part *p, double *d_shares_mine, double *d_stats) {
     return part_init_device(*p->p, d_shares_mine, d_stats);
 }
 int pr_part_round_device(pr_part *p, const double *d_shares_full, double *d_shares_mine, int32_t fast,
-                         double *d_stats) {
+                         int32_t kind, double *d_stats) {
     PART_ENTER(p);
     CHECK_PTR(d_stats, "stats");
-    return part_round_device(*p->p, d_shares_full, d_shares_mine, fast, d_stats);
+    return part_round_device(*p->p, d_shares_full, d_shares_mine, fast, kind, d_stats);
 }
 int pr_part_share_buffers(pr_part *p, int32_t parts, int32_t rank, void **d_full, void *ipc_handles) {
     PART_ENTER(p);
@@ -578,6 +579,10 @@ int pr_part_set_peers(pr_part *p, const void *ipc_handles) {
     CHECK_PTR(ipc_handles, "ipc_handles");
     return part_set_peers(*p->p, ipc_handles);
 }
+int pr_part_set_rank(pr_part *p, int32_t parts, int32_t rank) {
+    PART_ENTER(p);
+    return part_set_rank(*p->p, parts, rank);
+}
 int pr_part_set_peer_ptrs(pr_part *p, int32_t parts, int32_t rank, void *const *d_full) {
     PART_ENTER(p);
     CHECK_PTR(d_full, "d_full");
@@ -588,10 +593,10 @@ int pr_part_init_fused(pr_part *p, double *d_stats) {
     CHECK_PTR(d_stats, "stats");
     return part_init_fused(*p->p, d_stats);
 }
-int pr_part_round_fused(pr_part *p, int32_t parity, double *d_stats) {
+int pr_part_round_fused(pr_part *p, int32_t parity, int32_t kind, double *d_stats) {
     PART_ENTER(p);
     CHECK_PTR(d_stats, "stats");
-    return part_round_fused(*p->p, parity, d_stats);
+    return part_round_fused(*p->p, parity, kind, d_stats);
 }
 int pr_part_stream(pr_part *p, void **stream) {
     PART_ENTER(p);

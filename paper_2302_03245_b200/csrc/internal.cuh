@@ -228,7 +228,10 @@ int error_report(Ctx &ctx, const double *d_est, const double *d_ref, int64_t n, 
 
 constexpr int TILE = 256;   // edges per warp tile (long rows are cut into TILE chunks)
 constexpr int CSC_PAD = 1024;  // int32 padding past the compacted CSC for vector loads
-constexpr int64_t THREAD_DEG = 32;   // rows up to this in-degree: one thread each
+#ifndef PR_THREAD_DEG
+#define PR_THREAD_DEG 32
+#endif
+constexpr int64_t THREAD_DEG = PR_THREAD_DEG;   // rows up to this in-degree: one thread each
 #ifndef PR_HUB_CHUNK
 #define PR_HUB_CHUNK 4096
 #endif

@@ -62,6 +62,7 @@ struct Part {
     int64_t blocks = 0;       // persistent pull grid
     bool stream_csc = false;  // evict-first index loads (round working set > 0.6 L2)
     bool prefetch = false;    // drain inputs ahead of the gathers (round working set < 4 L2)
+    int nsec = 1;             // rank-local Gauss-Seidel sections (IFP2, rows == local ids)
     DevBuf outside;           // int32: owned vertices outside the schedule
     int64_t n_outside = 0;
     // fused exchange: replicas of the full share vector (parity 0/1) of
@@ -246,29 +247,48 @@ struct PartRows {
     }
 };
 
-template <bool STREAM, bool PREFETCH>
-__global__ void __launch_bounds__(256, PREFETCH ? 3 : 4) k_part_pull(PartArgs A, BinView T, const int32_t *outside,
-                                                                    int64_t n_outside, const double *__restrict__ s_full,
-                                                                    const ShareOut s_mine) {
-    Partial p;
-    zero(p);
-    const Src src{s_full, s_full, 0, 0};
+// One launch of a round: the units [u_lo, u_hi) of one Gauss-Seidel section
+// (all of them without sections).  kind: 0 Jacobi, 1 transition, 2 GS
+// (bins.cuh Src: sections are rank-local, early(u) tests this rank's padded
+// slot); the last section also drains the vertices outside the schedule.
+// Each section writes its block partials to its own region.
+struct PullSec {
+    int64_t u_lo, u_hi;
+    Src src;
+    int kind, last, region;
+};
+
+template <bool STREAM, bool PREFETCH, int SRC>
+__device__ __forceinline__ void part_bins(const PartArgs &A, const BinView &T, const PullSec &S, const ShareOut &s_mine,
+                                          Partial &p) {
     PartRows rows{A, T.ids, s_mine, p};
     if constexpr (PREFETCH) {
-        bins_run<STREAM, true, 0>(T, 0, T.n_units, src, rows);
+        bins_run<STREAM, true, SRC>(T, S.u_lo, S.u_hi, S.src, rows);
     } else {
         auto thread_row = [&](bool valid, int64_t row, double sum) {
             if (valid) part_finish(A, part_load(A, __ldg(&T.ids[row])), sum, s_mine, p);
         };
         auto single_row = [&](int64_t row, double sum) { rows.single(row, sum); };
-        bins_run_plain<STREAM, 0>(T, 0, T.n_units, src, thread_row, single_row);
+        bins_run_plain<STREAM, SRC>(T, S.u_lo, S.u_hi, S.src, thread_row, single_row);
     }
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_outside;
-         i += (int64_t)gridDim.x * blockDim.x)
-        part_finish(A, part_load(A, __ldg(&outside[i])), 0.0, s_mine, p);
+}
+
+template <bool STREAM, bool PREFETCH>
+__global__ void __launch_bounds__(256, PREFETCH ? 3 : 4) k_part_pull(PartArgs A, BinView T, const int32_t *outside,
+                                                                    int64_t n_outside, const PullSec S,
+                                                                    const ShareOut s_mine) {
+    Partial p;
+    zero(p);
+    if (S.kind == 0) part_bins<STREAM, PREFETCH, 0>(A, T, S, s_mine, p);
+    else if (S.kind == 1) part_bins<STREAM, PREFETCH, 2>(A, T, S, s_mine, p);
+    else part_bins<STREAM, PREFETCH, 1>(A, T, S, s_mine, p);
+    if (S.last)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_outside;
+             i += (int64_t)gridDim.x * blockDim.x)
+            part_finish(A, part_load(A, __ldg(&outside[i])), 0.0, s_mine, p);
     if (s_mine.n) __threadfence_system();   // peer stores performed before the round's barrier
     block_reduce(p);
-    if (threadIdx.x == 0) A.partials[blockIdx.x] = p;
+    if (threadIdx.x == 0) A.partials[(int64_t)S.region * gridDim.x + blockIdx.x] = p;
 }
 
 // state 0 (h = 1) of the fast form: shares through the ShareOut
@@ -334,7 +354,7 @@ __global__ void __launch_bounds__(256) k_part_total(PartArgs A, int include_h) {
 // one block: fixed-order reduction of the block partials; optionally the 9
 // statistics as doubles for a device all-reduce, and the unit counter reset
 __global__ void k_part_reduce(const Partial *partials, int64_t blocks, Partial *out, double *out9,
-                              unsigned long long *unit_ctr) {
+                              unsigned long long *unit_ctr, int nctr = 1) {
     Partial acc;
     zero(acc);
     for (int64_t b = threadIdx.x; b < blocks; b += blockDim.x) add(acc, partials[b]);
@@ -352,7 +372,8 @@ __global__ void k_part_reduce(const Partial *partials, int64_t blocks, Partial *
             out9[7] = (double)acc.conv_all;
             out9[8] = (double)acc.conv_scan;
         }
-        if (unit_ctr) *unit_ctr = 0;
+        if (unit_ctr)
+            for (int k = 0; k < nctr; ++k) unit_ctr[k] = 0;
     }
 }
 
@@ -442,15 +463,21 @@ int part_create(Ctx &ctx, int64_t owned, int64_t slot, const int64_t *in_off, co
         if ((rc = ensure(P->h, 8 * (owned ? owned : 1)))) break;
         if ((rc = ensure(P->reserved, 8 * (owned ? owned : 1)))) break;
         if ((rc = ensure(P->act, owned ? owned : 1))) break;
-        if ((rc = ensure(P->partials, sizeof(Partial) * (grid_for(owned, 256) + (int64_t)ctx.sm_count * 8 + 1)))) break;
-        if ((rc = ensure(P->stats, sizeof(Partial) + 64))) break;
+        if ((rc = ensure(P->partials, sizeof(Partial) * (grid_for(owned, 256) +
+                                                         (int64_t)ctx.sm_count * 4 * PR_MAX_SECTIONS + 1))))
+            break;
+        if ((rc = ensure(P->stats, sizeof(Partial) + 32 + 8 * PR_MAX_SECTIONS))) break;
         P->unit_ctr = (unsigned long long *)(P->stats.as<char>() + sizeof(Partial) + 32);
-        cudaMemsetAsync(P->unit_ctr, 0, 8, ctx.stream);
+        cudaMemsetAsync(P->unit_ctr, 0, 8 * PR_MAX_SECTIONS, ctx.stream);
         if (cudaStreamSynchronize(ctx.stream) != cudaSuccess) rc = fail(PR_ERR_CUDA, "partition upload");
     } while (0);
     if (rc) { delete P; return rc; }
     *out = P;
     return PR_OK;
+}
+
+__global__ void k_ids_identity(const int32_t *ids, int64_t count, unsigned long long *bad) {
+    GRID_STRIDE(i, count) if (ids[i] != (int32_t)i) atomicAdd(bad, 1ull);
 }
 
 // the fast form's pull schedule, built on first use
@@ -479,7 +506,29 @@ static int ensure_part_sched(Part &P) {
         P.stream_csc = ws > 0.6 * l2;
         P.prefetch = ws < 4.0 * l2;
         P.blocks = (int64_t)ctx.sm_count * (P.prefetch ? 3 : 4);
-        if ((rc = ensure_units(*g, P.which, P.blocks, 1))) break;
+        // rank-local Gauss-Seidel sections, as the engine chooses them
+        // (rounds.cu): IFP2 on rows that are the local ids in order (a
+        // run-layout partition), 2 past 1.5x L2 of round working set, 4 past 16x
+        P.nsec = 1;
+        if (P.which == 1) {
+            P.nsec = ws > 16.0 * l2 ? 4 : ws > 1.5 * l2 ? 2 : 1;
+            if (const char *e = getenv("PUSHRANK_GS_SECTIONS")) P.nsec = atoi(e);
+            if (P.nsec < 1) P.nsec = 1;
+            if (P.nsec > PR_MAX_SECTIONS) P.nsec = PR_MAX_SECTIONS;
+            if (P.nsec > 1) {
+                auto &S = g->sched[P.which];
+                DevBuf bad;
+                if ((rc = ensure(bad, 8))) break;
+                cudaMemsetAsync(bad.ptr, 0, 8, st);
+                if (S.count) k_ids_identity<<<grid_for(S.count, 256), 256, 0, st>>>(S.ids.as<int32_t>(), S.count,
+                                                                                  bad.as<unsigned long long>());
+                unsigned long long nbad = 0;
+                cudaMemcpyAsync(&nbad, bad.ptr, 8, cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                if (nbad) P.nsec = 1;
+            }
+        }
+        if ((rc = ensure_units(*g, P.which, P.blocks, P.nsec))) break;
         // owned vertices outside the schedule: no inflow, drained alone
         {
             DevBuf cnt;
@@ -522,17 +571,33 @@ static BinView part_view(Part &P) {
     return T;
 }
 
-static void launch_part_pull(Part &P, const double *s_full, const ShareOut &so) {
+// one round: a launch per section; x = shares of the previous round (all
+// ranks), x_new = this round's full vector (own slot written by the earlier
+// sections); kind 0 Jacobi / 1 transition / 2 GS (ignored without sections)
+static void launch_part_pull(Part &P, const double *s_full, const double *x_new, int kind, const ShareOut &so) {
     cudaStream_t st = P.ctx->stream;
     const unsigned g = (unsigned)P.blocks;
     const int32_t *out = P.outside.as<int32_t>();
     const int64_t no = P.n_outside;
-    if (P.stream_csc) {
-        if (P.prefetch) k_part_pull<true, true><<<g, 256, 0, st>>>(args_of(P), part_view(P), out, no, s_full, so);
-        else k_part_pull<true, false><<<g, 256, 0, st>>>(args_of(P), part_view(P), out, no, s_full, so);
-    } else {
-        if (P.prefetch) k_part_pull<false, true><<<g, 256, 0, st>>>(args_of(P), part_view(P), out, no, s_full, so);
-        else k_part_pull<false, false><<<g, 256, 0, st>>>(args_of(P), part_view(P), out, no, s_full, so);
+    auto &Sc = P.sg->sched[P.which];
+    const int nsec = P.nsec > 1 ? P.nsec : 1;
+    for (int k = 0; k < nsec; ++k) {
+        PullSec S;
+        S.u_lo = nsec > 1 ? Sc.sec_unit[k] : 0;
+        S.u_hi = nsec > 1 ? Sc.sec_unit[k + 1] : Sc.n_units;
+        S.kind = nsec > 1 ? kind : 0;
+        S.src = Src{s_full, x_new, S.kind ? (int)Sc.sec_row[k] : 0, (int)((int64_t)P.rank * P.slot)};
+        S.last = k == nsec - 1;
+        S.region = k;
+        BinView T = part_view(P);
+        T.unit_ctr = P.unit_ctr + k;
+        if (P.stream_csc) {
+            if (P.prefetch) k_part_pull<true, true><<<g, 256, 0, st>>>(args_of(P), T, out, no, S, so);
+            else k_part_pull<true, false><<<g, 256, 0, st>>>(args_of(P), T, out, no, S, so);
+        } else {
+            if (P.prefetch) k_part_pull<false, true><<<g, 256, 0, st>>>(args_of(P), T, out, no, S, so);
+            else k_part_pull<false, false><<<g, 256, 0, st>>>(args_of(P), T, out, no, S, so);
+        }
     }
 }
 
@@ -560,7 +625,7 @@ int part_share_buffers(Part &P, int parts, int rank, void **d_full, void *ipc) {
 }
 
 int part_set_peers(Part &P, const void *handles) {
-    if (P.parts < 1) return fail(PR_ERR_STATE, "fused exchange: call pr_part_share_buffers first");
+    if (!P.own_full[0]) return fail(PR_ERR_STATE, "fused exchange: call pr_part_share_buffers first");
     const cudaIpcMemHandle_t *h = (const cudaIpcMemHandle_t *)handles;
     for (int r = 0; r < P.parts; ++r) {
         if (r == P.rank) continue;
@@ -571,6 +636,16 @@ int part_set_peers(Part &P, const void *handles) {
             P.opened.push_back(ptr);
         }
     }
+    return PR_OK;
+}
+
+// this partition's place among the ranks (the padded slot it owns: the
+// rank-local Gauss-Seidel test and the fused exchange's store offset)
+int part_set_rank(Part &P, int parts, int rank) {
+    if (parts < 1 || parts > PR_MAX_PEERS || rank < 0 || rank >= parts)
+        return fail(PR_ERR_ARG, "partition: need 1 <= parts <= 8 and 0 <= rank < parts");
+    P.parts = parts;
+    P.rank = rank;
     return PR_OK;
 }
 
@@ -608,12 +683,14 @@ int part_init_fused(Part &P, double *d_stats9) {
 }
 
 // round reading this rank's replica `parity`, writing every replica 1-parity
-int part_round_fused(Part &P, int parity, double *d_stats9) {
+int part_round_fused(Part &P, int parity, int kind, double *d_stats9) {
     if (P.parts < 1 || !P.peer[0][P.rank]) return fail(PR_ERR_STATE, "fused exchange not set up");
     PR_TRY(ensure_part_sched(P));
-    launch_part_pull(P, P.peer[parity & 1][P.rank], fused_out(P, 1 - (parity & 1)));
-    k_part_reduce<<<1, 256, 0, P.ctx->stream>>>(P.partials.as<Partial>(), (unsigned)P.blocks, P.stats.as<Partial>(),
-                                                d_stats9, P.unit_ctr);
+    launch_part_pull(P, P.peer[parity & 1][P.rank], P.peer[1 - (parity & 1)][P.rank], kind,
+                     fused_out(P, 1 - (parity & 1)));
+    k_part_reduce<<<1, 256, 0, P.ctx->stream>>>(P.partials.as<Partial>(),
+                                                (unsigned)(P.blocks * (P.nsec > 1 ? P.nsec : 1)),
+                                                P.stats.as<Partial>(), d_stats9, P.unit_ctr, PR_MAX_SECTIONS);
     PR_CUDA(cudaGetLastError());
     return PR_OK;
 }
@@ -627,7 +704,7 @@ int part_init_device(Part &P, double *d_s_mine, double *d_stats9) {
     return PR_OK;
 }
 
-int part_round_device(Part &P, const double *d_s_full, double *d_s_mine, int fast, double *d_stats9) {
+int part_round_device(Part &P, const double *d_s_full, double *d_s_mine, int fast, int kind, double *d_stats9) {
     cudaStream_t st = P.ctx->stream;
     unsigned g;
     if (fast) {
@@ -636,12 +713,15 @@ int part_round_device(Part &P, const double *d_s_full, double *d_s_mine, int fas
         ShareOut so;
         memset(&so, 0, sizeof(so));
         so.mine = d_s_mine;
-        launch_part_pull(P, d_s_full, so);
+        // d_s_mine is this rank's slot of the next round's full vector
+        launch_part_pull(P, d_s_full, d_s_mine - (int64_t)P.rank * P.slot, kind, so);
+        g = (unsigned)(P.blocks * (P.nsec > 1 ? P.nsec : 1));
     } else {
         g = grid_for(P.owned, 256);
         k_part_round<<<g, 256, 0, st>>>(args_of(P), d_s_full, d_s_mine);
     }
-    k_part_reduce<<<1, 256, 0, st>>>(P.partials.as<Partial>(), g, P.stats.as<Partial>(), d_stats9, P.unit_ctr);
+    k_part_reduce<<<1, 256, 0, st>>>(P.partials.as<Partial>(), g, P.stats.as<Partial>(), d_stats9, P.unit_ctr,
+                                     PR_MAX_SECTIONS);
     PR_CUDA(cudaGetLastError());
     return PR_OK;
 }

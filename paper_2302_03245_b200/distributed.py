@@ -325,9 +325,9 @@ def run_partitioned_queued(step, comm, part: Partition, algorithm: str, damping:
             for j in range(nb):
                 tt = t0 + j
                 if fused:
-                    step.round_fused(tt & 1, stats[j])
+                    step.round_fused(tt, stats[j])
                 else:
-                    step.round_device(full[tt & 1], mine[(tt + 1) & 1], stats[j])
+                    step.round_device(full[tt & 1], mine[(tt + 1) & 1], stats[j], tt)
                     comm.allgather_slots(full[(tt + 1) & 1], mine[(tt + 1) & 1])
                 comm.allreduce_row(stats[j])
 
@@ -337,10 +337,12 @@ def run_partitioned_queued(step, comm, part: Partition, algorithm: str, damping:
                 queue_batch(nb, t0)
                 return nb
             if cache["graph"] is None and t0 > 0:
-                # capture once the schedule exists (built by the first, eager batch)
+                # capture once the schedule exists (built by the first, eager
+                # batch); every later batch has the same parities and sweep
+                # kinds (Gauss-Seidel from round 2 on) as this one
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=stream):
-                    queue_batch(batch, 0)
+                    queue_batch(batch, t0)
                 cache["graph"] = g
             if cache["graph"] is None:
                 queue_batch(batch, t0)
@@ -385,6 +387,13 @@ def run_partitioned_queued(step, comm, part: Partition, algorithm: str, damping:
         values = step.values(total) if host_values else None
     return values, rows, {"rounds": t, "mass_total": total, "push_ops": push_ops,
                           "push_ops_dangling": push_dang, "settled": settled}
+
+
+def sweep_kind(t: int) -> int:
+    """Kind of round t (0-based, after the state-0 drain) for rank-local
+    Gauss-Seidel sections (csrc/part.cu, bins.cuh Src): 0 Jacobi (every share
+    owed to every target), 1 transition, 2 Gauss-Seidel."""
+    return 0 if t == 0 else 1 if t == 1 else 2
 
 
 def _stats_row(row, ints, floats) -> None:
@@ -441,8 +450,8 @@ class NumpyLocalStep:
     def init_device(self, s_mine, stats_row):
         _stats_row(stats_row, *self.init(s_mine))
 
-    def round_device(self, s_in, s_mine, stats_row):
-        _stats_row(stats_row, *self.round(None, s_in, s_mine))
+    def round_device(self, s_in, s_mine, stats_row, t: int = 0):
+        _stats_row(stats_row, *self.round(t, s_in, s_mine))
 
     def settle_shares(self, x_mine):
         p = self.p
@@ -518,6 +527,7 @@ class CudaLocalStep:
                                     _lib.ALGO[algorithm], float(damping), float(threshold), ctypes.byref(h)),
                    "pr_part_create")
         self.h = h
+        _lib.check(L.pr_part_set_rank(h, int(part.parts), int(part.rank)), "pr_part_set_rank")
         self.s_full = torch.zeros(part.slot * part.parts, dtype=torch.float64, device=self.dev)
         self.s_mine = torch.zeros(part.slot, dtype=torch.float64, device=self.dev)
 
@@ -575,10 +585,10 @@ class CudaLocalStep:
         self._lib.check(self.L.pr_part_init_device(self.h, self._ct.c_void_p(s_mine.data_ptr()),
                                                    self._ct.c_void_p(stats_row.data_ptr())), "pr_part_init_device")
 
-    def round_device(self, s_in, s_mine, stats_row):
+    def round_device(self, s_in, s_mine, stats_row, t: int = 0):
         self._lib.check(self.L.pr_part_round_device(self.h, self._ct.c_void_p(s_in.data_ptr()),
                                                     self._ct.c_void_p(s_mine.data_ptr()), int(self.fast),
-                                                    self._ct.c_void_p(stats_row.data_ptr())),
+                                                    sweep_kind(t), self._ct.c_void_p(stats_row.data_ptr())),
                         "pr_part_round_device")
 
     # -- fused exchange (run_partitioned_queued(fused=True)): replicas of the
@@ -620,9 +630,9 @@ class CudaLocalStep:
         self._lib.check(self.L.pr_part_init_fused(self.h, self._ct.c_void_p(stats_row.data_ptr())),
                         "pr_part_init_fused")
 
-    def round_fused(self, parity: int, stats_row):
-        self._lib.check(self.L.pr_part_round_fused(self.h, int(parity), self._ct.c_void_p(stats_row.data_ptr())),
-                        "pr_part_round_fused")
+    def round_fused(self, t: int, stats_row):
+        self._lib.check(self.L.pr_part_round_fused(self.h, int(t) & 1, sweep_kind(t),
+                                                   self._ct.c_void_p(stats_row.data_ptr())), "pr_part_round_fused")
 
     def settle_shares(self, x_mine):
         out = self._out(x_mine)
