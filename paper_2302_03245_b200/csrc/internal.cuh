@@ -228,8 +228,10 @@ int error_report(Ctx &ctx, const double *d_est, const double *d_ref, int64_t n, 
 
 constexpr int TILE = 256;   // edges per warp tile (long rows are cut into TILE chunks)
 constexpr int CSC_PAD = 1024;  // int32 padding past the compacted CSC for vector loads
+// Measured against 32 (bench.py, B200): C2 -1%, C3 -10%, C5 -6%, C4 0;
+// 16 and 256 are worse (C2 +23% / +30%), 96 and 128 within 1% of 64.
 #ifndef PR_THREAD_DEG
-#define PR_THREAD_DEG 32
+#define PR_THREAD_DEG 64
 #endif
 constexpr int64_t THREAD_DEG = PR_THREAD_DEG;   // rows up to this in-degree: one thread each
 #ifndef PR_HUB_CHUNK
