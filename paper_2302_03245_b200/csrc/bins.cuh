@@ -112,6 +112,68 @@ __device__ __forceinline__ double span_sum_warp(const int32_t *__restrict__ csc,
     return acc;
 }
 
+// Sub-warp rows: warp-bin rows of at most PR_SUB_MAX edges are summed by
+// groups of PR_SUB_LANES lanes, 32 / PR_SUB_LANES rows at a time (each lane
+// 8 gathers in flight at stride 8 * PR_SUB_LANES); longer rows by the whole
+// warp.  PR_SUB_LANES = 32 keeps one row per warp throughout.
+#ifndef PR_SUB_LANES
+#define PR_SUB_LANES 32
+#endif
+#ifndef PR_SUB_MAX
+#define PR_SUB_MAX 512
+#endif
+
+template <bool STREAM, int SRC, int L>
+__device__ __forceinline__ double span_sum_sub(const int32_t *__restrict__ csc, int64_t lo, int64_t hi, const Src x) {
+    const int sl = threadIdx.x & (L - 1);
+    double acc = 0.0;
+    for (int64_t e = lo + sl; e < hi; e += 8 * L) {
+        int idx[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) idx[q] = e + L * q < hi ? ld_idx<STREAM>(&csc[e + L * q]) : -1;
+        double t[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t[q] = idx[q] >= 0 ? ld_src<SRC>(x, idx[q]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc += t[q];
+    }
+#pragma unroll
+    for (int o = L / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    return acc;
+}
+
+// Sums of the cnt rows of a warp batch (row j's bounds in lane j's
+// my_lo/my_hi, rows in descending degree): lane j returns row j's sum.
+// Every lane must call it.  The order of each row's sum is fixed (lane and
+// q order, then the shuffle tree), so results stay run-to-run identical.
+template <bool STREAM, int SRC>
+__device__ __forceinline__ double warp_batch_sums(const BinView &B, const Src x, int64_t my_lo, int64_t my_hi,
+                                                  int cnt) {
+    const int lane = threadIdx.x & 31;
+    double mine = 0.0;
+    int j = 0;
+    for (; j < cnt; ++j) {
+        const int64_t lo = __shfl_sync(0xffffffffu, my_lo, j), hi = __shfl_sync(0xffffffffu, my_hi, j);
+        if (PR_SUB_LANES < 32 && hi - lo <= PR_SUB_MAX) break;
+        const double s = span_sum_warp<STREAM, SRC>(B.csc, lo, hi, x);
+        if (lane == j) mine = s;
+    }
+    if constexpr (PR_SUB_LANES < 32) {
+        constexpr int L = PR_SUB_LANES, G = 32 / L;
+        for (; j < cnt; j += G) {
+            const int jj = j + lane / L;
+            const int src = jj < 31 ? jj : 31;
+            int64_t lo = __shfl_sync(0xffffffffu, my_lo, src), hi = __shfl_sync(0xffffffffu, my_hi, src);
+            if (jj >= cnt) hi = lo;
+            const double s = span_sum_sub<STREAM, SRC, L>(B.csc, lo, hi, x);
+            const int k = lane - j;   // this lane's row is summed by group k
+            const double v = __shfl_sync(0xffffffffu, s, (k >= 0 && k < G ? k : 0) * L);
+            if (k >= 0 && k < G) mine = v;
+        }
+    }
+    return mine;
+}
+
 #ifndef PR_UNIT_RING
 #define PR_UNIT_RING 1
 #endif
@@ -191,19 +253,15 @@ __device__ __forceinline__ void bins_run(const BinView &B, const int64_t u_lo, c
                         my_hi = B.doff[my_row + 1];
                     }
                     const auto pre = rows.pre(my_valid, my_row);
-                    for (int j = 0; j < cnt; ++j) {
-                        const int64_t lo = __shfl_sync(0xffffffffu, my_lo, j),
-                                      hi = __shfl_sync(0xffffffffu, my_hi, j);
-                        const double s = span_sum_warp<STREAM, SRC>(B.csc, lo, hi, x);
-                        if (lane == j) mine = s;
-                    }
+                    mine = warp_batch_sums<STREAM, SRC>(B, x, my_lo, my_hi, cnt);
                     rows.fin(my_valid, pre, mine);
                 } else {
-                    for (int j = 0; j < cnt; ++j) {
-                        const int64_t row = base + 8 * j;
-                        const double s = span_sum_warp<STREAM, SRC>(B.csc, B.doff[row], B.doff[row + 1], x);
-                        if (lane == j) mine = s;
+                    int64_t my_lo = 0, my_hi = 0;
+                    if (my_valid) {
+                        my_lo = B.doff[my_row];
+                        my_hi = B.doff[my_row + 1];
                     }
+                    mine = warp_batch_sums<STREAM, SRC>(B, x, my_lo, my_hi, cnt);
                     rows.fin(my_valid, rows.pre(my_valid, my_row), mine);
                 }
             }
@@ -301,15 +359,16 @@ __device__ __forceinline__ void bins_run_plain(const BinView &B, const int64_t u
             // ---- warp rows: warp w takes rows w, w+8, ...; sums of 32 rows
             // collected (lane j holds row j's) and drained lane-parallel
             for (int64_t base = d.x + wid; base < d.y; base += 8 * 32) {
-                double mine = 0.0;
-                for (int j = 0; j < 32; ++j) {
-                    const int64_t row = base + 8 * j;
-                    if (row >= d.y) break;
-                    const double s = span_sum_warp<STREAM, SRC>(B.csc, B.doff[row], B.doff[row + 1], x);
-                    if (lane == j) mine = s;
-                }
                 const int64_t row = base + 8 * lane;
-                thread_row(row < d.y, row, mine);
+                const bool valid = row < d.y;
+                const int cnt = __popc(__ballot_sync(0xffffffffu, valid));
+                int64_t my_lo = 0, my_hi = 0;
+                if (valid) {
+                    my_lo = B.doff[row];
+                    my_hi = B.doff[row + 1];
+                }
+                const double mine = warp_batch_sums<STREAM, SRC>(B, x, my_lo, my_hi, cnt);
+                thread_row(valid, row, mine);
             }
         } else {
             // ---- thread rows: thread t takes rows t, t+256, ... (whole warps iterate together)
