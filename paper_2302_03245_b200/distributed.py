@@ -669,3 +669,57 @@ class CudaLocalStep:
         r, h = self.export()
         x = r + h if self.algo == "ifp1" else r
         return x / total
+
+
+def run_emulated(g, parts: int, algorithm: str, damping: float = 0.85, threshold: float = 1e-10,
+                 fused: bool = True, device: int = 0, max_rounds: int = 1_000_000):
+    """The partitioned fast path with ``parts`` ranks emulated in one process
+    on one device (B200_PROFILING.md: ranks sharing a GPU must not wait on
+    each other): every rank's round is its own launch on the shared library
+    stream, in rank order, and a round starts once every rank finished the
+    previous one.  ``fused``: shares stored into every rank's replica by the
+    round kernel (pr_part_set_peer_ptrs); else each rank's slot of one shared
+    full vector (what the all-gather produces).  Returns (values in original
+    ids, rounds).  For tests and smoke checks on a single GPU."""
+    import torch
+    n = int(g.n)
+    order = run_order(np.diff(np.asarray(g.out_offsets)), np.diff(np.asarray(g.in_offsets)))
+    plist = [partition_graph(g, parts, r, algorithm, order=order) for r in range(parts)]
+    steps = [CudaLocalStep(p, damping, threshold, algorithm, device=device, fast=True) for p in plist]
+    S = plist[0].slot
+    dev = torch.device("cuda", device)
+    stats = torch.zeros((parts, 9), dtype=torch.float64, device=dev)
+    full = [torch.zeros(S * parts, dtype=torch.float64, device=dev) for _ in range(2)]
+    if fused:
+        ptrs = [q for r, st in enumerate(steps) for q in st.share_buffers(parts, r)]
+        for r, st in enumerate(steps):
+            st.set_peer_ptrs(parts, r, ptrs)
+            st.init_fused(stats[r])
+    else:
+        for r, st in enumerate(steps):
+            st.init_device(full[0][r * S:(r + 1) * S], stats[r])
+    rounds = 0
+    while True:
+        torch.cuda.synchronize()
+        if stats[:, 3].sum().item() == 0:
+            break
+        if rounds >= max_rounds:
+            raise RuntimeError(f"sync simulation did not settle in {max_rounds} iterations")
+        for r, st in enumerate(steps):
+            if fused:
+                st.round_fused(rounds, stats[r])
+            else:
+                st.round_device(full[rounds & 1], full[(rounds + 1) & 1][r * S:(r + 1) * S], stats[r], rounds)
+        rounds += 1
+    torch.cuda.synchronize()
+    if algorithm == "ifp2":
+        x = torch.zeros(S * parts, dtype=torch.float64, device=dev)
+        for r, st in enumerate(steps):
+            st.settle_shares(x[r * S:(r + 1) * S])
+        for st in steps:
+            st.settle(x)
+    total = sum(st.local_total() for st in steps)
+    values = np.empty(n)
+    for p, st in zip(plist, steps):
+        values[order[p.lo:p.hi]] = st.values(total)
+    return values, rounds

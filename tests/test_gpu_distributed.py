@@ -106,58 +106,12 @@ def test_fast_partitions_queued(algorithm):
 
 
 def _emulate(algorithm, parts, fused, config="c1"):
-    """The ranks emulated in one process on one device (B200_PROFILING.md: no
-    kernels waiting on each other across processes of one GPU): every rank's
-    round runs as its own launch on the shared library stream, in rank order,
-    and a round starts after every rank finished the previous one.  fused:
-    shares stored into every rank's replica by the round kernel
-    (pr_part_round_fused); else each rank's slice of one shared full vector
-    (the all-gather of the queued path)."""
-    import torch
+    """distributed.run_emulated on a BASELINE config (ranks in one process)."""
     from paper_2302_03245_b200 import distributed as D
     from paper_2302_03245_b200 import synthetic
     n, src, dst = synthetic.make(config, seed=0)
     g = oracle.from_edges(n, src, dst)
-    order = D.run_order(np.diff(g.out_offsets), np.diff(g.in_offsets))
-    parts_ = [D.partition_graph(g, parts, r, algorithm, order=order) for r in range(parts)]
-    steps = [D.CudaLocalStep(p, 0.85, 1e-10, algorithm, device=0, fast=True) for p in parts_]
-    S = parts_[0].slot
-    dev = torch.device("cuda", 0)
-    stats = torch.zeros((parts, 9), dtype=torch.float64, device=dev)
-    full = [torch.zeros(S * parts, dtype=torch.float64, device=dev) for _ in range(2)]
-    if fused:
-        ptrs = [p for r, s in enumerate(steps) for p in s.share_buffers(parts, r)]
-        for r, s in enumerate(steps):
-            s.set_peer_ptrs(parts, r, ptrs)
-        for r, s in enumerate(steps):
-            s.init_fused(stats[r])
-    else:
-        for r, s in enumerate(steps):
-            s.init_device(full[0][r * S:(r + 1) * S], stats[r])
-    rounds = 0
-    while True:
-        torch.cuda.synchronize()
-        if stats[:, 3].sum().item() == 0:
-            break
-        t = rounds
-        for r, s in enumerate(steps):
-            if fused:
-                s.round_fused(t, stats[r])
-            else:
-                s.round_device(full[t & 1], full[(t + 1) & 1][r * S:(r + 1) * S], stats[r], t)
-        rounds += 1
-        assert rounds < 10_000
-    torch.cuda.synchronize()
-    if algorithm == "ifp2":
-        x = torch.zeros(S * parts, dtype=torch.float64, device=dev)
-        for r, s in enumerate(steps):
-            s.settle_shares(x[r * S:(r + 1) * S])
-        for s in steps:
-            s.settle(x)
-    total = sum(s.local_total() for s in steps)
-    vals = np.empty(n)
-    for p, s in zip(parts_, steps):
-        vals[order[p.lo:p.hi]] = s.values(total)
+    vals, rounds = D.run_emulated(g, parts, algorithm, fused=fused)
     return vals, rounds, g
 
 
