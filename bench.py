@@ -365,6 +365,15 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
     te = torch.tensor([(time.perf_counter() - t0) / 2], dtype=torch.float64, device=red_dev)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_s = float(te.item())
+    # roofline of the partitioned round loop: the algorithmic bytes of the
+    # rounds (12 B per pushed edge, 40 B per drained vertex,
+    # 8 B per scanned vertex and round; the IFP2 settle's pushes counted as
+    # edges) over the whole solve's device time, per GPU, against the HBM peak
+    peak = float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)) \
+        if os.path.exists(os.path.join(REPO, "MEASURED_PEAKS.json")) else 6650.0
+    n_scan = float(np.count_nonzero(np.diff(np.asarray(g.out_offsets)) > 0))
+    bytes_solve = 12.0 * info["push_ops"] + 40.0 * info.get("drained", 0) + 8.0 * n_scan * (info["rounds"] + 1)
+    achieved = bytes_solve * args.steps / total_s / world / 1e9
     if rank == 0:
         line = {"metric": "GTEPS", "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
@@ -375,6 +384,11 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
                         "h2d_bytes_per_step": int(part.in_sources.nbytes + part.in_offsets.nbytes),
                         "d2h_bytes_per_step": int(8 * part.owned), "ms_per_step": 1e3 * e2e_s,
                         "path": "per step: partition upload (pr_part_create) + rounds + owned values D2H"},
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak, "traffic": None,
+                             "kernel": "partitioned round loop per GPU (k_part_pull + exchange + statistics), "
+                                       "algorithmic bytes 12*E_pushed + 40*V_drained + 8*n_scan per round",
+                             "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
                 "gpu_launches": int(2 * (info["rounds"] + 2)), "clocks": clocks.summary(),
                 "exchange": ("fused: round kernel stores shares into every rank's replica (peer memory)"
                              if fused else "NCCL all-gather of shares per round"),

@@ -772,13 +772,18 @@ int ensure_run_layout(Graph &g) {
     r->orig = &g;
     r->has_csr = false;       // out_tgt on demand (ensure_run_csr)
     int rc = permute_adjacency(ctx, g.in_off, g.in_src, g.perm, g.rank, n, m, r->in_off, r->in_src);
-    // PUSHRANK_SORT_ROWS=1: sources of every row ascending in run ids, so the
-    // hot (low-id) sources of a warp or hub row sit next to each other.
-    // Measured: solve C2 -0.9%, C3/C4 0, C5 -4%, but the segmented sort adds
-    // 0.7 ms (C2) / 7.5 ms (C3) to a fresh graph's preprocessing: off.
+    // Sources of every row ascending in run ids, so the hot (low-id) sources
+    // of a warp or hub row sit next to each other and neighbouring lanes
+    // share 128-byte lines.  Measured: solve C5 -4% (-6% with 16-lane
+    // sub-warp rows), C2 -0.9%, C3/C4 0; the segmented sort adds 0.7 ms (C2)
+    // / 7.5 ms (C3) to a fresh graph's preprocessing.  So it runs only where
+    // the rounds are HBM-bound: a round working set past 16x L2 (C5), as for
+    // 4 Gauss-Seidel sections.  PUSHRANK_SORT_ROWS=0/1 forces it.
     {
-        const char *e = getenv("PUSHRANK_SORT_ROWS");
-        if (!rc && e && atoi(e) != 0) rc = sort_csc_rows(ctx, r->in_off, r->in_src, n, m);
+        const double l2 = (double)(ctx.l2_bytes ? ctx.l2_bytes : (size_t)126 << 20);
+        bool sort_rows = 4.0 * (double)m + 8.0 * (double)n > 16.0 * l2;
+        if (const char *e = getenv("PUSHRANK_SORT_ROWS")) sort_rows = atoi(e) != 0;
+        if (!rc && sort_rows) rc = sort_csc_rows(ctx, r->in_off, r->in_src, n, m);
     }
     DevBuf len;
     if (!rc) rc = ensure(len, 8 * (n + 1));

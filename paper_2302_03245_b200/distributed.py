@@ -300,8 +300,10 @@ def run_partitioned_queued(step, comm, part: Partition, algorithm: str, damping:
     rows = []
     push_ops = push_dang = 0
 
+    drained = 0   # vertices drained over the solve (the roofline's 40 B per active vertex)
+
     def record(r):
-        nonlocal push_ops, push_dang
+        nonlocal push_ops, push_dang, drained
         l1, above, nd_above = float(r[0]), float(r[1]), float(r[2])
         nact, work, pops, pdang, conv_all, conv_scan = (int(round(x)) for x in r[3:9])
         rows.append({"h_l1": l1, "converged": conv_all if conv_scope_all else conv_scan,
@@ -309,6 +311,7 @@ def run_partitioned_queued(step, comm, part: Partition, algorithm: str, damping:
                      "push_ops_dangling": push_dang, "active_mass": above, "carry_mass": l1 - above})
         push_ops += pops
         push_dang += pdang
+        drained += nact
         return nact
 
     with ctx:
@@ -386,7 +389,7 @@ def run_partitioned_queued(step, comm, part: Partition, algorithm: str, damping:
         total = float(gt[0])
         values = step.values(total) if host_values else None
     return values, rows, {"rounds": t, "mass_total": total, "push_ops": push_ops,
-                          "push_ops_dangling": push_dang, "settled": settled}
+                          "push_ops_dangling": push_dang, "settled": settled, "drained": drained}
 
 
 def sweep_kind(t: int) -> int:
