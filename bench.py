@@ -389,7 +389,8 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
                              "kernel": "partitioned round loop per GPU (k_part_pull + exchange + statistics), "
                                        "algorithmic bytes 12*E_pushed + 40*V_drained + 8*n_scan per round",
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
-                "gpu_launches": int(2 * (info["rounds"] + 2)), "clocks": clocks.summary(),
+                # per round: the sections' k_part_pull + k_part_reduce; init (2) and settle/total (4)
+                "gpu_launches": int(step.launches_per_round() * info["rounds"] + 6), "clocks": clocks.summary(),
                 "exchange": ("fused: round kernel stores shares into every rank's replica (peer memory)"
                              if fused else "NCCL all-gather of shares per round"),
                 "note": ("partitioned rounds queued on the device and graph-captured (statistics read back "

@@ -64,6 +64,7 @@ int part_share_buffers(Part &P, int parts, int rank, void **d_full, void *ipc);
 int part_set_peers(Part &P, const void *handles);
 int part_set_peer_ptrs(Part &P, int parts, int rank, void *const *ptrs);
 int part_set_rank(Part &P, int parts, int rank);
+int part_launches_per_round(Part &P, int *out);
 int part_init_fused(Part &P, double *d_stats9);
 int part_round_fused(Part &P, int parity, int kind, double *d_stats9);
 
@@ -578,6 +579,14 @@ int pr_part_set_peers(pr_part *p, const void *ipc_handles) {
     PART_ENTER(p);
     CHECK_PTR(ipc_handles, "ipc_handles");
     return part_set_peers(*p->p, ipc_handles);
+}
+int pr_part_launches_per_round(pr_part *p, int32_t *launches) {
+    PART_ENTER(p);
+    CHECK_PTR(launches, "launches");
+    int v = 0;
+    PR_TRY(part_launches_per_round(*p->p, &v));
+    *launches = v;
+    return PR_OK;
 }
 int pr_part_set_rank(pr_part *p, int32_t parts, int32_t rank) {
     PART_ENTER(p);

@@ -639,6 +639,14 @@ int part_set_peers(Part &P, const void *handles) {
     return PR_OK;
 }
 
+// launches per fast round (one per Gauss-Seidel section + the statistics
+// reduction); builds the schedule if needed
+int part_launches_per_round(Part &P, int *out) {
+    PR_TRY(ensure_part_sched(P));
+    *out = (P.nsec > 1 ? P.nsec : 1) + 1;
+    return PR_OK;
+}
+
 // this partition's place among the ranks (the padded slot it owns: the
 // rank-local Gauss-Seidel test and the fused exchange's store offset)
 int part_set_rank(Part &P, int parts, int rank) {

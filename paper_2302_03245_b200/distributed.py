@@ -629,6 +629,11 @@ class CudaLocalStep:
         arr = (self._ct.c_void_p * len(ptrs))(*ptrs)
         self._lib.check(self.L.pr_part_set_peer_ptrs(self.h, int(parts), int(rank), arr), "pr_part_set_peer_ptrs")
 
+    def launches_per_round(self) -> int:
+        v = self._ct.c_int32(0)
+        self._lib.check(self.L.pr_part_launches_per_round(self.h, self._ct.byref(v)), "pr_part_launches_per_round")
+        return int(v.value)
+
     def init_fused(self, stats_row):
         self._lib.check(self.L.pr_part_init_fused(self.h, self._ct.c_void_p(stats_row.data_ptr())),
                         "pr_part_init_fused")
