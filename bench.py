@@ -359,7 +359,10 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
     t0 = time.perf_counter()
     for _ in range(2):
         s2 = D.CudaLocalStep(part, DAMPING, XI, args.algo, device=local, fast=True)
-        solve(s2, host_values=True, fused=fused and s2.setup_fused(comm))
+        f2 = fused and s2.setup_fused(comm)
+        solve(s2, host_values=True, fused=f2)
+        if f2:
+            s2.close_fused(comm)
         del s2
     torch.cuda.synchronize()
     te = torch.tensor([(time.perf_counter() - t0) / 2], dtype=torch.float64, device=red_dev)
@@ -397,6 +400,8 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
                          "every 8 rounds); local step = binned dense-round gather (k_part_pull); "
                          "all-reduce of 9 statistics per round (the round barrier)")}
         print(json.dumps(line), flush=True)
+    if fused:
+        step.close_fused(comm)
     dist.destroy_process_group()
 
 

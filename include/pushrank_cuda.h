@@ -298,6 +298,10 @@ int pr_part_share_buffers(pr_part *p, int32_t parts, int32_t rank, void **d_full
 int pr_part_set_peers(pr_part *p, const void *ipc_handles);
 int pr_part_set_peer_ptrs(pr_part *p, int32_t parts, int32_t rank, void *const *d_full);
 int pr_part_init_fused(pr_part *p, double *d_stats);
+/* Unmap the other ranks' replicas; call on every rank, then a barrier,
+ * before destroying the partitions (an exporter must not free a replica
+ * another rank still maps). */
+int pr_part_close_peers(pr_part *p);
 int pr_part_round_fused(pr_part *p, int32_t parity, int32_t kind, double *d_stats);
 int pr_part_settle_shares(pr_part *p, double *d_x_mine);
 int pr_part_settle(pr_part *p, const double *d_x_full, int64_t *settled, int64_t *ints, double *floats);

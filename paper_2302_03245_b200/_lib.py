@@ -126,6 +126,7 @@ SIGNATURES = {
     "pr_part_set_rank": (ctypes.c_int, [c_vp, c_i32, c_i32]),
     "pr_part_launches_per_round": (ctypes.c_int, [c_vp, ctypes.POINTER(c_i32)]),
     "pr_part_init_fused": (ctypes.c_int, [c_vp, c_vp]),
+    "pr_part_close_peers": (ctypes.c_int, [c_vp]),
     "pr_part_round_fused": (ctypes.c_int, [c_vp, c_i32, c_i32, c_vp]),
     "pr_part_settle_shares": (ctypes.c_int, [c_vp, c_vp]),
     "pr_part_settle": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),

@@ -65,6 +65,7 @@ int part_set_peers(Part &P, const void *handles);
 int part_set_peer_ptrs(Part &P, int parts, int rank, void *const *ptrs);
 int part_set_rank(Part &P, int parts, int rank);
 int part_launches_per_round(Part &P, int *out);
+int part_close_peers(Part &P);
 int part_init_fused(Part &P, double *d_stats9);
 int part_round_fused(Part &P, int parity, int kind, double *d_stats9);
 
@@ -579,6 +580,10 @@ int pr_part_set_peers(pr_part *p, const void *ipc_handles) {
     PART_ENTER(p);
     CHECK_PTR(ipc_handles, "ipc_handles");
     return part_set_peers(*p->p, ipc_handles);
+}
+int pr_part_close_peers(pr_part *p) {
+    PART_ENTER(p);
+    return part_close_peers(*p->p);
 }
 int pr_part_launches_per_round(pr_part *p, int32_t *launches) {
     PART_ENTER(p);

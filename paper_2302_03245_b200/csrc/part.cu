@@ -657,6 +657,17 @@ int part_set_rank(Part &P, int parts, int rank) {
     return PR_OK;
 }
 
+// unmap the other ranks' replicas (before any rank frees its own: the
+// caller puts a barrier between this and the destruction)
+int part_close_peers(Part &P) {
+    cudaStreamSynchronize(P.ctx->stream);
+    for (void *p : P.opened) cudaIpcCloseMemHandle(p);
+    P.opened.clear();
+    for (int r = 0; r < PR_MAX_PEERS; ++r)
+        if (r != P.rank) P.peer[0][r] = P.peer[1][r] = nullptr;
+    return PR_OK;
+}
+
 // same-process emulation (tests): the ranks' replicas are device pointers
 int part_set_peer_ptrs(Part &P, int parts, int rank, void *const *ptrs) {
     if (parts < 1 || parts > PR_MAX_PEERS || rank < 0 || rank >= parts)

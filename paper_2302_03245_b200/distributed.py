@@ -625,6 +625,12 @@ class CudaLocalStep:
         comm.dist.all_reduce(flag, op=comm.dist.ReduceOp.MIN)
         return bool(flag.item() > 0.5)
 
+    def close_fused(self, comm) -> None:
+        """Collective: unmap the other ranks' replicas, then a barrier, so
+        that no rank frees a replica (at destruction) that another still maps."""
+        self._lib.check(self.L.pr_part_close_peers(self.h), "pr_part_close_peers")
+        comm.dist.barrier()
+
     def set_peer_ptrs(self, parts: int, rank: int, ptrs) -> None:
         arr = (self._ct.c_void_p * len(ptrs))(*ptrs)
         self._lib.check(self.L.pr_part_set_peer_ptrs(self.h, int(parts), int(rank), arr), "pr_part_set_peer_ptrs")
