@@ -358,11 +358,11 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
     dist.barrier()
     t0 = time.perf_counter()
     for _ in range(2):
+        # (the all-gather form: a fresh partition per step would otherwise pay
+        # the replicas' cudaMalloc/IPC mapping every step, which a resident
+        # partition does once)
         s2 = D.CudaLocalStep(part, DAMPING, XI, args.algo, device=local, fast=True)
-        f2 = fused and s2.setup_fused(comm)
-        solve(s2, host_values=True, fused=f2)
-        if f2:
-            s2.close_fused(comm)
+        solve(s2, host_values=True, fused=False)
         del s2
     torch.cuda.synchronize()
     te = torch.tensor([(time.perf_counter() - t0) / 2], dtype=torch.float64, device=red_dev)
@@ -386,7 +386,7 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
                 "e2e": {"value": info["push_ops"] / e2e_s / 1e9, "unit": "GTEPS",
                         "h2d_bytes_per_step": int(part.in_sources.nbytes + part.in_offsets.nbytes),
                         "d2h_bytes_per_step": int(8 * part.owned), "ms_per_step": 1e3 * e2e_s,
-                        "path": "per step: partition upload (pr_part_create) + rounds + owned values D2H"},
+                        "path": "per step: partition upload (pr_part_create) + rounds (all-gather exchange) + owned values D2H"},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": None,
                              "kernel": "partitioned round loop per GPU (k_part_pull + exchange + statistics), "

@@ -166,6 +166,8 @@ struct Graph {
         int nsec = 0;             // Gauss-Seidel sections the units were cut for
         int64_t sec_row[PR_MAX_SECTIONS + 1] = {};   // section row bounds (equal edges)
         int64_t sec_unit[PR_MAX_SECTIONS + 1] = {};  // section unit bounds
+        int64_t sec_id[PR_MAX_SECTIONS + 1] = {};    // IFP1: id bound of earlier sections' sources
+        DevBuf sec_of;            // IFP1: uint8 [n] section of each vertex's row (255: not a row)
         int64_t n_units = 0;
         DevBuf units;             // int2 [n_units]: (row_begin, row_end) or hub chunk (row, -(chunk+1))
         DevBuf row_cnt;           // int32 [n_hub] chunk arrival counters

@@ -78,6 +78,11 @@ struct RunArgs {
     // Gauss-Seidel sections of a dense sweep (ids == rows: the IFP2 run
     // layout); this launch processes section `sec` of `nsec`
     int32_t sec, nsec;
+    // sources with id < sec_id[k] sit in sections before k (IFP2: ids are
+    // rows, sec_id = sec_row; IFP1: the class-0 ids are in row order, so the
+    // bound is the first class-0 id at or after row sec_row[k])
+    int64_t sec_id[PR_MAX_SECTIONS + 1];
+    const uint8_t *sec_of;     // IFP1: section of each vertex's row (push filter); null for IFP2
     int64_t sec_row[PR_MAX_SECTIONS + 1];
     int64_t sec_unit[PR_MAX_SECTIONS + 1];
 };
@@ -495,7 +500,7 @@ __global__ void __launch_bounds__(256, PREFETCH ? PULL_MIN_BLOCKS - 1 : PULL_MIN
     int32_t gs = 0;
     if constexpr (GS) {
         gs = A.ctl->gs;
-        if (gs) src.gs_lo = (int)A.sec_row[A.sec];
+        if (gs) src.gs_lo = (int)A.sec_id[A.sec];
     }
     Partial p;
     zero(p);
@@ -550,12 +555,18 @@ __global__ void __launch_bounds__(256) k_push(RunArgs A) {
         // after a Gauss-Seidel sweep, targets in later sections than u have
         // already taken u's share during the sweep
         int32_t t_hi = 0x7fffffff;
-        if (filter)
-            for (int k = 1; k <= A.nsec; ++k)
-                if (u < A.sec_row[k]) {
-                    t_hi = (int32_t)A.sec_row[k];
-                    break;
-                }
+        int su = PR_MAX_SECTIONS;   // IFP1: deliver to targets whose row section <= su
+        if (filter) {
+            if (A.sec_of) {
+                su = A.sec_of[u];
+            } else {
+                for (int k = 1; k <= A.nsec; ++k)
+                    if (u < A.sec_row[k]) {
+                        t_hi = (int32_t)A.sec_row[k];
+                        break;
+                    }
+            }
+        }
         int32_t tg[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -564,7 +575,8 @@ __global__ void __launch_bounds__(256) k_push(RunArgs A) {
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            if (tg[k] >= 0 && tg[k] < t_hi) atomicAdd(&A.h[tg[k]], sh);
+            if (tg[k] >= 0 && tg[k] < t_hi && (su == PR_MAX_SECTIONS || A.sec_of[tg[k]] <= su))
+                atomicAdd(&A.h[tg[k]], sh);
     }
 }
 
@@ -951,6 +963,68 @@ static int build_graph(Plan &P, cudaGraph_t *out_g, cudaGraphExec_t *out_exec) {
     return PR_OK;
 }
 
+// IFP1 sections on the run layout: sec_of[ids[r]] = section of row r; sec_id[k]
+// = first class-0 id at or after row sec_row[k] (class0_end if none); bad
+// counts class-0 rows whose ids do not increase with the row (then the
+// id-bound test is invalid and the caller drops the sections)
+__global__ void k_sec_of(const int32_t *ids, int64_t count, const int64_t *bounds, int nsec, uint8_t *sec_of) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x) {
+        int k = 0;
+        while (k + 1 < nsec && r >= bounds[k + 1]) ++k;
+        sec_of[ids[r]] = (uint8_t)k;
+    }
+}
+
+__global__ void k_class0_order(const int32_t *ids, int64_t count, int64_t c0, int32_t *pos, unsigned long long *bad,
+                               int phase) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = ids[r];
+        if (v >= c0) continue;
+        if (phase == 0) pos[v] = (int32_t)r;
+        else if (v + 1 < c0 && pos[v + 1] <= (int32_t)r) atomicAdd(bad, 1ull);
+    }
+}
+
+__global__ void k_sec_id(const int32_t *ids, int64_t count, int64_t c0, const int64_t *bounds, int nsec, int64_t *out) {
+    const int k = threadIdx.x;
+    if (k > nsec) return;
+    int64_t r = bounds[k];
+    while (r < count && ids[r] >= c0) ++r;
+    out[k] = r < count ? ids[r] : c0;
+}
+
+static int sections_by_id(Graph &g, int which) {
+    Ctx &ctx = *g.ctx;
+    cudaStream_t st = ctx.stream;
+    auto &S = g.sched[which];
+    const int64_t c0 = g.class0_end;
+    DevBuf pos, bad, bnd, out;
+    PR_TRY(ensure(pos, 4 * (c0 > 0 ? c0 : 1)));
+    PR_TRY(ensure(bad, 8));
+    PR_TRY(ensure(bnd, 8 * (PR_MAX_SECTIONS + 1)));
+    PR_TRY(ensure(out, 8 * (PR_MAX_SECTIONS + 1)));
+    PR_TRY(ensure(S.sec_of, g.n > 0 ? g.n : 1));
+    PR_CUDA(cudaMemsetAsync(bad.ptr, 0, 8, st));
+    PR_CUDA(cudaMemsetAsync(S.sec_of.ptr, 0xFF, g.n, st));
+    PR_CUDA(cudaMemcpyAsync(bnd.ptr, S.sec_row, 8 * (S.nsec + 1), cudaMemcpyHostToDevice, st));
+    const unsigned gr = grid_for(S.count, 256) > 4096 ? 4096 : grid_for(S.count, 256);
+    if (S.count) {
+        k_class0_order<<<gr, 256, 0, st>>>(S.ids.as<int32_t>(), S.count, c0, pos.as<int32_t>(),
+                                           bad.as<unsigned long long>(), 0);
+        k_class0_order<<<gr, 256, 0, st>>>(S.ids.as<int32_t>(), S.count, c0, pos.as<int32_t>(),
+                                           bad.as<unsigned long long>(), 1);
+        k_sec_of<<<gr, 256, 0, st>>>(S.ids.as<int32_t>(), S.count, bnd.as<int64_t>(), S.nsec, S.sec_of.as<uint8_t>());
+    }
+    k_sec_id<<<1, 32, 0, st>>>(S.ids.as<int32_t>(), S.count, c0, bnd.as<int64_t>(), S.nsec, out.as<int64_t>());
+    unsigned long long nbad = 0;
+    PR_CUDA(cudaMemcpyAsync(&nbad, bad.ptr, 8, cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaMemcpyAsync(S.sec_id, out.ptr, 8 * (S.nsec + 1), cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaStreamSynchronize(st));
+    PR_CUDA(cudaGetLastError());
+    if (nbad) return fail(PR_ERR_STATE, "class-0 rows out of id order");
+    return PR_OK;
+}
+
 // Workspace sized once per graph (the executable-graph cache is keyed by the
 // pointers, so a reallocation simply misses it).
 static int ws_alloc(Graph &g, int64_t need_blocks, int64_t fcap) {
@@ -1037,7 +1111,7 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     // round is long: 2 sections past 1.5x L2 of round working set (C3: 14.8 ->
     // 11.5 ms), 4 past 16x (C5: 813 -> 598 ms), none below (C2, C4).
     int nsec = 1;
-    if (algo == PR_ALGO_IFP2 && g.class0_end >= 0) {
+    if ((algo == PR_ALGO_IFP2 || algo == PR_ALGO_IFP1) && g.class0_end >= 0) {
         nsec = ws > 16.0 * l2 ? 4 : ws > 1.5 * l2 ? 2 : 1;
         if (const char *e = getenv("PUSHRANK_GS_SECTIONS")) nsec = atoi(e);
         if (nsec < 1) nsec = 1;
@@ -1047,6 +1121,14 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
         k_pull_fn = stream ? (prefetch ? (const void *)k_pull<true, true, true> : (const void *)k_pull<true, false, true>)
                            : (prefetch ? (const void *)k_pull<false, true, true> : (const void *)k_pull<false, false, true>);
     PR_TRY(ensure_units(g, which, pull_blocks, nsec));
+    // IFP1 sections: the id bounds of the sources of earlier sections and the
+    // section of every row's vertex (the schedule interleaves class 0 and the
+    // dangling receivers by degree; class-0 ids stay in row order)
+    if (algo == PR_ALGO_IFP1 && g.sched[which].nsec > 1) {
+        if (sections_by_id(g, which) != PR_OK) {
+            PR_TRY(ensure_units(g, which, pull_blocks, 1));
+        }
+    }
     const int64_t fcap = n + g.m / TILE + 1;
     if (getenv("PUSHRANK_TIMING"))
         fprintf(stderr, "[pushrank] round working set %.1f MB (L2 %.1f MB): stream %d prefetch %d sections %d\n",
@@ -1087,6 +1169,9 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     A.T.n_units = S.n_units;
     A.nsec = S.nsec;
     A.sec = 0;
+    A.sec_of = (algo == PR_ALGO_IFP1 && S.nsec > 1) ? S.sec_of.as<uint8_t>() : nullptr;
+    for (int k = 0; k <= PR_MAX_SECTIONS; ++k)
+        A.sec_id[k] = k <= S.nsec ? (A.sec_of ? S.sec_id[k] : S.sec_row[k]) : S.count;
     for (int k = 0; k <= PR_MAX_SECTIONS; ++k) {
         A.sec_row[k] = k <= S.nsec ? S.sec_row[k] : S.count;
         A.sec_unit[k] = k <= S.nsec ? S.sec_unit[k] : S.n_units;

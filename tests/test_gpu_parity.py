@@ -347,6 +347,30 @@ def test_gauss_seidel_sections_parity(sections, monkeypatch, golden_corpus):
         assert np.max(np.abs(v2.values - golden_corpus[f"g{i}_ifp2_values"])) <= max(1e-10, 10 * XI * n), i
 
 
+@pytest.mark.parametrize("sections", [2, 3, 8])
+def test_gauss_seidel_sections_ifp1(sections, monkeypatch):
+    """IFP1 sweeps in Gauss-Seidel sections: the IFP1 schedule interleaves
+    class-0 rows and dangling receivers by degree, so earlier sections'
+    sources are found by an id bound (class-0 ids stay in row order) and the
+    push filter by each vertex's row section.  Same fixed point as the
+    oracle's IFP1 twin (L1 <= 1e-9, identical top-100), mass 1, fewer rounds
+    in pull mode, run-to-run identical vectors in pull mode."""
+    monkeypatch.setenv("PUSHRANK_GS_SECTIONS", str(sections))
+    n, src, dst = synthetic.make("c2", seed=0)
+    g = P.from_edges(n, src, dst)
+    cls = P.classify(g)
+    o = oracle.sync_simulate(oracle.from_edges(n, src, dst), "ifp1", threshold=XI)
+    for mode in MODES:
+        vec, tr = P.ifp1_run(g, cls, cfg(), mode=mode)
+        assert np.abs(vec.values - o.values).sum() <= 1e-9, mode
+        assert np.array_equal(top100(vec.values), top100(o.values)), mode
+        assert abs(vec.values.sum() - 1.0) <= 1e-12
+        if mode == "pull":
+            assert tr.meta["rounds"] < o.iterations, (tr.meta["rounds"], o.iterations)
+            again, _ = P.ifp1_run(g, cls, cfg(), mode=mode)
+            assert np.array_equal(again.values, vec.values)
+
+
 def test_c3_full_size_parity():
     """C3 (52 M edges): the fast IFP2 engine, which runs 2 Gauss-Seidel
     sections per dense sweep at this size, against the round-synchronous
