@@ -258,8 +258,9 @@ def run_ours(args):
             traffic = json.load(open(tpath)).get(f"{args.config}_{args.algo}")
         except Exception:
             traffic = None
-    launches = sum(3 + r.pull_rounds + 2 * r.push_rounds + (1 if args.algo == "ifp2" else 0) + 1
-                   for r in results)
+    # device-counted by the library (every solve kernel counts its own launch,
+    # including unrolled graph slots that exit at once), over the timed steps
+    launches = sum(r.launches for r in results)
     line = {"metric": "GTEPS", "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -393,7 +394,8 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
                                        "algorithmic bytes 12*E_pushed + 40*V_drained + 8*n_scan per round",
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
                 # per round: the sections' k_part_pull + k_part_reduce; init (2) and settle/total (4)
-                "gpu_launches": int(step.launches_per_round() * info["rounds"] + 6), "clocks": clocks.summary(),
+                "gpu_launches": int((step.launches_per_round() * info["rounds"] + 6) * args.steps),
+                "clocks": clocks.summary(),
                 "exchange": ("fused: round kernel stores shares into every rank's replica (peer memory)"
                              if fused else "NCCL all-gather of shares per round"),
                 "note": ("partitioned rounds queued on the device and graph-captured (statistics read back "

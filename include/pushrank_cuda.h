@@ -44,7 +44,7 @@ extern "C" {
 #define PR_ERR_NOMEM (-5)       /* device allocation failed */
 #define PR_ERR_FORMAT (-6)      /* edge-list text the device parser does not accept (graph.py:180-233) */
 
-#define PR_ABI_VERSION 2
+#define PR_ABI_VERSION 3
 
 typedef struct pr_ctx pr_ctx;       /* one device + stream + workspace */
 typedef struct pr_graph pr_graph;   /* device-resident CSR+CSC and derived data */
@@ -114,6 +114,8 @@ typedef struct pr_run_result {
                                  start .. last block finalise), summed over pull rounds */
     double pull_bytes;        /* algorithmic bytes of those pull rounds */
     double sparse_ms;         /* same for the sparse rounds (push + scan kernels) */
+    int64_t launches;         /* kernels launched by the solve (device-counted; unrolled graph
+                                 slots that exit at once included) -- ABI 3 */
 } pr_run_result;
 
 /* ---- library / context ------------------------------------------------ */

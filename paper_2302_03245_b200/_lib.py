@@ -52,7 +52,7 @@ class RunResult(ctypes.Structure):
     _fields_ = [("rounds", c_i64), ("rows", c_i64), ("push_ops", c_i64), ("push_ops_dangling", c_i64),
                 ("settled", c_i64), ("pull_rounds", c_i64), ("push_rounds", c_i64),
                 ("mass_total", c_f64), ("push_ms", c_f64), ("round_ms", c_f64), ("bytes_moved", c_f64),
-                ("pull_ms", c_f64), ("pull_bytes", c_f64), ("sparse_ms", c_f64)]
+                ("pull_ms", c_f64), ("pull_bytes", c_f64), ("sparse_ms", c_f64), ("launches", c_i64)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}

@@ -103,6 +103,7 @@ struct RunCtl {
     double mass_total;
     int64_t settled;
     unsigned long long unit_ctr;  // pull-unit dispatch counter (bins.cuh), reset every round
+    unsigned long long launches;  // kernels launched in this solve (each counts itself once)
     // per-kernel device timing (globaltimer): the first block of a round's
     // first kernel stamps t_k0, the finalising block closes the round
     uint32_t k_started;

@@ -87,6 +87,12 @@ struct RunArgs {
     int64_t sec_unit[PR_MAX_SECTIONS + 1];
 };
 
+// every solve kernel counts its own launch once (block 0, thread 0), early
+// exits included: pr_run_result.launches
+__device__ __forceinline__ void count_launch(const RunArgs &A) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&A.ctl->launches, 1ull);
+}
+
 __device__ __forceinline__ uint64_t digest_term(int64_t v, double r, double h) {
     uint64_t a = (uint64_t)__double_as_longlong(r), b = (uint64_t)__double_as_longlong(h);
     uint64_t w = ((uint64_t)v * 0x9E3779B97F4A7C15ull) | 1ull;
@@ -336,6 +342,7 @@ __device__ __forceinline__ void warp_fold(Partial &bp, Partial &acc) {
 
 __global__ void k_reset(RunArgs A) {
     RunCtl *c = A.ctl;
+    c->launches = 1;
     c->round = 0;
     c->rows = 0;
     c->push_ops = c->push_ops_dangling = 0;
@@ -367,6 +374,7 @@ __global__ void k_reset(RunArgs A) {
 // every later row (recorded as constants) and their round-0 shares are
 // scattered once by k_seed_scatter.
 __global__ void __launch_bounds__(256) k_init(RunArgs A) {
+    count_launch(A);
     Partial p, cst;
     zero(p);
     zero(cst);
@@ -421,6 +429,7 @@ __global__ void __launch_bounds__(256) k_init(RunArgs A) {
 
 // round-0 shares of active vertices outside D (in-degree 0): scatter once
 __global__ void __launch_bounds__(256) k_seed_scatter(RunArgs A) {
+    count_launch(A);
     if (!(1.0 > A.xi)) return;
     int lane = threadIdx.x & 31;
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -486,6 +495,7 @@ __device__ __forceinline__ bool round_is(const RunArgs &A, int mode) {
 // GS: the launch is one Gauss-Seidel section of a sweep
 template <bool STREAM, bool PREFETCH, bool GS>
 __global__ void __launch_bounds__(256, PREFETCH ? PULL_MIN_BLOCKS - 1 : PULL_MIN_BLOCKS) k_pull(RunArgs A) {
+    count_launch(A);
     if (A.use_graph && !round_is(A, 0)) return;
     stamp_round_start(A.ctl);
     const int64_t t = A.ctl->round;
@@ -535,6 +545,7 @@ __global__ void __launch_bounds__(256, PREFETCH ? PULL_MIN_BLOCKS - 1 : PULL_MIN
 // one warp per push item (a TILE-edge chunk of one vertex's out-row), the 8
 // target loads of a lane issued before its 8 reductions.
 __global__ void __launch_bounds__(256) k_push(RunArgs A) {
+    count_launch(A);
     if (A.use_graph && !round_is(A, 1)) return;
     stamp_round_start(A.ctl);
     int64_t t = A.ctl->round;
@@ -582,6 +593,7 @@ __global__ void __launch_bounds__(256) k_push(RunArgs A) {
 
 // Sparse round t, step 2: drain state t+1 over D
 __global__ void __launch_bounds__(256) k_scan(RunArgs A) {
+    count_launch(A);
     if (A.use_graph && !round_is(A, 1)) return;
     const int64_t t = A.ctl->round;
     const int64_t r = t + 1;
@@ -607,6 +619,7 @@ __global__ void __launch_bounds__(256) k_scan(RunArgs A) {
 // ---------------------------------------------------------------- exact engine
 
 __global__ void k_ex_init(RunArgs A) {
+    count_launch(A);
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < A.n; v += (int64_t)gridDim.x * blockDim.x) {
         A.h[v] = 1.0;
         A.reserved[v] = 0.0;
@@ -615,6 +628,7 @@ __global__ void k_ex_init(RunArgs A) {
 
 // trace row of state t (engines.py:421-435) and its drain (engines.py:438-444)
 __global__ void __launch_bounds__(256) k_ex_prep(RunArgs A) {
+    count_launch(A);
     int64_t t = A.ctl->rows;  // state index = rows produced so far
     Partial p;
     zero(p);
@@ -653,6 +667,7 @@ __global__ void __launch_bounds__(256) k_ex_prep(RunArgs A) {
 // h(t+1)_v = (active ? 0 : h_v) + sum over in-edges in ascending source order
 // (== the sequential np.bincount accumulation, engines.py:446-448)
 __global__ void k_ex_pull(RunArgs A) {
+    count_launch(A);
     int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (v >= A.n) return;
     double acc = 0.0;
@@ -670,6 +685,7 @@ __global__ void k_ex_pull(RunArgs A) {
 // source order) when `thread_mode`, else warp per vertex (fixed tree).
 __global__ void k_settle(RunArgs A, const int32_t *dang_ids, int64_t lo, int64_t nd, const int64_t *src_off,
                          const int32_t *src_ids, int thread_mode) {
+    count_launch(A);
     if (thread_mode) {
         for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd;
              i += (int64_t)gridDim.x * blockDim.x) {
@@ -707,6 +723,7 @@ __global__ void k_settle(RunArgs A, const int32_t *dang_ids, int64_t lo, int64_t
 // row with 8 loads in flight (bins.cuh helpers): one random load per edge
 // instead of two loads and a division.
 __global__ void k_settle_w(RunArgs A, int64_t n_src, double *__restrict__ w) {
+    count_launch(A);
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n_src; u += (int64_t)gridDim.x * blockDim.x) {
         const int32_t du = A.deg[u];
         w[u] = du > 0 ? __ddiv_rn(__dmul_rn(A.c, A.reserved[u]), (double)du) : 0.0;
@@ -716,6 +733,7 @@ __global__ void k_settle_w(RunArgs A, int64_t n_src, double *__restrict__ w) {
 __global__ void k_settle_fast(RunArgs A, const double *__restrict__ w, const int32_t *__restrict__ dang_ids, int64_t lo,
                               int64_t nd, const int64_t *__restrict__ src_off, const int32_t *__restrict__ src_ids,
                               int thread_mode) {
+    count_launch(A);
     if (thread_mode) {
         for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd;
              i += (int64_t)gridDim.x * blockDim.x) {
@@ -765,6 +783,7 @@ static int count_settle_big(Graph &g, int64_t *big) {
 // total mass (deterministic; x = reserved [+ h]) and, for IFP2, the
 // post-settle trace row (engines.py:331-335)
 __global__ void __launch_bounds__(256) k_total(RunArgs A, int include_h, int64_t settled, int write_row) {
+    count_launch(A);
     __shared__ bool is_last;
     Partial p, x;
     zero(p);
@@ -834,6 +853,7 @@ __global__ void __launch_bounds__(256) k_total(RunArgs A, int include_h, int64_t
 
 // values in original vertex order (perm: run id -> original id, or identity)
 __global__ void k_scale(RunArgs A, int include_h, double *values, const int32_t *perm) {
+    count_launch(A);
     double tot = A.ctl->mass_total;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < A.n; v += (int64_t)gridDim.x * blockDim.x) {
         double x = include_h ? A.reserved[v] + A.h[v] : A.reserved[v];
@@ -1372,6 +1392,8 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
         res->pull_ms = hc.pull_ns * 1e-6;
         res->pull_bytes = hc.pull_bytes;
         res->sparse_ms = hc.sparse_ns * 1e-6;
+        // device-counted solve kernels + the host-launched un-permute copies
+        res->launches = (int64_t)hc.launches + (d_reserved ? 1 : 0) + (d_pending ? 1 : 0);
     }
     if (hc.done == 2)
         return fail(PR_ERR_NOT_SETTLED,

@@ -29,13 +29,13 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in names if not hasattr(L, n)]
     assert not missing, missing
     assert set(names) <= set(_lib.SIGNATURES), set(names) - set(_lib.SIGNATURES)
-    assert L.pr_abi_version() == 2
+    assert L.pr_abi_version() == 3
 
 
 def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.RoundStats) == 80
     assert _lib.ROUND_DTYPE.itemsize == 80
-    assert ctypes.sizeof(_lib.RunResult) == 14 * 8
+    assert ctypes.sizeof(_lib.RunResult) == 15 * 8
 
 
 def test_library_is_sm100a_only():
