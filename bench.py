@@ -393,7 +393,8 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
                              "kernel": "partitioned round loop per GPU (k_part_pull + exchange + statistics), "
                                        "algorithmic bytes 12*E_pushed + 40*V_drained + 8*n_scan per round",
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
-                # per round: the sections' k_part_pull + k_part_reduce; init (2) and settle/total (4)
+                # per round: one k_part_pull per section (the last also reduces the statistics);
+                # init (2) and settle/total (4)
                 "gpu_launches": int((step.launches_per_round() * info["rounds"] + 6) * args.steps),
                 "clocks": clocks.summary(),
                 "exchange": ("fused: round kernel stores shares into every rank's replica (peer memory)"

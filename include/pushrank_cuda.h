@@ -277,7 +277,8 @@ int pr_part_round(pr_part *p, const double *d_shares_full, double *d_shares_mine
  * the fast form before the first round (rank-local Gauss-Seidel sections);
  * the fused-exchange setup sets it too. */
 int pr_part_set_rank(pr_part *p, int32_t parts, int32_t rank);
-/* Kernel launches of one fast round (Gauss-Seidel sections + 1). */
+/* Kernel launches of one fast round (one per Gauss-Seidel section; the
+ * last section's launch also reduces the statistics). */
 int pr_part_launches_per_round(pr_part *p, int32_t *launches);
 int pr_part_init_device(pr_part *p, double *d_shares_mine, double *d_stats);
 int pr_part_round_device(pr_part *p, const double *d_shares_full, double *d_shares_mine, int32_t fast,

@@ -72,6 +72,7 @@ struct Part {
     double *peer[2][PR_MAX_PEERS] = {};
     std::vector<void *> opened;
     unsigned long long *unit_ctr = nullptr;
+    unsigned *done = nullptr;   // last-block counter of the fast round's last section
     ~Part() {
         delete sg;
         for (void *p : opened) cudaIpcCloseMemHandle(p);
@@ -256,6 +257,12 @@ struct PullSec {
     int64_t u_lo, u_hi;
     Src src;
     int kind, last, region;
+    // the last section's last block reduces every section's partials (fixed
+    // order) into the statistics, so a round needs no separate reduction
+    unsigned *done;          // block arrival counter of the last section
+    Partial *stats;          // the reduced statistics
+    double *out9;            // and as 9 doubles (may be null)
+    unsigned long long *ctr; // unit counters to reset (PR_MAX_SECTIONS)
 };
 
 template <bool STREAM, bool PREFETCH, int SRC>
@@ -289,6 +296,36 @@ __global__ void __launch_bounds__(256, PREFETCH ? 3 : 4) k_part_pull(PartArgs A,
     if (s_mine.n) __threadfence_system();   // peer stores performed before the round's barrier
     block_reduce(p);
     if (threadIdx.x == 0) A.partials[(int64_t)S.region * gridDim.x + blockIdx.x] = p;
+    if (!S.last) return;
+    __shared__ bool is_last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        is_last = atomicAdd(S.done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    Partial acc;
+    zero(acc);
+    const int64_t total = (int64_t)(S.region + 1) * gridDim.x;
+    for (int64_t b = threadIdx.x; b < total; b += blockDim.x) add(acc, load_partial(A.partials + b));
+    block_reduce(acc);
+    if (threadIdx.x == 0) {
+        *S.stats = acc;
+        if (S.out9) {
+            S.out9[0] = acc.l1;
+            S.out9[1] = acc.above;
+            S.out9[2] = acc.nd_above;
+            S.out9[3] = (double)acc.nact;
+            S.out9[4] = (double)acc.work;
+            S.out9[5] = (double)acc.push_ops;
+            S.out9[6] = (double)acc.push_dang;
+            S.out9[7] = (double)acc.conv_all;
+            S.out9[8] = (double)acc.conv_scan;
+        }
+        for (int k = 0; k < PR_MAX_SECTIONS; ++k) S.ctr[k] = 0;
+        *S.done = 0;
+    }
 }
 
 // state 0 (h = 1) of the fast form: shares through the ShareOut
@@ -466,9 +503,10 @@ int part_create(Ctx &ctx, int64_t owned, int64_t slot, const int64_t *in_off, co
         if ((rc = ensure(P->partials, sizeof(Partial) * (grid_for(owned, 256) +
                                                          (int64_t)ctx.sm_count * 4 * PR_MAX_SECTIONS + 1))))
             break;
-        if ((rc = ensure(P->stats, sizeof(Partial) + 32 + 8 * PR_MAX_SECTIONS))) break;
+        if ((rc = ensure(P->stats, sizeof(Partial) + 32 + 8 * PR_MAX_SECTIONS + 16))) break;
         P->unit_ctr = (unsigned long long *)(P->stats.as<char>() + sizeof(Partial) + 32);
-        cudaMemsetAsync(P->unit_ctr, 0, 8 * PR_MAX_SECTIONS, ctx.stream);
+        P->done = (unsigned *)(P->unit_ctr + PR_MAX_SECTIONS);
+        cudaMemsetAsync(P->unit_ctr, 0, 8 * PR_MAX_SECTIONS + 16, ctx.stream);
         if (cudaStreamSynchronize(ctx.stream) != cudaSuccess) rc = fail(PR_ERR_CUDA, "partition upload");
     } while (0);
     if (rc) { delete P; return rc; }
@@ -574,7 +612,8 @@ static BinView part_view(Part &P) {
 // one round: a launch per section; x = shares of the previous round (all
 // ranks), x_new = this round's full vector (own slot written by the earlier
 // sections); kind 0 Jacobi / 1 transition / 2 GS (ignored without sections)
-static void launch_part_pull(Part &P, const double *s_full, const double *x_new, int kind, const ShareOut &so) {
+static void launch_part_pull(Part &P, const double *s_full, const double *x_new, int kind, const ShareOut &so,
+                             double *out9) {
     cudaStream_t st = P.ctx->stream;
     const unsigned g = (unsigned)P.blocks;
     const int32_t *out = P.outside.as<int32_t>();
@@ -589,6 +628,10 @@ static void launch_part_pull(Part &P, const double *s_full, const double *x_new,
         S.src = Src{s_full, x_new, S.kind ? (int)Sc.sec_row[k] : 0, (int)((int64_t)P.rank * P.slot)};
         S.last = k == nsec - 1;
         S.region = k;
+        S.done = P.done;
+        S.stats = P.stats.as<Partial>();
+        S.out9 = out9;
+        S.ctr = P.unit_ctr;
         BinView T = part_view(P);
         T.unit_ctr = P.unit_ctr + k;
         if (P.stream_csc) {
@@ -643,7 +686,7 @@ int part_set_peers(Part &P, const void *handles) {
 // reduction); builds the schedule if needed
 int part_launches_per_round(Part &P, int *out) {
     PR_TRY(ensure_part_sched(P));
-    *out = (P.nsec > 1 ? P.nsec : 1) + 1;
+    *out = P.nsec > 1 ? P.nsec : 1;   // the last section's launch also reduces the statistics
     return PR_OK;
 }
 
@@ -706,10 +749,7 @@ int part_round_fused(Part &P, int parity, int kind, double *d_stats9) {
     if (P.parts < 1 || !P.peer[0][P.rank]) return fail(PR_ERR_STATE, "fused exchange not set up");
     PR_TRY(ensure_part_sched(P));
     launch_part_pull(P, P.peer[parity & 1][P.rank], P.peer[1 - (parity & 1)][P.rank], kind,
-                     fused_out(P, 1 - (parity & 1)));
-    k_part_reduce<<<1, 256, 0, P.ctx->stream>>>(P.partials.as<Partial>(),
-                                                (unsigned)(P.blocks * (P.nsec > 1 ? P.nsec : 1)),
-                                                P.stats.as<Partial>(), d_stats9, P.unit_ctr, PR_MAX_SECTIONS);
+                     fused_out(P, 1 - (parity & 1)), d_stats9);
     PR_CUDA(cudaGetLastError());
     return PR_OK;
 }
@@ -733,14 +773,13 @@ int part_round_device(Part &P, const double *d_s_full, double *d_s_mine, int fas
         memset(&so, 0, sizeof(so));
         so.mine = d_s_mine;
         // d_s_mine is this rank's slot of the next round's full vector
-        launch_part_pull(P, d_s_full, d_s_mine - (int64_t)P.rank * P.slot, kind, so);
-        g = (unsigned)(P.blocks * (P.nsec > 1 ? P.nsec : 1));
+        launch_part_pull(P, d_s_full, d_s_mine - (int64_t)P.rank * P.slot, kind, so, d_stats9);
     } else {
         g = grid_for(P.owned, 256);
         k_part_round<<<g, 256, 0, st>>>(args_of(P), d_s_full, d_s_mine);
+        k_part_reduce<<<1, 256, 0, st>>>(P.partials.as<Partial>(), g, P.stats.as<Partial>(), d_stats9, P.unit_ctr,
+                                         PR_MAX_SECTIONS);
     }
-    k_part_reduce<<<1, 256, 0, st>>>(P.partials.as<Partial>(), g, P.stats.as<Partial>(), d_stats9, P.unit_ctr,
-                                     PR_MAX_SECTIONS);
     PR_CUDA(cudaGetLastError());
     return PR_OK;
 }
