@@ -62,7 +62,8 @@ struct Part {
     int64_t blocks = 0;       // persistent pull grid
     bool stream_csc = false;  // evict-first index loads (round working set > 0.6 L2)
     bool prefetch = false;    // drain inputs ahead of the gathers (round working set < 4 L2)
-    int nsec = 1;             // rank-local Gauss-Seidel sections (IFP2, rows == local ids)
+    int nsec = 1;             // rank-local Gauss-Seidel sections
+    int64_t sec_id[PR_MAX_SECTIONS + 1] = {};   // local-id bound of earlier sections' sources
     DevBuf outside;           // int32: owned vertices outside the schedule
     int64_t n_outside = 0;
     // fused exchange: replicas of the full share vector (parity 0/1) of
@@ -518,6 +519,74 @@ __global__ void k_ids_identity(const int32_t *ids, int64_t count, unsigned long 
     GRID_STRIDE(i, count) if (ids[i] != (int32_t)i) atomicAdd(bad, 1ull);
 }
 
+// IFP1 partitions: the schedule interleaves class-0 rows (in > 0, out > 0)
+// with dangling receivers by degree.  In a run-layout partition the class-0
+// vertices are the local ids [0, c0), and the stable degree sort keeps them
+// in id order, so the sources of sections before k are the local ids below
+// the first class-0 id at or after row sec_row[k] (as the engine's IFP1
+// sections, rounds.cu).  Both properties are checked; on failure the caller
+// keeps one section.
+__global__ void k_part_c0(const int64_t *in_off, const int32_t *deg, int64_t owned, unsigned long long *cnt) {
+    GRID_STRIDE(v, owned) if (deg[v] > 0 && in_off[v + 1] > in_off[v]) atomicAdd(cnt, 1ull);
+}
+
+__global__ void k_part_c0_check(const int64_t *in_off, const int32_t *deg, int64_t owned, int64_t c0,
+                                const int32_t *ids, int64_t count, int32_t *pos, unsigned long long *bad, int phase) {
+    if (phase == 0) {
+        GRID_STRIDE(v, owned) {
+            const bool c = deg[v] > 0 && in_off[v + 1] > in_off[v];
+            if (c != (v < c0)) atomicAdd(bad, 1ull);
+        }
+        GRID_STRIDE(r, count) if (ids[r] < c0) pos[ids[r]] = (int32_t)r;
+    } else {
+        GRID_STRIDE(r, count) {
+            const int32_t v = ids[r];
+            if (v < c0 && v + 1 < c0 && pos[v + 1] <= (int32_t)r) atomicAdd(bad, 1ull);
+        }
+    }
+}
+
+__global__ void k_part_sec_id(const int32_t *ids, int64_t count, int64_t c0, const int64_t *bounds, int nsec,
+                              int64_t *out) {
+    const int k = threadIdx.x;
+    if (k > nsec) return;
+    int64_t r = bounds[k];
+    while (r < count && ids[r] >= c0) ++r;
+    out[k] = r < count ? ids[r] : c0;
+}
+
+static int part_sections_by_id(Part &P, Graph &g) {
+    Ctx &ctx = *P.ctx;
+    cudaStream_t st = ctx.stream;
+    auto &S = g.sched[P.which];
+    DevBuf cnt, pos, bnd, out;
+    PR_TRY(ensure(cnt, 16));
+    PR_TRY(ensure(pos, 4 * (P.owned > 0 ? P.owned : 1)));
+    PR_TRY(ensure(bnd, 8 * (PR_MAX_SECTIONS + 1)));
+    PR_TRY(ensure(out, 8 * (PR_MAX_SECTIONS + 1)));
+    PR_CUDA(cudaMemsetAsync(cnt.ptr, 0, 16, st));
+    const unsigned gr = grid_for(P.owned > S.count ? P.owned : S.count, 256) > 4096
+                            ? 4096 : grid_for(P.owned > S.count ? P.owned : S.count, 256);
+    unsigned long long *c = cnt.as<unsigned long long>();
+    if (P.owned) k_part_c0<<<gr, 256, 0, st>>>(P.in_off.as<int64_t>(), P.deg.as<int32_t>(), P.owned, c);
+    unsigned long long c0 = 0;
+    PR_CUDA(cudaMemcpyAsync(&c0, c, 8, cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaStreamSynchronize(st));
+    for (int phase = 0; phase < 2; ++phase)
+        k_part_c0_check<<<gr, 256, 0, st>>>(P.in_off.as<int64_t>(), P.deg.as<int32_t>(), P.owned, (int64_t)c0,
+                                            S.ids.as<int32_t>(), S.count, pos.as<int32_t>(), c + 1, phase);
+    PR_CUDA(cudaMemcpyAsync(bnd.ptr, S.sec_row, 8 * (S.nsec + 1), cudaMemcpyHostToDevice, st));
+    k_part_sec_id<<<1, 32, 0, st>>>(S.ids.as<int32_t>(), S.count, (int64_t)c0, bnd.as<int64_t>(), S.nsec,
+                                    out.as<int64_t>());
+    unsigned long long nbad = 0;
+    PR_CUDA(cudaMemcpyAsync(&nbad, c + 1, 8, cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaMemcpyAsync(P.sec_id, out.ptr, 8 * (S.nsec + 1), cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaStreamSynchronize(st));
+    PR_CUDA(cudaGetLastError());
+    if (nbad) return fail(PR_ERR_STATE, "partition: class-0 rows out of id order");
+    return PR_OK;
+}
+
 // the fast form's pull schedule, built on first use
 static int ensure_part_sched(Part &P) {
     if (P.sg) return PR_OK;
@@ -547,26 +616,29 @@ static int ensure_part_sched(Part &P) {
         // rank-local Gauss-Seidel sections, as the engine chooses them
         // (rounds.cu): IFP2 on rows that are the local ids in order (a
         // run-layout partition), 2 past 1.5x L2 of round working set, 4 past 16x
-        P.nsec = 1;
-        if (P.which == 1) {
-            P.nsec = ws > 16.0 * l2 ? 4 : ws > 1.5 * l2 ? 2 : 1;
-            if (const char *e = getenv("PUSHRANK_GS_SECTIONS")) P.nsec = atoi(e);
-            if (P.nsec < 1) P.nsec = 1;
-            if (P.nsec > PR_MAX_SECTIONS) P.nsec = PR_MAX_SECTIONS;
-            if (P.nsec > 1) {
-                auto &S = g->sched[P.which];
-                DevBuf bad;
-                if ((rc = ensure(bad, 8))) break;
-                cudaMemsetAsync(bad.ptr, 0, 8, st);
-                if (S.count) k_ids_identity<<<grid_for(S.count, 256), 256, 0, st>>>(S.ids.as<int32_t>(), S.count,
-                                                                                  bad.as<unsigned long long>());
-                unsigned long long nbad = 0;
-                cudaMemcpyAsync(&nbad, bad.ptr, 8, cudaMemcpyDeviceToHost, st);
-                cudaStreamSynchronize(st);
-                if (nbad) P.nsec = 1;
-            }
+        P.nsec = ws > 16.0 * l2 ? 4 : ws > 1.5 * l2 ? 2 : 1;
+        if (const char *e = getenv("PUSHRANK_GS_SECTIONS")) P.nsec = atoi(e);
+        if (P.nsec < 1) P.nsec = 1;
+        if (P.nsec > PR_MAX_SECTIONS) P.nsec = PR_MAX_SECTIONS;
+        auto &Sc = g->sched[P.which];
+        if (P.nsec > 1 && P.which == 1) {
+            // IFP2: the rows must be the local ids in order
+            DevBuf bad;
+            if ((rc = ensure(bad, 8))) break;
+            cudaMemsetAsync(bad.ptr, 0, 8, st);
+            if (Sc.count) k_ids_identity<<<grid_for(Sc.count, 256), 256, 0, st>>>(Sc.ids.as<int32_t>(), Sc.count,
+                                                                                bad.as<unsigned long long>());
+            unsigned long long nbad = 0;
+            cudaMemcpyAsync(&nbad, bad.ptr, 8, cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            if (nbad) P.nsec = 1;
         }
         if ((rc = ensure_units(*g, P.which, P.blocks, P.nsec))) break;
+        for (int k = 0; k <= PR_MAX_SECTIONS; ++k) P.sec_id[k] = k <= Sc.nsec ? Sc.sec_row[k] : Sc.count;
+        if (P.nsec > 1 && P.which == 0 && part_sections_by_id(P, *g) != PR_OK) {
+            P.nsec = 1;
+            if ((rc = ensure_units(*g, P.which, P.blocks, 1))) break;
+        }
         // owned vertices outside the schedule: no inflow, drained alone
         {
             DevBuf cnt;
@@ -625,7 +697,7 @@ static void launch_part_pull(Part &P, const double *s_full, const double *x_new,
         S.u_lo = nsec > 1 ? Sc.sec_unit[k] : 0;
         S.u_hi = nsec > 1 ? Sc.sec_unit[k + 1] : Sc.n_units;
         S.kind = nsec > 1 ? kind : 0;
-        S.src = Src{s_full, x_new, S.kind ? (int)Sc.sec_row[k] : 0, (int)((int64_t)P.rank * P.slot)};
+        S.src = Src{s_full, x_new, S.kind ? (int)P.sec_id[k] : 0, (int)((int64_t)P.rank * P.slot)};
         S.last = k == nsec - 1;
         S.region = k;
         S.done = P.done;

@@ -132,19 +132,21 @@ def test_fused_exchange_emulated(algorithm):
     assert abs(r1 - o.iterations) <= 1
 
 
+@pytest.mark.parametrize("algorithm", ["ifp2", "ifp1"])
 @pytest.mark.parametrize("sections", [2, 3])
-def test_rank_local_gauss_seidel_emulated(sections, monkeypatch):
-    """Rank-local Gauss-Seidel sections in the partitioned local step (IFP2,
-    run-layout partitions; PUSHRANK_GS_SECTIONS forces them at C2): 2 ranks
-    emulated on one device, fused exchange bit-identical to the all-gather
-    form, the sync twin's fixed point (L1 <= 1e-9, identical top-100), and
-    fewer rounds than Jacobi."""
+def test_rank_local_gauss_seidel_emulated(sections, algorithm, monkeypatch):
+    """Rank-local Gauss-Seidel sections in the partitioned local step
+    (run-layout partitions; PUSHRANK_GS_SECTIONS forces them at C2; IFP1 by
+    the id bound of earlier sections' class-0 sources): 2 ranks emulated on
+    one device, fused exchange bit-identical to the all-gather form, the sync
+    twin's fixed point (L1 <= 1e-9, identical top-100), and fewer rounds than
+    Jacobi."""
     monkeypatch.setenv("PUSHRANK_GS_SECTIONS", str(sections))
-    fused, r1, g = _emulate("ifp2", 2, True, config="c2")
-    gathered, r2, _ = _emulate("ifp2", 2, False, config="c2")
+    fused, r1, g = _emulate(algorithm, 2, True, config="c2")
+    gathered, r2, _ = _emulate(algorithm, 2, False, config="c2")
     assert np.array_equal(fused, gathered)
     assert r1 == r2
-    o = oracle.sync_simulate(g, "ifp2", threshold=1e-10)
+    o = oracle.sync_simulate(g, algorithm, threshold=1e-10)
     assert np.abs(fused - o.values).sum() <= 1e-9
     top = lambda v: np.lexsort((np.arange(v.size), -v))[:100]   # noqa: E731
     assert np.array_equal(top(fused), top(o.values))
