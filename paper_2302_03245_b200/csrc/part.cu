@@ -604,6 +604,14 @@ static int ensure_part_sched(Part &P) {
         cudaMemcpyAsync(g->in_off.ptr, P.in_off.ptr, 8 * (P.owned + 1), cudaMemcpyDeviceToDevice, st);
         if (P.edges) cudaMemcpyAsync(g->in_src.ptr, P.in_src.ptr, 4 * P.edges, cudaMemcpyDeviceToDevice, st);
         if (P.owned) cudaMemcpyAsync(g->out_deg.ptr, P.deg.ptr, 4 * P.owned, cudaMemcpyDeviceToDevice, st);
+        // rows' sources ascending on HBM-bound partitions, as the engine's run
+        // layout (graph.cu): past 16x L2 of round working set
+        {
+            const double l2b = (double)(ctx.l2_bytes ? ctx.l2_bytes : (size_t)126 << 20);
+            bool sort_rows = 4.0 * (double)P.edges + 8.0 * (double)P.slot > 16.0 * l2b;
+            if (const char *e = getenv("PUSHRANK_SORT_ROWS")) sort_rows = atoi(e) != 0;
+            if (sort_rows && (rc = sort_csc_rows(ctx, g->in_off, g->in_src, P.owned, P.edges))) break;
+        }
         // IFP2 pulls into non-dangling rows only (receives = !dangling), IFP1 into all
         P.which = P.algorithm == PR_ALGO_IFP2 ? 1 : 0;
         if ((rc = ensure_sched(*g, P.which))) break;
