@@ -14,8 +14,8 @@
 // unit, issued at the start of the previous one); a launch covers the unit
 // range of one Gauss-Seidel section.  Every summation order is fixed by the
 // schedule (row sums do not depend on which block claims a unit), so a pull
-// round is run-to-run deterministic; the engine's round-0 seed scatter and
-// sparse push rounds add with atomics (rounds.cu).
+// round is run-to-run deterministic; the engine's sparse push rounds add with
+// atomics (rounds.cu).
 #pragma once
 
 #include "internal.cuh"

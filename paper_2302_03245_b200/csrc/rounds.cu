@@ -372,7 +372,7 @@ __global__ void k_reset(RunArgs A) {
 // and its drain.  Vertices in D go through the common epilogue; vertices
 // outside D never receive mass, so their post-drain value is constant for
 // every later row (recorded as constants) and their round-0 shares are
-// scattered once by k_seed_scatter.
+// gathered by the first dense round (their shares sit in buffer 0).
 __global__ void __launch_bounds__(256) k_init(RunArgs A) {
     count_launch(A);
     Partial p, cst;
@@ -411,7 +411,11 @@ __global__ void __launch_bounds__(256) k_init(RunArgs A) {
                     if (A.dtc) p.push_dang += A.dtc[v];
                 }
                 A.h[v] = after;
-                A.s[v] = 0.0;
+                // an active vertex outside D has in-degree 0 (a round-0 seed):
+                // its share is gathered by the first dense round like any other
+                // source's -- in fixed order, no scatter -- and k_clear_seeds
+                // zeroes it during round 1, before this buffer is read again
+                A.s[v] = active && dv > 0 ? __ddiv_rn(__dmul_rn(A.c, 1.0), (double)dv) : 0.0;
                 cst.l1 += after;
                 if (after > A.xi) {
                     cst.above += after;
@@ -427,20 +431,12 @@ __global__ void __launch_bounds__(256) k_init(RunArgs A) {
     finish_round(A, p, 0, true, true, cst);
 }
 
-// round-0 shares of active vertices outside D (in-degree 0): scatter once
-__global__ void __launch_bounds__(256) k_seed_scatter(RunArgs A) {
-    count_launch(A);
-    if (!(1.0 > A.xi)) return;
-    int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < A.n_seed; i += nwarps) {
-        int32_t u = A.seeds[i];
-        int32_t du = A.deg[u];
-        if (du <= 0) continue;
-        double share = __ddiv_rn(__dmul_rn(A.c, 1.0), (double)du);
-        for (int64_t e = A.push_off[u] + lane; e < A.push_off[u + 1]; e += 32) atomicAdd(&A.h[A.push_tgt[e]], share);
-    }
+// Round 1 (any kind): clear the round-0 seed shares in buffer 0, which
+// round 2 reads next; round 1 itself reads buffer 1.
+__device__ __forceinline__ void clear_seeds(const RunArgs &A, int64_t t) {
+    if (t != 1) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.n_seed; i += (int64_t)gridDim.x * blockDim.x)
+        A.s[A.seeds[i]] = 0.0;
 }
 
 // Dense round t: h(t+1)_v = h_drained(t)_v + sum_{u in in(v)} s(t)_u over D,
@@ -504,6 +500,7 @@ __global__ void __launch_bounds__(256, PREFETCH ? PULL_MIN_BLOCKS - 1 : PULL_MIN
     const bool app = A.ctl->append != 0;
     long long *F = A.frontier + (r & 1) * A.fcap;
     int64_t *fsize = &A.ctl->fsize[r & 1];
+    clear_seeds(A, t);
     // this launch's section and the sweep kind (Src in bins.cuh)
     const int64_t u_lo = A.sec_unit[A.sec], u_hi = A.sec_unit[A.sec + 1];
     Src src{s_in, A.s + (r & 1) * A.n, 0, 0};
@@ -596,6 +593,7 @@ __global__ void __launch_bounds__(256) k_scan(RunArgs A) {
     count_launch(A);
     if (A.use_graph && !round_is(A, 1)) return;
     const int64_t t = A.ctl->round;
+    clear_seeds(A, t);
     const int64_t r = t + 1;
     const bool app = A.ctl->append != 0;
     long long *F = A.frontier + (r & 1) * A.fcap;
@@ -946,7 +944,7 @@ static int build_graph(Plan &P, cudaGraph_t *out_g, cudaGraphExec_t *out_exec) {
         PR_TRY(add_kernel(G, &n_seed, &n_init, 1, (void *)k_ex_prep, P.g_all, 256, args));
     } else {
         PR_TRY(add_kernel(G, &n_init, &n_reset, 1, (void *)k_init, P.g_red, 256, args));
-        PR_TRY(add_kernel(G, &n_seed, &n_init, 1, (void *)k_seed_scatter, P.g_push, 256, args));
+        n_seed = n_init;   // round-0 seeds are gathered by the first dense round
     }
     cudaGraph_t body;
     PR_TRY(add_while(G, &n_while, &n_seed, A.h_loop, &body));
@@ -1286,7 +1284,6 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
             k_ex_prep<<<P.g_all, 256, 0, st>>>(A);
         } else {
             k_init<<<P.g_red, 256, 0, st>>>(A);
-            k_seed_scatter<<<P.g_push, 256, 0, st>>>(A);
         }
         std::vector<double> obs_r, obs_h;
         if (p.on_round) {
