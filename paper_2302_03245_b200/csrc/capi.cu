@@ -43,8 +43,10 @@ int upload_graph(Ctx &ctx, int64_t n, int64_t m, const int64_t *out_off, const i
 int export_graph(Graph &g, int64_t *out_off, int64_t *out_tgt, int64_t *in_off, int64_t *in_src);
 int export_i32(Ctx &ctx, const DevBuf &src, int64_t count, int64_t *host);
 int export_i64(Ctx &ctx, const DevBuf &src, int64_t count, int64_t *host);
+#ifdef PR_UBENCH
 int debug_gather(Graph &g0, int variant, int iters, int blocks_per_sm, double *ms_out);
 int debug_graph(Ctx &ctx, int variant, int64_t iters, int blocks, double *us_out);
+#endif
 struct Part;
 int part_create(Ctx &ctx, int64_t owned, int64_t slot, const int64_t *in_off, const int64_t *in_src, int64_t edges,
                 const int64_t *deg, const int64_t *row_len, const int64_t *dtc, const uint8_t *dang,
@@ -642,6 +644,7 @@ int pr_part_destroy(pr_part *p) {
     return PR_OK;
 }
 
+#ifdef PR_UBENCH  // tools/ubench.cu, variant libraries only (tools/ubench.py)
 // diagnostics (not part of the documented ABI): gather microbenchmarks
 int pr_debug_gather(pr_graph *g, int variant, int iters, int blocks_per_sm, double *ms_out) {
     CHECK_PTR(g, "graph");
@@ -654,5 +657,6 @@ int pr_debug_graph(pr_ctx *ctx, int variant, int64_t iters, int blocks, double *
     PR_TRY(set_device(ctx->c));
     return debug_graph(ctx->c, variant, iters, blocks, us_out);
 }
+#endif
 
 }  // extern "C"

@@ -72,6 +72,9 @@ struct Part {
     void *own_full[2] = {nullptr, nullptr};
     double *peer[2][PR_MAX_PEERS] = {};
     std::vector<void *> opened;
+    // the replicas of every rank are mapped (set_peers / set_peer_ptrs) and
+    // not yet closed: the fused entry points refuse to run otherwise
+    bool fused_ready = false;
     unsigned long long *unit_ctr = nullptr;
     unsigned *done = nullptr;   // last-block counter of the fast round's last section
     ~Part() {
@@ -744,6 +747,7 @@ int part_share_buffers(Part &P, int parts, int rank, void **d_full, void *ipc) {
     for (int r = 0; r < PR_MAX_PEERS; ++r) P.peer[0][r] = P.peer[1][r] = nullptr;
     P.peer[0][rank] = (double *)P.own_full[0];
     P.peer[1][rank] = (double *)P.own_full[1];
+    P.fused_ready = false;   // until set_peers has mapped the other ranks' replicas
     return PR_OK;
 }
 
@@ -759,6 +763,7 @@ int part_set_peers(Part &P, const void *handles) {
             P.opened.push_back(ptr);
         }
     }
+    P.fused_ready = true;
     return PR_OK;
 }
 
@@ -788,6 +793,7 @@ int part_close_peers(Part &P) {
     P.opened.clear();
     for (int r = 0; r < PR_MAX_PEERS; ++r)
         if (r != P.rank) P.peer[0][r] = P.peer[1][r] = nullptr;
+    P.fused_ready = false;
     return PR_OK;
 }
 
@@ -801,6 +807,8 @@ int part_set_peer_ptrs(Part &P, int parts, int rank, void *const *ptrs) {
         P.peer[0][r] = (double *)ptrs[2 * r];
         P.peer[1][r] = (double *)ptrs[2 * r + 1];
     }
+    P.fused_ready = true;
+    for (int r = 0; r < parts; ++r) P.fused_ready = P.fused_ready && P.peer[0][r] && P.peer[1][r];
     return PR_OK;
 }
 
@@ -814,7 +822,7 @@ static ShareOut fused_out(Part &P, int parity) {
 }
 
 int part_init_fused(Part &P, double *d_stats9) {
-    if (P.parts < 1 || !P.peer[0][P.rank]) return fail(PR_ERR_STATE, "fused exchange not set up");
+    if (P.parts < 1 || !P.fused_ready) return fail(PR_ERR_STATE, "fused exchange not set up (or closed)");
     PR_TRY(ensure_part_sched(P));
     cudaStream_t st = P.ctx->stream;
     const unsigned g = grid_for(P.owned, 256);
@@ -826,7 +834,7 @@ int part_init_fused(Part &P, double *d_stats9) {
 
 // round reading this rank's replica `parity`, writing every replica 1-parity
 int part_round_fused(Part &P, int parity, int kind, double *d_stats9) {
-    if (P.parts < 1 || !P.peer[0][P.rank]) return fail(PR_ERR_STATE, "fused exchange not set up");
+    if (P.parts < 1 || !P.fused_ready) return fail(PR_ERR_STATE, "fused exchange not set up (or closed)");
     PR_TRY(ensure_part_sched(P));
     launch_part_pull(P, P.peer[parity & 1][P.rank], P.peer[1 - (parity & 1)][P.rank], kind,
                      fused_out(P, 1 - (parity & 1)), d_stats9);

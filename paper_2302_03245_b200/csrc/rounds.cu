@@ -413,8 +413,12 @@ __global__ void __launch_bounds__(256) k_init(RunArgs A) {
                 A.h[v] = after;
                 // an active vertex outside D has in-degree 0 (a round-0 seed):
                 // its share is gathered by the first dense round like any other
-                // source's -- in fixed order, no scatter -- and k_clear_seeds
-                // zeroes it during round 1, before this buffer is read again
+                // source's -- in fixed order, no scatter -- and clear_seeds
+                // (called by k_pull / k_scan) zeroes it during round 1, before
+                // this buffer is read again.  Safe under Gauss-Seidel sections
+                // only because seed ids lie at or above every section bound
+                // (checked in run_rounds): the round-1 transition sweep never
+                // reads a seed's entry of x_new (buffer 0) while it is zeroed
                 A.s[v] = active && dv > 0 ? __ddiv_rn(__dmul_rn(A.c, 1.0), (double)dv) : 0.0;
                 cst.l1 += after;
                 if (after > A.xi) {
@@ -1190,6 +1194,11 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     A.sec_of = (algo == PR_ALGO_IFP1 && S.nsec > 1) ? S.sec_of.as<uint8_t>() : nullptr;
     for (int k = 0; k <= PR_MAX_SECTIONS; ++k)
         A.sec_id[k] = k <= S.nsec ? (A.sec_of ? S.sec_id[k] : S.sec_row[k]) : S.count;
+    // clear_seeds invariant: the round-0 seeds (in-degree 0, run-layout class
+    // 1, ids >= class0_end) are never an "early" source of any section
+    if (S.nsec > 1 && g.class0_end >= 0)
+        for (int k = 0; k <= S.nsec; ++k)
+            if (A.sec_id[k] > g.class0_end) return fail(PR_ERR_STATE, "section bound above the first seed id");
     for (int k = 0; k <= PR_MAX_SECTIONS; ++k) {
         A.sec_row[k] = k <= S.nsec ? S.sec_row[k] : S.count;
         A.sec_unit[k] = k <= S.nsec ? S.sec_unit[k] : S.n_units;

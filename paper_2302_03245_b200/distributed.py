@@ -339,18 +339,21 @@ def run_partitioned_queued(step, comm, part: Partition, algorithm: str, damping:
                 nb = max(1, min(batch, max_rounds - t0))
                 queue_batch(nb, t0)
                 return nb
-            if cache["graph"] is None and t0 > 0:
+            if t0 == 0:
+                # the first batch of every solve runs eagerly: it holds the
+                # Jacobi and transition sweeps (sweep_kind 0 and 1), which the
+                # captured steady-state batch does not
+                queue_batch(batch, t0)
+                return batch
+            if cache["graph"] is None:
                 # capture once the schedule exists (built by the first, eager
-                # batch); every later batch has the same parities and sweep
-                # kinds (Gauss-Seidel from round 2 on) as this one
+                # batch); every later batch (t0 > 0) has the same parities and
+                # sweep kinds (Gauss-Seidel from round 2 on) as this one
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=stream):
                     queue_batch(batch, t0)
                 cache["graph"] = g
-            if cache["graph"] is None:
-                queue_batch(batch, t0)
-            else:
-                cache["graph"].replay()
+            cache["graph"].replay()
             return batch
 
         if fused:
@@ -627,7 +630,9 @@ class CudaLocalStep:
 
     def close_fused(self, comm) -> None:
         """Collective: unmap the other ranks' replicas, then a barrier, so
-        that no rank frees a replica (at destruction) that another still maps."""
+        that no rank frees a replica (at destruction) that another still maps.
+        The captured batch graph holds the unmapped peer addresses: drop it."""
+        self._queued = None
         self._lib.check(self.L.pr_part_close_peers(self.h), "pr_part_close_peers")
         comm.dist.barrier()
 

@@ -3,8 +3,14 @@ import ctypes
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2302_03245_b200 import _lib
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+if "PUSHRANK_LIB" not in os.environ:  # pr_debug_graph lives in tools/ubench.cu (variant library)
+    import subprocess
+    subprocess.run([sys.executable, os.path.join(ROOT, "tools", "var.py"), "ubench", "-DPR_UBENCH"], check=True,
+                   env=dict(os.environ, VAR_EXTRA=os.path.join(ROOT, "tools", "ubench.cu")))
+    os.environ["PUSHRANK_LIB"] = os.path.join(ROOT, "build", "var", "lib_ubench.so")
+from paper_2302_03245_b200 import _lib  # noqa: E402
 
 L = _lib.load()
 L.pr_debug_graph.restype = ctypes.c_int

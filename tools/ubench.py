@@ -1,6 +1,14 @@
-"""Gather microbenchmarks on the C2 run layout (pr_debug_gather)."""
-import ctypes, os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+"""Gather microbenchmarks on the C2 run layout (pr_debug_gather).
+
+tools/ubench.cu is not part of the product library: this script builds a
+variant library with it (tools/var.py, VAR_EXTRA) and loads that one."""
+import ctypes, os, subprocess, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+if "PUSHRANK_LIB" not in os.environ:
+    subprocess.run([sys.executable, os.path.join(ROOT, "tools", "var.py"), "ubench", "-DPR_UBENCH"], check=True,
+                   env=dict(os.environ, VAR_EXTRA=os.path.join(ROOT, "tools", "ubench.cu")))
+    os.environ["PUSHRANK_LIB"] = os.path.join(ROOT, "build", "var", "lib_ubench.so")
 import paper_2302_03245_b200 as P
 from paper_2302_03245_b200 import _lib, synthetic
 
