@@ -68,6 +68,10 @@ def lib():
         L.orc_sync_rounds.restype = _I
         L.orc_sync_rounds.argtypes = [ctypes.c_int, _I, _i64p, _i64p, _i64p, ctypes.c_void_p,
                                       _D, _D, _I, _f64p, _f64p, _rowp, _I, ctypes.POINTER(_I)]
+        L.orc_sync_rounds_pull.restype = _I
+        L.orc_sync_rounds_pull.argtypes = [ctypes.c_int, _I, _i64p, _i64p, _i64p, _i64p, ctypes.c_void_p,
+                                           _D, _D, _I, ctypes.c_int, _f64p, _f64p, _rowp, _I,
+                                           ctypes.POINTER(_I)]
         L.orc_settle.restype = _I
         L.orc_settle.argtypes = [_I, _i64p, _i64p, _i64p, _i64p, _D, _f64p, _f64p]
         L.orc_power.restype = _I
@@ -170,11 +174,16 @@ VARIANTS = {"ifp1": 0, "ifp2": 1, "fp-full": 2}
 
 
 def sync_simulate(g, variant: str = "ifp1", damping: float = 0.85, threshold: float = 1e-10,
-                  max_iterations: int = 1_000_000, pg=None) -> SimpleNamespace:
+                  max_iterations: int = 1_000_000, pg=None, threads: int = 0) -> SimpleNamespace:
     """Restates engines.py:349-485 (round-synchronous twin).
 
     ``rows`` is a structured array (ROW_DTYPE) with one row per state; an
     ifp2 run appends the post-settle row (engines.py:458-472).
+
+    ``threads > 0`` runs the rounds as a CSC pull over that many threads
+    (orc_sync_rounds_pull): the reserved/pending state is bit-identical to
+    the sequential scatter form (tests/test_oracle_golden.py checks it), the
+    trace's float sums are combined per thread.  For the full-size configs.
     """
     if variant not in VARIANTS:
         raise ValueError(f"unknown variant {variant!r}")
@@ -192,7 +201,20 @@ def sync_simulate(g, variant: str = "ifp1", damping: float = 0.85, threshold: fl
     reserved = np.zeros(n, np.float64)
     h = np.zeros(n, np.float64)
     cap = 4096
-    while True:
+    if threads > 0:
+        row_len = np.ascontiguousarray(np.diff(offsets), np.int64)
+        while True:
+            rows = np.zeros(cap, ROW_DTYPE)
+            nrows = _I(0)
+            it = lib().orc_sync_rounds_pull(VARIANTS[variant], n, g.in_offsets,
+                                            np.ascontiguousarray(g.in_sources if g.m else np.zeros(1, np.int64)),
+                                            g.out_degree, row_len, dt.ctypes.data if dt is not None else None,
+                                            damping, threshold, max_iterations, int(threads), reserved, h,
+                                            rows, cap, ctypes.byref(nrows))
+            if it != -2:
+                break
+            cap *= 4
+    while threads <= 0:
         rows = np.zeros(cap, ROW_DTYPE)
         nrows = _I(0)
         targets_c = np.ascontiguousarray(targets if targets.size else np.zeros(1, np.int64))

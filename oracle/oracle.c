@@ -264,6 +264,155 @@ int64_t orc_sync_rounds(int variant, int64_t n, const int64_t *offsets, const in
     return settled ? iterations : -1;
 }
 
+/*
+ * The same rounds as orc_sync_rounds, restated as a pull over the CSC and
+ * spread over `threads` POSIX threads, for the full-size configs (C5: 1.06 B
+ * edges, where the sequential scatter takes tens of minutes).  Bit-identity
+ * with the scatter form: np.bincount (engines.py:444-448) adds target v's
+ * contributions in CSR edge order, i.e. ascending source -- exactly the
+ * order of v's CSC column (graph.py:161-164, stable argsort) -- and an
+ * inactive source contributes +0.0, which leaves a non-negative sum
+ * unchanged.  So inflow[v] = sum over v's column of share[u] (share 0 when
+ * u is inactive) is the same double, bit for bit.  Receivers: every vertex
+ * (ifp1, fp-full) or the non-dangling ones (ifp2: the live CSR drops edges
+ * into dangling targets, graph.py:355-360).  `row_len` is the pushed row
+ * length (live out-degree for ifp2, out-degree otherwise).  Per-round
+ * digests are order-free and equal the sequential form's; trace float sums
+ * are combined per thread (not numpy's pairwise order).
+ */
+typedef struct {
+    int variant, tid, nthreads;
+    int64_t n;
+    const int64_t *in_offsets, *in_sources, *degree, *dt_count, *row_len;
+    double c, xi, reserve_frac;
+    double *reserved, *h, *share;
+    uint8_t *active;
+    pthread_barrier_t *bar;
+    volatile int *stop;
+    /* per-round partials (phase A) */
+    double l1, above, nd_above;
+    int64_t conv, work, nact, pops, pdang;
+    uint64_t digest;
+} pull_worker;
+
+static void *pull_worker_main(void *arg)
+{
+    pull_worker *W = (pull_worker *)arg;
+    const int64_t n = W->n;
+    const int64_t lo = n * W->tid / W->nthreads, hi = n * (W->tid + 1) / W->nthreads;
+    for (;;) {
+        /* phase A: statistics of the state, activity, shares, reservation */
+        double l1 = 0.0, above_m = 0.0, nd_above = 0.0;
+        int64_t conv = 0, work = 0, nact = 0, pops = 0, pdang = 0;
+        uint64_t dig = 0;
+        for (int64_t v = lo; v < hi; ++v) {
+            const double hv = W->h[v];
+            const int dang = W->degree[v] == 0;
+            const int above = hv > W->xi;
+            const int scan = W->variant == 2 ? 1 : !dang;
+            uint64_t a, b;
+            memcpy(&a, &W->reserved[v], 8);
+            memcpy(&b, &W->h[v], 8);
+            dig += (a ^ (b * 0xBF58476D1CE4E5B9ull)) * (((uint64_t)v * 0x9E3779B97F4A7C15ull) | 1ull);
+            l1 += hv;
+            if (above) { above_m += hv; if (!dang) nd_above += hv; } else ++conv;
+            W->active[v] = (uint8_t)(above && scan);
+            W->share[v] = 0.0;
+            if (W->active[v]) {
+                work += W->degree[v] + 1;
+                ++nact;
+            }
+        }
+        W->l1 = l1; W->above = above_m; W->nd_above = nd_above;
+        W->conv = conv; W->work = work; W->nact = nact; W->digest = dig;
+        pthread_barrier_wait(W->bar);      /* main: row + termination */
+        pthread_barrier_wait(W->bar);
+        if (*W->stop) break;
+        for (int64_t v = lo; v < hi; ++v) {
+            if (!W->active[v]) continue;
+            const double hv = W->h[v];
+            W->reserved[v] += W->reserve_frac * hv;                            /* engines.py:439 */
+            if (W->row_len[v] > 0) W->share[v] = W->c * hv / (double)W->degree[v];   /* engines.py:444 */
+            pops += W->row_len[v];
+            pdang += W->dt_count ? W->dt_count[v] : 0;
+        }
+        W->pops = pops; W->pdang = pdang;
+        pthread_barrier_wait(W->bar);      /* every share written */
+        /* phase B: pull (ascending source = bincount order) */
+        for (int64_t v = lo; v < hi; ++v) {
+            double acc = 0.0;
+            if (W->variant != 1 || W->degree[v] > 0)
+                for (int64_t e = W->in_offsets[v]; e < W->in_offsets[v + 1]; ++e) acc += W->share[W->in_sources[e]];
+            W->h[v] = (W->active[v] ? 0.0 : W->h[v]) + acc;                    /* engines.py:448 */
+        }
+        pthread_barrier_wait(W->bar);      /* state t+1 complete */
+    }
+    return NULL;
+}
+
+int64_t orc_sync_rounds_pull(int variant, int64_t n, const int64_t *in_offsets, const int64_t *in_sources,
+                             const int64_t *degree, const int64_t *row_len, const int64_t *dt_count,
+                             double c, double xi, int64_t max_iterations, int threads,
+                             double *reserved, double *h, orc_row *rows, int64_t trace_cap, int64_t *n_rows)
+{
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    pull_worker *W = (pull_worker *)calloc((size_t)threads, sizeof(pull_worker));
+    pthread_t *th = (pthread_t *)calloc((size_t)threads, sizeof(pthread_t));
+    double *share = (double *)malloc(sizeof(double) * (size_t)(n ? n : 1));
+    uint8_t *active = (uint8_t *)malloc((size_t)(n ? n : 1));
+    pthread_barrier_t bar;
+    pthread_barrier_init(&bar, NULL, (unsigned)threads + 1);
+    volatile int stop = 0;
+    for (int64_t v = 0; v < n; ++v) { reserved[v] = 0.0; h[v] = 1.0; }
+    for (int k = 0; k < threads; ++k) {
+        W[k] = (pull_worker){variant, k, threads, n, in_offsets, in_sources, degree, dt_count, row_len,
+                             c, xi, variant == 2 ? 1.0 - c : 1.0, reserved, h, share, active, &bar, &stop};
+        pthread_create(&th[k], NULL, pull_worker_main, &W[k]);
+    }
+    int64_t push_ops = 0, push_dang = 0, iterations = 0, r = 0;
+    int settled = 0;
+    for (int64_t t = 0;; ++t) {
+        pthread_barrier_wait(&bar);        /* phase A done */
+        double l1 = 0.0, above = 0.0, nd_above = 0.0;
+        int64_t conv = 0, work = 0, nact = 0;
+        uint64_t dig = 0;
+        for (int k = 0; k < threads; ++k) {
+            l1 += W[k].l1; above += W[k].above; nd_above += W[k].nd_above;
+            conv += W[k].conv; work += W[k].work; nact += W[k].nact; dig += W[k].digest;
+        }
+        int done = 0;
+        if (r >= trace_cap) { r = -1; done = 1; }
+        else {
+            rows[r].h_l1 = l1;
+            rows[r].converged = conv;
+            rows[r].alpha = above > 0.0 ? nd_above / above : 1.0;
+            rows[r].work = work;
+            rows[r].push_ops = push_ops;
+            rows[r].push_ops_dangling = push_dang;
+            rows[r].active_mass = above;
+            rows[r].carry_mass = l1 - above;
+            rows[r].digest = dig;
+            ++r;
+            if (nact == 0) { settled = 1; done = 1; }
+            else if (t >= max_iterations) done = 1;
+        }
+        stop = done;
+        pthread_barrier_wait(&bar);
+        if (done) break;
+        pthread_barrier_wait(&bar);        /* reservation + shares */
+        for (int k = 0; k < threads; ++k) { push_ops += W[k].pops; push_dang += W[k].pdang; }
+        pthread_barrier_wait(&bar);        /* pull done */
+        iterations = t + 1;
+    }
+    for (int k = 0; k < threads; ++k) pthread_join(th[k], NULL);
+    pthread_barrier_destroy(&bar);
+    free(W); free(th); free(share); free(active);
+    *n_rows = r < 0 ? trace_cap : r;
+    if (r < 0) return -2;
+    return settled ? iterations : -1;
+}
+
 /* _settle_dangling (engines.py:269-289), sequential ascending-source sum */
 int64_t orc_settle(int64_t n_d, const int64_t *dangling_ids, const int64_t *source_offsets,
                    const int64_t *source_ids, const int64_t *out_degree, double c,

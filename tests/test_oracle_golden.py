@@ -35,10 +35,10 @@ def oracle_ints(g):
     }, cls
 
 
-def check_sync(gold, prefix, g):
+def check_sync(gold, prefix, g, threads=0):
     for variant in ("ifp1", "ifp2", "fp-full"):
         key = f"{prefix}sync_{variant.replace('-', '_')}_"
-        r = oracle.sync_simulate(g, variant, threshold=XI)
+        r = oracle.sync_simulate(g, variant, threshold=XI, threads=threads)
         rows = r.rows
         for col in ("converged", "work", "push_ops", "push_ops_dangling"):
             assert np.array_equal(rows[col], gold[key + col]), (key, col)
@@ -66,10 +66,13 @@ def test_corpus_integer_preprocessing_bit_exact(golden_corpus):
         assert cls.dangling_edge_count == int(golden_corpus[f"g{i}_m_d"])
 
 
-def test_corpus_sync_rounds_bit_exact(golden_corpus):
+@pytest.mark.parametrize("threads", [0, 3])
+def test_corpus_sync_rounds_bit_exact(golden_corpus, threads):
+    """threads=0: the sequential scatter restatement; threads=3: the threaded
+    CSC pull form used at full size (C3-C5) -- same state, bit for bit."""
     for i in range(int(golden_corpus["count"])):
         n, src, dst = corpus_graph(golden_corpus, i)
-        check_sync(golden_corpus, f"g{i}_", oracle.from_edges(n, src, dst))
+        check_sync(golden_corpus, f"g{i}_", oracle.from_edges(n, src, dst), threads=threads)
 
 
 def test_corpus_async_port_and_power(golden_corpus):
@@ -103,6 +106,7 @@ def test_c1_oracle_matches_reference(golden_c1):
     for k in INT_KEYS:
         assert _sha(ints[k]) == str(golden_c1[f"{k}_sha256"]), k
     check_sync(golden_c1, "", g)
+    check_sync(golden_c1, "", g, threads=4)
     r1 = oracle.async_run(g, "ifp1", threshold=XI, workers=4)
     assert np.abs(r1.values - golden_c1["ifp1_values"]).sum() <= 1e-9
     pw = oracle.power_method(g, iterations=210)
@@ -116,6 +120,7 @@ def test_synth42_oracle_matches_reference(golden_synth42):
     for k in INT_KEYS:
         assert _sha(ints[k]) == str(gold[f"{k}_sha256"]), k
     check_sync(gold, "", g)
+    check_sync(gold, "", g, threads=4)
 
 
 @pytest.mark.skipif(not __import__("oracle.refdriver").refdriver.available(),
