@@ -1,4 +1,4 @@
-"""Benchmark: IFP2 (default) push rounds on BASELINE config C2 on the B200.
+"""Benchmark: IFP2 (default) push rounds on BASELINE config C5 on the B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config c2] [--algo ifp2|ifp1] [--mode auto|pull|push]
@@ -13,6 +13,12 @@ line (rank 0).
 --impl reference times the reference's own compiled CPU push kernel
 (oracle/_ref, /root/reference/pkg/src/pushrank/_kernels.pyx) driven like
 ifp2_run / ifp1_run with all host threads, on the same graph and metric.
+At C5 (1.06 B edges) one CPU solve takes many minutes, so every reference
+step is a bounded sample: the asynchronous push phase run for a fixed wall
+budget from the initial state, GTEPS = pushes / elapsed (the line says so).
+The C5 graph for the CPU legs is built on the GPU and exported as the
+reference's int64 CSR/CSC (that build is bit-exact
+against the oracle: profiles/r02_parity_c5.json).
 """
 
 from __future__ import annotations
@@ -41,10 +47,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c5")
     ap.add_argument("--algo", default="ifp2", choices=["ifp1", "ifp2"])
     ap.add_argument("--mode", default="auto", choices=["auto", "pull", "push"])
     ap.add_argument("--cpu-sample-steps", type=int, default=3)
+    ap.add_argument("--cpu-budget", type=float, default=0.0,
+                    help="seconds per bounded CPU sample (0: full solves below C5, 6 s at C5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--push-switch", type=float, default=0.0,
@@ -117,54 +125,157 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def cpu_reference_run(g_host, algo, steps, threads):
-    """Time the reference's compiled push kernel (oracle/_ref) or, if absent,
-    the oracle's pthread port; returns (gteps, wall list, push_ops, kind)."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_graph(g):
+    """The reference's int64 CSR/CSC of a device graph, in page-locked host
+    memory (the e2e leg uploads from it; the CPU legs read it)."""
+    from types import SimpleNamespace
+    from paper_2302_03245_b200 import _lib
+    n, m = int(g.n), int(g.m)
+    out = {"out_offsets": _lib.pinned_empty(n + 1, np.int64), "out_targets": _lib.pinned_empty(max(m, 1), np.int64),
+           "in_offsets": _lib.pinned_empty(n + 1, np.int64), "in_sources": _lib.pinned_empty(max(m, 1), np.int64)}
+    dev = g.dev
+    dev.need_out_targets()
+    _lib.check(_lib.load().pr_graph_export(dev.handle, *[_lib.ptr(out[k]) for k in
+                                                         ("out_offsets", "out_targets", "in_offsets", "in_sources")]),
+               "export")
+    out["out_targets"] = out["out_targets"][:m]
+    out["in_sources"] = out["in_sources"][:m]
+    return SimpleNamespace(n=n, m=m, out_degree=np.diff(out["out_offsets"]), in_degree=np.diff(out["in_offsets"]),
+                           **out)
+
+
+def _ref_solve(g_host, algo, threads, pg, dt, budget):
+    """One run of the reference's compiled worker loop (oracle/_ref) or, if
+    it is missing, the oracle's pthread port; budget=None: a full solve."""
     import oracle
     from oracle import refdriver
-    pg = oracle.preprocess_ifp2(g_host, np.flatnonzero(g_host.out_degree == 0)) if algo == "ifp2" else None
-    walls, ops = [], 0
     if refdriver.available():
-        kind = "reference"
-        for _ in range(steps):
-            r = refdriver.run(g_host, algo, DAMPING, XI, workers=threads, pg=pg)
-            walls.append(r.wall_s)
-            ops = r.push_ops
-    else:
-        kind = "port"
-        for _ in range(steps):
-            t0 = time.perf_counter()
-            r = oracle.async_run(g_host, algo, DAMPING, XI, workers=threads, pg=pg)
-            walls.append(time.perf_counter() - t0)
-            ops = r.push_ops
-    med = statistics.median(walls)
-    return ops / med / 1e9, walls, ops, kind
+        r = refdriver.run(g_host, algo, DAMPING, XI, workers=threads, pg=pg, budget_s=budget, dt=dt)
+        return r.push_ops, r.wall_s, r.complete, "reference"
+    t0 = time.perf_counter()
+    r = oracle.async_run(g_host, algo, DAMPING, XI, workers=threads, pg=pg)
+    return r.push_ops, time.perf_counter() - t0, True, "port"
+
+
+def cpu_plan(g_host, config, budget, reps=3):
+    """BASELINE.md section 3's CPU baseline on this host: the reference's
+    ifp1/ifp2 push phase at workers = os.cpu_count() and 1, power iteration
+    as spi (1 worker) and mpi (cpu_count workers), classify + preprocess_ifp2
+    timed apart (bench.py:192-206's Table-2 style), median of ``reps`` as in
+    _median_timed (bench.py:151-159).  With ``budget`` (C5) every engine run
+    is a bounded sample (GTEPS over the first ``budget`` seconds of the
+    solve) and the power method runs a few iterations (per-iteration time x
+    210 is reported); the engines are the reference's compiled kernel
+    (oracle/_ref), classify / preprocess / power are the oracle's C port."""
+    import oracle
+    cores = os.cpu_count() or 1
+    plan = {"host": cpu_model(), "cpu_count": cores, "bounded_s": budget}
+    t0 = time.perf_counter()
+    cls = oracle.classify(g_host)
+    t1 = time.perf_counter()
+    pg = oracle.preprocess_ifp2(g_host, cls.dangling)
+    t2 = time.perf_counter()
+    dt = oracle.dangling_target_counts(g_host, cls.dangling)
+    plan["classify_s"] = t1 - t0
+    plan["preprocess_ifp2_s"] = t2 - t1
+    plan["preprocess_kind"] = "port (oracle.c)"
+    head = None
+    for algo in ("ifp2", "ifp1"):
+        for k in (cores, 1):
+            runs = []
+            for _ in range(1 if (budget or k == 1) else reps):
+                runs.append(_ref_solve(g_host, algo, k, pg if algo == "ifp2" else None,
+                                       dt if algo == "ifp1" else None,
+                                       (budget if k > 1 else budget / 2) if budget else None))
+            walls = [r[1] for r in runs]
+            med = statistics.median(walls)
+            ops = runs[-1][0]
+            key = f"{algo}_k{k}"
+            plan[key] = {"gteps": ops / med / 1e9, "wall_s": med, "push_ops": int(ops),
+                         "complete_solve": bool(runs[-1][2]), "kind": runs[-1][3], "workers": k,
+                         "samples": len(runs)}
+            if head is None:
+                head = plan[key]
+    iters = 2 if budget else 210
+    for name, k in (("spi", 1), ("mpi", cores)):
+        t0 = time.perf_counter()
+        pw = oracle.power_method(g_host, DAMPING, iterations=(1 if (budget and k == 1) else iters), workers=k)
+        dt_s = time.perf_counter() - t0
+        per_it = dt_s / max(pw.iterations, 1)
+        plan[name] = {"iterations_run": int(pw.iterations), "s_per_iteration": per_it,
+                      "s_for_210": per_it * 210, "workers": k, "kind": "port (oracle.c orc_power)"}
+    return head, plan
 
 
 def run_reference(args):
+    """--impl reference: the reference's compiled push kernel (oracle/_ref)
+    on this host's cores, on the same graph, metric and config as our arm.
+    Below C5 every step is a full solve; at C5 a bounded sample (see the
+    module docstring)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     import oracle
-    n, src, dst = make_host_graph(args.config)
-    g = oracle.from_edges(n, src, dst)
-    threads = os.cpu_count() or 1
     import oracle.refdriver as rd
-    pg = oracle.preprocess_ifp2(g, np.flatnonzero(g.out_degree == 0)) if args.algo == "ifp2" else None
+    threads = os.cpu_count() or 1
+    build_note = "oracle.from_edges (C restatement of graph.py:133-177) on the host"
+    t0 = time.perf_counter()
+    if args.config == "c5":
+        os.environ.setdefault("PUSHRANK_DEVICE", "0")
+        import paper_2302_03245_b200 as P
+        dev = P.graph.DeviceGraph.rmat(26, 16, seed=0)
+        g = host_graph(P.graph.Graph(dev, raw_edge_count=16 << 26, name="c5"))
+        del dev
+        build_note = ("built on the GPU (pr_graph_rmat + from_edges kernels) and exported as the reference's "
+                      "int64 CSR/CSC, per BASELINE.md section 3; bit-exact vs the oracle: profiles/r02_parity_c5.json")
+    else:
+        n, src, dst = make_host_graph(args.config)
+        g = oracle.from_edges(n, src, dst)
+    build_s = time.perf_counter() - t0
+    dang = np.flatnonzero(g.out_degree == 0)
+    pg = oracle.preprocess_ifp2(g, dang) if args.algo == "ifp2" else None
+    dt = oracle.dangling_target_counts(g, dang) if args.algo == "ifp1" else None
+    bounded = args.config == "c5"
+    budget = None
+    if bounded:
+        # the whole --steps K --warmup W run within a few minutes
+        budget = args.cpu_budget or max(3.0, min(12.0, 120.0 / max(args.steps, 1)))
     for _ in range(args.warmup):
-        (rd.run if rd.available() else oracle.async_run)(g, args.algo, DAMPING, XI, workers=threads, pg=pg)
-    gteps, walls, ops, kind = cpu_reference_run(g, args.algo, args.steps, threads)
+        _ref_solve(g, args.algo, threads, pg, dt, 1.0 if bounded else None)
+    walls, ops_list, kind, complete = [], [], "reference", True
+    for _ in range(args.steps):
+        ops, wall, comp, kind = _ref_solve(g, args.algo, threads, pg, dt, budget)
+        walls.append(wall)
+        ops_list.append(ops)
+        complete = complete and comp
     total = sum(walls)
-    value = ops * len(walls) / total / 1e9
+    value = sum(ops_list) / total / 1e9
+    sample = (f"{args.steps} bounded samples of the {args.algo} push phase on {args.config}: each runs the reference "
+              f"kernel with {threads} workers for {budget:.1f} s from the initial state (xi={XI}); GTEPS = pushes / "
+              f"elapsed" if bounded else
+              f"{args.steps} full {args.algo} solves of {args.config} (xi={XI}), mean")
     line = {"impl": "reference", "metric": "GTEPS", "value": value, "unit": "GTEPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(walls),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": config_desc(args, g.n, g.m),
             "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": threads, "kind": kind,
-                             "sample": f"{args.steps} full {args.algo} solves of {args.config} "
-                                       f"(xi={XI}), median-free mean"},
+                             "sample": sample, "model": cpu_model()},
             "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "push_ops_per_step": int(ops), "time_to_l1_ms": 1e3 * total / len(walls)}
+            "push_ops_per_step": int(statistics.median(ops_list)), "complete_solves": complete,
+            "time_to_l1_ms": (1e3 * total / len(walls)) if complete else None,
+            "graph_build": build_note, "graph_build_s": build_s,
+            "driver": "oracle/refdriver.py: K Python threads run the compiled worker_loop with the GIL released "
+                      "while the caller polls probe (engines.py:185-216); the final _sample is skipped"}
     print(json.dumps(line), flush=True)
 
 
@@ -283,21 +394,32 @@ def run_ours(args):
             "gpu_launches": int(launches), "clocks": clocks.summary()}
     if args.algo == "ifp2":
         line["l1_crossing"] = l1_crossing(args, dev, r0)
-    if not args.no_e2e and args.config != "c5":
-        line["e2e"] = e2e_measure(args, g, dev)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config != "c5":
+    host = None
+    if not args.no_e2e or (rank == 0 and world == 1 and not args.no_cpu_baseline):
+        t0 = time.perf_counter()
+        host = host_graph(g)
+        line["host_export_s"] = time.perf_counter() - t0
+    if not args.no_e2e:
+        line["e2e"] = e2e_measure(args, host)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            import oracle
-            host = oracle.graph_arrays(g)
-            gteps, walls, cops, kind = cpu_reference_run(host, args.algo, args.cpu_sample_steps,
-                                                         os.cpu_count() or 1)
-            line["cpu_baseline"] = {"value": gteps, "unit": "GTEPS", "cores": os.cpu_count() or 1,
-                                    "kind": kind, "sample": f"{len(walls)} full {args.algo} solves of "
-                                    f"{args.config} (xi={XI}), median wall {statistics.median(walls):.3f}s, "
-                                    f"{cops} pushes/solve"}
+            budget = args.cpu_budget or (6.0 if args.config == "c5" else None)
+            head, plan = cpu_plan(host, args.config, budget)
+            line["cpu_baseline"] = {
+                "value": head["gteps"], "unit": "GTEPS", "cores": head["workers"], "kind": head["kind"],
+                "model": plan["host"],
+                "sample": (f"{args.algo} push phase, reference kernel, {head['workers']} workers: "
+                           + (f"bounded sample, first {budget:.0f} s of the solve from the initial state"
+                              if budget else f"median of {head['samples']} full solves")),
+                "plan": plan}
+            # time-based context beside GTEPS (the engines push different edge counts)
+            if head["complete_solve"]:
+                line["vs_cpu_time_to_solution"] = head["wall_s"] * 1e3 / line["time_to_l1_ms"]
+            line["pushes_per_solve"] = {"ours": int(r0.push_ops), "cpu_reference": head["push_ops"]
+                                        if head["complete_solve"] else None}
         except Exception as e:  # baseline failure must not hide the GPU number
             line["cpu_baseline"] = {"value": None, "unit": "GTEPS", "cores": os.cpu_count(), "kind": "port",
-                                    "sample": f"failed: {e}"}
+                                    "sample": f"failed: {e!r}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -393,9 +515,11 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
                              "kernel": "partitioned round loop per GPU (k_part_pull + exchange + statistics), "
                                        "algorithmic bytes 12*E_pushed + 40*V_drained + 8*n_scan per round",
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
-                # per round: one k_part_pull per section (the last also reduces the statistics);
+                # per queued round (rounds queued past termination launch too): one
+                # k_part_pull per section (the last also reduces the statistics);
                 # init (2) and settle/total (4)
-                "gpu_launches": int((step.launches_per_round() * info["rounds"] + 6) * args.steps),
+                "gpu_launches": int((step.launches_per_round() * info.get("queued_rounds", info["rounds"]) + 6)
+                                    * args.steps),
                 "clocks": clocks.summary(),
                 "exchange": ("fused: round kernel stores shares into every rank's replica (peer memory)"
                              if fused else "NCCL all-gather of shares per round"),
@@ -428,26 +552,24 @@ def l1_crossing(args, dev, res_timed):
             "ms": float(rows["wall_ms"][r] + (res_timed.push_ms - res_timed.round_ms))}
 
 
-def e2e_measure(args, g, dev_resident):
+def e2e_measure(args, host):
     """Same metric through the public API from HOST buffers: each step uploads
-    the reference-layout graph (pinned int64 arrays; the upload copies what the
-    fast engine needs -- in-adjacency + out_offsets -- and defers out_targets),
-    builds the run layout and IFP2 split on the device, solves, and copies the
-    vector back.  h2d_bytes_per_step counts the bytes actually copied."""
+    the reference-layout graph from page-locked int64 arrays (the upload
+    copies what the fast engine needs -- in-adjacency + out_offsets -- and
+    defers out_targets), builds the run layout and IFP2 split on the device,
+    solves, and copies the vector back.  h2d_bytes_per_step counts the bytes
+    actually copied."""
     from paper_2302_03245_b200.graph import device_graph
     import torch
     import paper_2302_03245_b200 as P
     from types import SimpleNamespace
-    arrays = {k: torch.from_numpy(np.ascontiguousarray(getattr(g, k))).pin_memory().numpy()
-              for k in ("out_offsets", "out_targets", "in_offsets", "in_sources")}
-    host = SimpleNamespace(n=g.n, m=g.m, **arrays)
-    h2d = sum(a.nbytes for a in arrays.values())
+    base = {k: getattr(host, k) for k in ("n", "m", "out_offsets", "out_targets", "in_offsets", "in_sources")}
     cfg = P.SolverConfig(threshold=XI)
-    times, ops = [], 0
+    times, ops, h2d = [], 0, 0
     for i in range(args.warmup + args.steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        obj = SimpleNamespace(**vars(host))
+        obj = SimpleNamespace(**base)
         if args.algo == "ifp2":
             pg = P.preprocess_ifp2(obj, None)
             vec, tr = P.ifp2_run(pg, cfg, mode=args.mode, sample_every=float("inf"))
@@ -464,11 +586,12 @@ def e2e_measure(args, g, dev_resident):
         # graph
         if args.algo == "ifp2":
             del pg
-        del obj
+        del obj, vec
     mean = sum(times) / len(times)
     return {"value": ops / mean / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(8 * g.n), "ms_per_step": 1e3 * mean,
-            "path": f"{args.algo}_run() on a host-array graph: upload + device preprocess + solve + D2H"}
+            "d2h_bytes_per_step": int(8 * host.n), "ms_per_step": 1e3 * mean,
+            "path": f"{args.algo}_run() on a host-array graph (page-locked int64 CSR/CSC): upload + device "
+                    f"preprocess + solve + D2H of the vector"}
 
 
 def main():

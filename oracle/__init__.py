@@ -72,10 +72,13 @@ def lib():
         L.orc_sync_rounds_pull.argtypes = [ctypes.c_int, _I, _i64p, _i64p, _i64p, _i64p, ctypes.c_void_p,
                                            _D, _D, _I, ctypes.c_int, _f64p, _f64p, _rowp, _I,
                                            ctypes.POINTER(_I)]
+        L.orc_rmat.restype = _I
+        L.orc_rmat.argtypes = [ctypes.c_int, _I, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                               ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
         L.orc_settle.restype = _I
         L.orc_settle.argtypes = [_I, _i64p, _i64p, _i64p, _i64p, _D, _f64p, _f64p]
         L.orc_power.restype = _I
-        L.orc_power.argtypes = [_I, _i64p, _i64p, _i64p, _D, _f64p, _I, _D, _f64p, _f64p]
+        L.orc_power.argtypes = [_I, _i64p, _i64p, _i64p, _D, _f64p, _I, _D, _f64p, _f64p, ctypes.c_int]
         L.orc_async_phase.restype = ctypes.c_int
         L.orc_async_phase.argtypes = [_I, _f64p, _f64p, _i64p, _i64p, _i64p, _i64p, _i64p,
                                       ctypes.c_int, _i64p, _I, ctypes.c_void_p, _D, _D,
@@ -166,6 +169,23 @@ def preprocess_ifp2(g, dangling_ids) -> SimpleNamespace:
         live_offsets=live_off, live_targets=live_tgt[:live_m].copy(), live_degree=live_deg,
         dangling_ids=d_ids[:n_d].copy(), source_offsets=s_off,
         source_ids=s_ids[:int(s_off[-1])].copy(), dangling_edge_count=int(s_off[-1]))
+
+
+def rmat_graph_edges(scale: int, edge_factor: int, seed: int = 0, threads: int = 0,
+                     a: float = 0.57, b: float = 0.19, c: float = 0.19):
+    """``(n, src, dst)``: the R-MAT samples of the BASELINE configs with
+    self-loops dropped in sample order -- the same edge list as
+    ``synthetic.rmat_graph`` (numpy) and the device generator
+    (``pr_graph_rmat``), computed by threaded C (orc_rmat) so that C5's
+    1.07 B samples reach the oracle without the device."""
+    threads = threads or (os.cpu_count() or 1)
+    S = float(1 << 32)
+    ta, tb, tc = int(a * S), int((a + b) * S), int((a + b + c) * S)
+    kept = lib().orc_rmat(scale, edge_factor, ta, tb, tc, seed, threads, None, None)
+    src = np.empty(kept, np.int64)
+    dst = np.empty(kept, np.int64)
+    lib().orc_rmat(scale, edge_factor, ta, tb, tc, seed, threads, src.ctypes.data, dst.ctypes.data)
+    return 1 << scale, src, dst
 
 
 # ---------------------------------------------------------------- engines
@@ -267,8 +287,10 @@ def settle(pg, out_degree, damping: float, reserved: np.ndarray, h: np.ndarray) 
 
 
 def power_method(g, damping: float = 0.85, iterations: int = 210, tolerance: float = 0.0,
-                 personalization=None) -> SimpleNamespace:
-    """Restates solvers.py:186-243 (pull SpMV + rank-one dangling restart)."""
+                 personalization=None, workers: int = 1) -> SimpleNamespace:
+    """Restates solvers.py:186-243 (pull SpMV + rank-one dangling restart);
+    ``workers`` threads split the multiply by destination range (identical
+    result, solvers.py:124-183)."""
     g = graph_arrays(g)
     p = (np.full(g.n, 1.0 / g.n) if personalization is None
          else np.ascontiguousarray(personalization, np.float64))
@@ -276,7 +298,7 @@ def power_method(g, damping: float = 0.85, iterations: int = 210, tolerance: flo
     deltas = np.zeros(max(iterations, 1), np.float64)
     src = g.in_sources if g.in_sources.size else np.zeros(1, np.int64)
     k = lib().orc_power(g.n, g.in_offsets, np.ascontiguousarray(src), g.out_degree, damping, p,
-                        iterations, tolerance, pi, deltas)
+                        iterations, tolerance, pi, deltas, int(workers))
     if iterations == 0:
         pi = p.copy()
     return SimpleNamespace(values=pi, deltas=deltas[:k].copy(), iterations=int(k))

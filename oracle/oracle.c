@@ -432,15 +432,107 @@ int64_t orc_settle(int64_t n_d, const int64_t *dangling_ids, const int64_t *sour
 }
 
 /* ------------------------------------------------------------------ */
+/* R-MAT samples of the BASELINE configs (paper_2302_03245_b200/       */
+/* synthetic.py rmat_edges + _drop_self_loops), threaded, for C5 on    */
+/* the host.  Not a reference function: the reference has no R-MAT    */
+/* generator; this restates the repo's seeded definition so the C5     */
+/* edge list reaches the oracle independently of the device generator. */
+/* ------------------------------------------------------------------ */
+static inline uint64_t orc_mix64(uint64_t x)
+{
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+typedef struct {
+    int scale, pass;
+    uint64_t key0, ta, tb, tc;
+    int64_t lo, hi, kept, out;
+    int64_t *src, *dst;
+} rmat_job;
+
+static void *rmat_main(void *arg)
+{
+    rmat_job *J = (rmat_job *)arg;
+    const uint64_t G = 0x9E3779B97F4A7C15ull;
+    int64_t k = 0;
+    for (int64_t i = J->lo; i < J->hi; ++i) {
+        uint64_t base = J->key0 + (uint64_t)i * 64ull * G, s = 0, d = 0;
+        for (int l = 0; l < J->scale; ++l) {
+            uint64_t u = orc_mix64(base + (uint64_t)l * G) >> 32;
+            s = (s << 1) | (uint64_t)(u >= J->tb);
+            d = (d << 1) | (uint64_t)((u >= J->ta && u < J->tb) || u >= J->tc);
+        }
+        if (s == d) continue;                      /* self-loop dropped, order kept */
+        if (J->pass) { J->src[J->out + k] = (int64_t)s; J->dst[J->out + k] = (int64_t)d; }
+        ++k;
+    }
+    J->kept = k;
+    return NULL;
+}
+
+/* ta/tb/tc are the cumulative thresholds (synthetic.rmat_thresholds).
+ * src/dst NULL: count only.  Returns the number of non-loop samples. */
+int64_t orc_rmat(int scale, int64_t edge_factor, uint64_t ta, uint64_t tb, uint64_t tc, uint64_t seed,
+                 int threads, int64_t *src, int64_t *dst)
+{
+    if (threads < 1) threads = 1;
+    const int64_t total = edge_factor << scale;
+    rmat_job *J = (rmat_job *)calloc((size_t)threads, sizeof(rmat_job));
+    pthread_t *th = (pthread_t *)calloc((size_t)threads, sizeof(pthread_t));
+    const uint64_t key0 = orc_mix64(seed);
+    for (int pass = 0; pass < (src ? 2 : 1); ++pass) {
+        int64_t out = 0;
+        for (int k = 0; k < threads; ++k) {
+            J[k].scale = scale; J[k].pass = pass; J[k].key0 = key0;
+            J[k].ta = ta; J[k].tb = tb; J[k].tc = tc;
+            J[k].lo = total * k / threads; J[k].hi = total * (k + 1) / threads;
+            J[k].src = src; J[k].dst = dst;
+            if (pass) { J[k].out = out; out += J[k].kept; }
+            pthread_create(&th[k], NULL, rmat_main, &J[k]);
+        }
+        for (int k = 0; k < threads; ++k) pthread_join(th[k], NULL);
+    }
+    int64_t kept = 0;
+    for (int k = 0; k < threads; ++k) kept += J[k].kept;
+    free(J); free(th);
+    return kept;
+}
+
+/* ------------------------------------------------------------------ */
 /* power_method (solvers.py:186-243) with _WalkMultiplier (124-183)    */
 /* ------------------------------------------------------------------ */
+typedef struct {
+    int64_t lo, hi;
+    const int64_t *in_offsets, *in_sources;
+    const double *z, *p;
+    double restart, *nxt;
+} power_job;
+
+static void *power_main(void *arg)
+{
+    power_job *J = (power_job *)arg;
+    for (int64_t v = J->lo; v < J->hi; ++v) {
+        double y = 0.0;
+        for (int64_t e = J->in_offsets[v]; e < J->in_offsets[v + 1]; ++e) y += J->z[J->in_sources[e]];
+        J->nxt[v] = y + J->restart * J->p[v];
+    }
+    return NULL;
+}
+
+/* threads > 1: the multiply split by destination range, as
+ * _WalkMultiplier(workers) does (solvers.py:124-183) -- identical result */
 int64_t orc_power(int64_t n, const int64_t *in_offsets, const int64_t *in_sources,
                   const int64_t *out_degree, double c, const double *p,
-                  int64_t iterations, double tolerance, double *pi, double *deltas)
+                  int64_t iterations, double tolerance, double *pi, double *deltas, int threads)
 {
+    if (threads < 1) threads = 1;
     double *inv = (double *)malloc(sizeof(double) * n);
     double *z = (double *)malloc(sizeof(double) * n);
     double *nxt = (double *)malloc(sizeof(double) * n);
+    power_job *J = (power_job *)calloc((size_t)threads, sizeof(power_job));
+    pthread_t *th = (pthread_t *)calloc((size_t)threads, sizeof(pthread_t));
     for (int64_t v = 0; v < n; ++v) {
         inv[v] = out_degree[v] > 0 ? 1.0 / (double)out_degree[v] : 0.0;
         pi[v] = p[v];
@@ -453,13 +545,15 @@ int64_t orc_power(int64_t n, const int64_t *in_offsets, const int64_t *in_source
             if (out_degree[v] == 0) dang += pi[v];
         }
         double restart = c * dang + (1.0 - c);                           /* solvers.py:219 */
-        double total = 0.0;
-        for (int64_t v = 0; v < n; ++v) {
-            double y = 0.0;
-            for (int64_t e = in_offsets[v]; e < in_offsets[v + 1]; ++e) y += z[in_sources[e]];
-            nxt[v] = y + restart * p[v];
-            total += nxt[v];
+        for (int t = 0; t < threads; ++t) {
+            J[t] = (power_job){n * t / threads, n * (t + 1) / threads, in_offsets, in_sources, z, p, restart, nxt};
+            if (threads > 1) pthread_create(&th[t], NULL, power_main, &J[t]);
+            else power_main(&J[t]);
         }
+        if (threads > 1)
+            for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+        double total = 0.0;
+        for (int64_t v = 0; v < n; ++v) total += nxt[v];
         double delta = 0.0;
         for (int64_t v = 0; v < n; ++v) {
             double x = nxt[v] / total;
@@ -469,7 +563,7 @@ int64_t orc_power(int64_t n, const int64_t *in_offsets, const int64_t *in_source
         deltas[k] = delta;
         if (tolerance > 0.0 && delta < tolerance) { ++k; break; }
     }
-    free(inv); free(z); free(nxt);
+    free(inv); free(z); free(nxt); free(J); free(th);
     return k;
 }
 

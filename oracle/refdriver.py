@@ -44,9 +44,17 @@ def kernels():
 
 
 def run(g, algorithm: str = "ifp1", damping: float = 0.85, threshold: float = 1e-10,
-        workers: int = 1, strategy: str = "degree-balanced", pg=None) -> SimpleNamespace:
+        workers: int = 1, strategy: str = "degree-balanced", pg=None, budget_s: float | None = None,
+        dt=None) -> SimpleNamespace:
     """ifp1_run / ifp2_run on the reference's compiled kernel; returns the
-    normalised vector, push counters and the push-phase wall time."""
+    normalised vector, push counters and the push-phase wall time.
+
+    ``budget_s`` bounds the sample (bench.py at C5, where one CPU solve
+    takes many minutes): the monitor raises the stop flag after that many
+    seconds, as the reference's own stop path does (engines.py:205-216), and
+    the result has ``complete=False``, the pushes done and the elapsed time
+    (no settle, no vector).  ``dt`` passes precomputed dangling target
+    counts (IFP1)."""
     K = kernels()
     g = graph_arrays(g)
     n = g.n
@@ -57,7 +65,8 @@ def run(g, algorithm: str = "ifp1", damping: float = 0.85, threshold: float = 1e
     reserved = np.zeros(n, np.float64)
     if algorithm == "ifp1":
         offsets, targets = g.out_offsets, g.out_targets
-        dt = dangling_target_counts(g, np.flatnonzero(dang))
+        if dt is None:
+            dt = dangling_target_counts(g, np.flatnonzero(dang))
     else:
         if pg is None:
             pg = preprocess_ifp2(g, np.flatnonzero(dang))
@@ -74,8 +83,12 @@ def run(g, algorithm: str = "ifp1", damping: float = 0.85, threshold: float = 1e
     for t in threads:
         t.start()
     pause = 0.0005 if universe.size > 100_000 else 0.0
+    complete = True
     try:
         while not K.probe(h, universe, threshold, wstate, len(threads), None):
+            if budget_s is not None and time.perf_counter() - start >= budget_s:
+                complete = False
+                break
             time.sleep(pause)
     finally:
         ctrl[0] = 1
@@ -83,6 +96,10 @@ def run(g, algorithm: str = "ifp1", damping: float = 0.85, threshold: float = 1e
             t.join()
     push_ops = int(wstate[2::8].sum())
     push_dang = int(wstate[3::8].sum())
+    if not complete:
+        wall = time.perf_counter() - start
+        return SimpleNamespace(values=None, push_ops=push_ops, push_ops_dangling=push_dang, wall_s=wall,
+                               mass_total=None, complete=False)
     if algorithm == "ifp2":
         settled = settle(pg, g.out_degree, damping, reserved, h)
         push_ops += settled
@@ -93,4 +110,4 @@ def run(g, algorithm: str = "ifp1", damping: float = 0.85, threshold: float = 1e
     wall = time.perf_counter() - start
     total = float(values.sum())
     return SimpleNamespace(values=values / total, push_ops=push_ops, push_ops_dangling=push_dang,
-                           wall_s=wall, mass_total=total)
+                           wall_s=wall, mass_total=total, complete=True)

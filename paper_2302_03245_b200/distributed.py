@@ -364,10 +364,12 @@ def run_partitioned_queued(step, comm, part: Partition, algorithm: str, damping:
         comm.allreduce_row(stats[0])
         nact = record(stats[0].cpu().numpy())
         t = 0
+        queued = 0   # rounds launched, including those queued past termination (no-ops)
         while nact > 0:
             if t >= max_rounds:
                 raise RuntimeError(f"sync simulation did not settle in {max_rounds} iterations")
             nb = run_batch(t)
+            queued += nb
             host = stats[:nb].cpu().numpy()
             for j in range(nb):
                 nact = record(host[j])
@@ -392,7 +394,8 @@ def run_partitioned_queued(step, comm, part: Partition, algorithm: str, damping:
         total = float(gt[0])
         values = step.values(total) if host_values else None
     return values, rows, {"rounds": t, "mass_total": total, "push_ops": push_ops,
-                          "push_ops_dangling": push_dang, "settled": settled, "drained": drained}
+                          "push_ops_dangling": push_dang, "settled": settled, "drained": drained,
+                          "queued_rounds": queued}
 
 
 def sweep_kind(t: int) -> int:

@@ -57,7 +57,7 @@ def test_corpus_preprocessing_bit_exact(golden_corpus):
             assert np.array_equal(getattr(pg, k), golden_corpus[f"g{i}_{k}"]), (i, k)
 
 
-@pytest.mark.parametrize("config", ["c1", "c2", "c4"])
+@pytest.mark.parametrize("config", ["c1", "c2", "c3", "c4"])
 def test_config_preprocessing_bit_exact(config, golden_c1):
     n, src, dst = synthetic.make(config, seed=0)
     g = P.from_edges(n, src, dst)
@@ -372,20 +372,33 @@ def test_gauss_seidel_sections_ifp1(sections, monkeypatch):
             assert np.array_equal(again.values, vec.values)
 
 
-def test_c3_full_size_parity():
-    """C3 (52 M edges): the fast IFP2 engine, which runs 2 Gauss-Seidel
-    sections per dense sweep at this size, against the round-synchronous
-    oracle -- L1 <= 1e-9, identical top-100, every dangling in-edge settled."""
-    n, src, dst = synthetic.make("c3", seed=0)
-    g = P.from_edges(n, src, dst)
-    ref = oracle.from_edges(n, src, dst)
-    cls = P.classify(g)
-    o = oracle.sync_simulate(ref, "ifp2", threshold=XI)
-    vec, tr = P.ifp2_run(P.preprocess_ifp2(g, cls), cfg())
-    assert np.abs(vec.values - o.values).sum() <= 1e-9
-    assert np.array_equal(top100(vec.values), top100(o.values))
-    assert tr.final.push_ops_dangling == cls.dangling_edge_count
-    assert tr.meta["rounds"] < o.iterations          # the sections cut rounds
+@pytest.mark.parametrize("config", ["c3", "c4"])
+def test_config_engines_parity(config):
+    """C3 (52 M edges, 2 Gauss-Seidel sections) and C4 (the DAG that
+    exercises IFP1 peeling and dangling convergence): integer preprocessing
+    bit-exact, then IFP1 and IFP2 in auto, pull and push modes against the
+    oracle's round-synchronous twin -- L1 <= 1e-9, identical top-100, mass 1,
+    push_ops_dangling == m_d (IFP2) -- via tests/full_size_parity.py."""
+    import full_size_parity as F
+    v = F.run(config, xi=1e-10)
+    bad = [c for c in v["checks"] if not c["ok"]]
+    assert not bad, bad
+
+
+def test_forced_c5_code_path_parity(monkeypatch):
+    """C5's code path at a size the oracle finishes in about a minute: R-MAT
+    scale 23 (134 M edges) with 4 Gauss-Seidel sections, source-sorted CSC
+    rows and the streamed (evict-first) k_pull forced as at C5.  Device vs
+    host edge generators, integer preprocessing bit-exact, IFP2 and IFP1
+    (auto + pull) against the oracle twin.  The full C5 run of the same
+    script is profiles/r02_parity_c5.json."""
+    import full_size_parity as F
+    monkeypatch.setenv("PUSHRANK_GS_SECTIONS", "4")
+    monkeypatch.setenv("PUSHRANK_SORT_ROWS", "1")
+    monkeypatch.setenv("PUSHRANK_PREFETCH", "0")
+    v = F.run("rmat", scale=23, modes=("auto", "pull"), xi=1e-10)
+    bad = [c for c in v["checks"] if not c["ok"]]
+    assert not bad, bad
 
 
 def test_c5_full_size_properties():

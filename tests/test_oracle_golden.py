@@ -134,3 +134,13 @@ def test_reference_kernel_driver_matches_golden(golden_c1):
         r = refdriver.run(g, algo, threshold=XI, workers=4)
         assert np.abs(r.values - golden_c1[f"{algo}_values"]).sum() <= 1e-9
     assert r.push_ops_dangling == int(golden_c1["ifp2_push_ops_dangling"])
+
+
+def test_oracle_rmat_matches_synthetic():
+    """orc_rmat (threaded C, used to bring C5's edge list to the oracle) is
+    the repo's seeded R-MAT definition, self-loops dropped in sample order."""
+    from paper_2302_03245_b200 import synthetic
+    for scale, ef, seed, threads in ((12, 16, 0, 1), (14, 5, 7, 3), (16, 8, 3, 8)):
+        n, s, d = synthetic.rmat_graph(scale, ef, seed=seed)
+        n2, s2, d2 = oracle.rmat_graph_edges(scale, ef, seed=seed, threads=threads)
+        assert n == n2 and np.array_equal(s, s2) and np.array_equal(d, d2)
