@@ -8,7 +8,9 @@
 //   * warp unit   -- rows with THREAD_DEG < d <= HUB_DEG; warp w takes rows
 //                    w, w+8, ...; lanes stride a row with 8 gathers in flight;
 //   * thread unit -- rows with d <= THREAD_DEG; thread t takes rows t, t+256,
-//                    ... (coalesced drains), 8 index loads then 8 gathers.
+//                    ... (coalesced drains), 8 index loads then 8 gathers;
+//                    the bin is stored SELL-32 (column-major 32-row slices)
+//                    so each warp index load is one 128-byte line.
 // Rows of a unit have near-equal degree (sorted), so warps carry uniform
 // work.  Blocks of a persistent grid claim units dynamically (an atomic per
 // unit, issued at the start of the previous one); a launch covers the unit
@@ -27,12 +29,63 @@ namespace pr {
 // ld.global.cs (evict-first) so that it does not push the share vector out
 // of L2; when everything fits (C1, C2) the CSC stays L2-resident across
 // rounds with plain loads.  Measured: C3 -5%, C5 -1%, C2 +4% if streamed.
+#ifndef PR_IDXP
+#define PR_IDXP 0
+#endif
 template <bool STREAM>
 __device__ __forceinline__ int ld_idx(const int32_t *p) {
-    if constexpr (STREAM) return __ldcs(p);
-    else return __ldg(p);
+    if constexpr (STREAM) {
+#if PR_IDXP == 1
+        int v;
+        asm("{ .reg .b64 pol; createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+            "  ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], pol; }"
+            : "=r"(v) : "l"(p));
+        return v;
+#else
+        return __ldcs(p);
+#endif
+    } else {
+        return __ldg(p);
+    }
 }
-__device__ __forceinline__ double ld_share(const double *p) { return __ldg(p); }
+// Share gathers (random 8-byte loads; A/B builds): 0 ld.global.nc; 1 without
+// L1 allocation; 2 ld.global.cg (L2 only); 3-5 split by source id (hot =
+// id < PR_HOT, the run layout's most-gathered sources): 3 hot L1::evict_last,
+// cold L1::no_allocate; 4 hot evict_last, cold plain; 5 hot plain, cold
+// no_allocate
+#ifndef PR_GATHER
+#define PR_GATHER 0
+#endif
+#ifndef PR_HOT
+#define PR_HOT 32768
+#endif
+#define PR_LDSPLIT(A, B)                                                                      \
+    asm("{ .reg .pred p; setp.ne.u32 p, %2, 0;\n"                                             \
+        "  @p ld.global.nc" A ".f64 %0, [%1];\n"                                               \
+        "  @!p ld.global.nc" B ".f64 %0, [%1]; }"                                               \
+        : "=d"(v) : "l"(p), "r"((unsigned)hot))
+__device__ __forceinline__ double ld_share(const double *p, int idx) {
+#if PR_GATHER == 1
+    double v;
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+#elif PR_GATHER == 2
+    return __ldcg(p);
+#elif PR_GATHER >= 3
+    const bool hot = (unsigned)idx < (unsigned)PR_HOT;
+    double v;
+#if PR_GATHER == 3
+    PR_LDSPLIT(".L1::evict_last", ".L1::no_allocate");
+#elif PR_GATHER == 4
+    PR_LDSPLIT(".L1::evict_last", "");
+#else
+    PR_LDSPLIT("", ".L1::no_allocate");
+#endif
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
 
 // Share sources of a dense round (rounds.cu, Gauss-Seidel sections):
 //   Jacobi      gs_lo = 0:              x[u]
@@ -54,18 +107,19 @@ __device__ __forceinline__ bool early(const Src &S, int idx) { return (unsigned)
 template <int SRC>
 __device__ __forceinline__ double ld_src(const Src S, int idx) {
     if constexpr (SRC == 0) {
-        return ld_share(S.x + idx);
+        return ld_share(S.x + idx, idx);
     } else if constexpr (SRC == 1) {
-        return ld_share((early(S, idx) ? S.x_new : S.x) + idx);
+        return ld_share((early(S, idx) ? S.x_new : S.x) + idx, idx);
     } else {
-        return ld_share(S.x + idx) + (early(S, idx) ? ld_share(S.x_new + idx) : 0.0);
+        return ld_share(S.x + idx, idx) + (early(S, idx) ? ld_share(S.x_new + idx, idx) : 0.0);
     }
 }
 
 struct BinView {
     const int32_t *ids;      // row -> vertex id
     const int64_t *doff;     // row offsets in csc
-    const int32_t *csc;      // compacted sources (padded)
+    const int32_t *csc;      // compacted sources (padded); thread rows in SELL-32 slices
+    const int64_t *sell_off; // csc offset of each 32-row slice of the thread bin (sched.cu sell_layout)
     int64_t count, n_hub, n_warp;
     const int64_t *chunk_base;   // first chunk unit of each hub row
     const int2 *units;           // (row_begin, row_end) or hub chunk (row, -(chunk+1))
@@ -90,6 +144,39 @@ __device__ __forceinline__ double row_sum_thread(const int32_t *__restrict__ csc
         for (int q = 0; q < 8; ++q) acc += t[q];
     }
     return acc;
+}
+
+// A thread row in its SELL-32 slice: the k-th source at p[32 k].  Same
+// summation order as row_sum_thread (ascending position, 8 at a time), so a
+// row's sum is bit-identical to the CSR form; the warp's loads of position k
+// are one 128-byte line.
+template <bool STREAM, int SRC>
+__device__ __forceinline__ double row_sum_sell(const int32_t *__restrict__ p, int deg, const Src x) {
+    double acc = 0.0;
+    for (int k = 0; k < deg; k += 8) {
+        int idx[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) idx[q] = k + q < deg ? ld_idx<STREAM>(&p[32 * (k + q)]) : -1;
+        double t[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t[q] = idx[q] >= 0 ? ld_src<SRC>(x, idx[q]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc += t[q];
+    }
+    return acc;
+}
+
+// Sum of thread row `row` (rows of a warp are one slice: base aligned to 32
+// rows past the bin start t0)
+template <bool STREAM, int SRC>
+__device__ __forceinline__ double thread_row_sum(const BinView &B, int64_t t0, int64_t row, const Src x) {
+#if PR_SELL
+    const int64_t i = row - t0;
+    const int deg = (int)(B.doff[row + 1] - B.doff[row]);
+    return row_sum_sell<STREAM, SRC>(B.csc + B.sell_off[i >> 5] + (i & 31), deg, x);
+#else
+    return row_sum_thread<STREAM, SRC>(B.csc, B.doff[row], B.doff[row + 1], x);
+#endif
 }
 
 // lanes stride [lo, hi) with 8 gathers in flight; warp-reduced (fixed tree)
@@ -268,16 +355,18 @@ __device__ __forceinline__ void bins_run(const BinView &B, const int64_t u_lo, c
                 }
             }
         } else {
-            // ---- thread rows: thread t takes rows t, t+256, ... (whole warps iterate together)
-            for (int64_t base = d.x; base < d.y; base += 256) {
+            // ---- thread rows: thread t takes rows t, t+256, ... from the
+            // 32-row slice boundary at or before the unit start (a warp walks
+            // whole SELL slices; rows outside the unit idle)
+            for (int64_t base = warp_rows + ((d.x - warp_rows) & ~(int64_t)31); base < d.y; base += 256) {
                 const int64_t row = base + tid;
-                const bool valid = row < d.y;
+                const bool valid = row >= d.x && row < d.y;
                 if constexpr (PREFETCH) {
                     const auto pre = rows.pre(valid, row);
-                    const double s = valid ? row_sum_thread<STREAM, SRC>(B.csc, B.doff[row], B.doff[row + 1], x) : 0.0;
+                    const double s = valid ? thread_row_sum<STREAM, SRC>(B, warp_rows, row, x) : 0.0;
                     rows.fin(valid, pre, s);
                 } else {
-                    const double s = valid ? row_sum_thread<STREAM, SRC>(B.csc, B.doff[row], B.doff[row + 1], x) : 0.0;
+                    const double s = valid ? thread_row_sum<STREAM, SRC>(B, warp_rows, row, x) : 0.0;
                     rows.fin(valid, rows.pre(valid, row), s);
                 }
             }
@@ -373,11 +462,11 @@ __device__ __forceinline__ void bins_run_plain(const BinView &B, const int64_t u
                 thread_row(valid, row, mine);
             }
         } else {
-            // ---- thread rows: thread t takes rows t, t+256, ... (whole warps iterate together)
-            for (int64_t base = d.x; base < d.y; base += 256) {
+            // ---- thread rows: whole SELL slices per warp (see bins_run)
+            for (int64_t base = warp_rows + ((d.x - warp_rows) & ~(int64_t)31); base < d.y; base += 256) {
                 const int64_t row = base + tid;
-                const bool valid = row < d.y;
-                const double s = valid ? row_sum_thread<STREAM, SRC>(B.csc, B.doff[row], B.doff[row + 1], x) : 0.0;
+                const bool valid = row >= d.x && row < d.y;
+                const double s = valid ? thread_row_sum<STREAM, SRC>(B, warp_rows, row, x) : 0.0;
                 thread_row(valid, row, s);
             }
         }

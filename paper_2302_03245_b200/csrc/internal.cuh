@@ -160,7 +160,10 @@ struct Graph {
         int64_t n_chunks = 0;     // CHUNK-edge units of the hub rows
         DevBuf ids;               // int32 [|D|] vertex id of each row (descending in-degree)
         DevBuf doff;              // int64 [|D|+1] compacted CSC offsets
-        DevBuf csc;               // int32 [edges + pad] compacted sources
+        DevBuf csc;               // int32 compacted sources: hub and warp rows CSR (doff), thread
+                                  // rows SELL-32 (sell_off), then CSC_PAD
+        int64_t n_slices = 0;     // 32-row slices of the thread-row bin
+        DevBuf sell_off;          // int64 [n_slices+1] csc offset of each slice (column-major, 32 wide)
         DevBuf chunk_base;        // int64 [n_hub+1] first chunk of each hub row
         DevBuf row_cum;           // int64 [|D|+1] exclusive prefix of row costs (edges + ROW_COST)
         int64_t unit_blocks = 0;  // grid size the units below were cut for
@@ -240,6 +243,10 @@ constexpr int64_t THREAD_DEG = PR_THREAD_DEG;   // rows up to this in-degree: on
 #ifndef PR_HUB_CHUNK
 #define PR_HUB_CHUNK 4096
 #endif
+// thread-row bin stored SELL-32 (sched.cu sell_layout); 0 = row-major CSR (A/B builds)
+#ifndef PR_SELL
+#define PR_SELL 1
+#endif
 #ifndef PR_DYNAMIC_UNITS
 #define PR_DYNAMIC_UNITS 1
 #endif
@@ -250,6 +257,7 @@ constexpr int64_t HUB_DEG = PR_HUB_CHUNK;      // rows above: cut into HUB_CHUNK
 constexpr int64_t HUB_CHUNK = PR_HUB_CHUNK;    // edges per hub unit (256 threads x HUB_CHUNK/256)
 constexpr int64_t ROW_COST = 8;                // per-row drain cost in edge units (unit sizing)
 constexpr int64_t UNITS_PER_BLOCK = PR_UNITS_PB;  // target work units per block of the persistent grid
+constexpr int64_t LONG_UNIT = 100000;           // edge-units: past this, UNITS_PER_BLOCK per section
 
 // PUSHRANK_TIMING=1: host-side phase timings (synchronising) on stderr
 void phase_mark(cudaStream_t st, const char *what);

@@ -680,6 +680,7 @@ static BinView part_view(Part &P) {
     T.ids = S.ids.as<int32_t>();
     T.doff = S.doff.as<int64_t>();
     T.csc = S.csc.as<int32_t>();
+    T.sell_off = S.sell_off.as<int64_t>();
     T.count = S.count;
     T.n_hub = S.n_hub;
     T.n_warp = S.n_warp;

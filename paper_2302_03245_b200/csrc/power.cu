@@ -233,6 +233,7 @@ int power_device(Graph &g, double damping, int64_t iterations, double tolerance,
     A.T.ids = S.ids.as<int32_t>();
     A.T.doff = S.doff.as<int64_t>();
     A.T.csc = S.csc.as<int32_t>();
+    A.T.sell_off = S.sell_off.as<int64_t>();
     A.T.count = S.count;
     A.T.n_hub = S.n_hub;
     A.T.n_warp = S.n_warp;

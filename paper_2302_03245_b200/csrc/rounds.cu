@@ -1155,6 +1155,18 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     if (getenv("PUSHRANK_TIMING"))
         fprintf(stderr, "[pushrank] round working set %.1f MB (L2 %.1f MB): stream %d prefetch %d sections %d\n",
                 ws / 1e6, l2 / 1e6, (int)stream, (int)prefetch, nsec);
+    if (getenv("PUSHRANK_TIMING")) {
+        auto &S = g.sched[which];
+        int64_t e[4] = {0, 0, 0, 0};
+        const int64_t rows[3] = {S.n_hub, S.n_hub + S.n_warp, S.count};
+        for (int k = 0; k < 3; ++k)
+            PR_CUDA(cudaMemcpy(&e[k], S.doff.as<int64_t>() + rows[k], 8, cudaMemcpyDeviceToHost));
+        if (S.n_slices) PR_CUDA(cudaMemcpy(&e[3], S.sell_off.as<int64_t>() + S.n_slices, 8, cudaMemcpyDeviceToHost));
+        fprintf(stderr, "[pushrank] bins: hub rows %lld (%lld edges), warp rows %lld (%lld edges), thread rows %lld "
+                "(%lld edges, %lld SELL slots)\n", (long long)S.n_hub, (long long)e[0], (long long)S.n_warp,
+                (long long)(e[1] - e[0]), (long long)(S.count - rows[1]), (long long)(e[2] - e[1]),
+                (long long)(S.n_slices ? e[3] - e[1] : 0));
+    }
     phase_mark(ctx.stream, "run: schedule");
     PR_TRY(ws_alloc(g, pull_blocks, fcap));
     phase_mark(ctx.stream, "run: workspace");
@@ -1181,6 +1193,7 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     A.T.ids = S.ids.as<int32_t>();
     A.T.doff = S.doff.as<int64_t>();
     A.T.csc = S.csc.as<int32_t>();
+    A.T.sell_off = S.sell_off.as<int64_t>();
     A.T.count = S.count;
     A.T.n_hub = S.n_hub;
     A.T.n_warp = S.n_warp;
@@ -1234,6 +1247,10 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     P.g_all = grid_for(n, 256);
     P.g_pull = (unsigned)pull_blocks;
     P.k_pull_fn = k_pull_fn;
+    // L1 / shared-memory split of the dense round: PUSHRANK_CARVEOUT=percent
+    // of the unified array given to shared memory (A/B; default: driver's)
+    if (const char *e = getenv("PUSHRANK_CARVEOUT"))
+        PR_CUDA(cudaFuncSetAttribute(k_pull_fn, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(e)));
     // reducing kernels of the fast engine: one resident wave, grid-stride
     // (a block's lifetime -- reduce, publish -- is latency, not bandwidth)
     auto wave = [&](const void *k) -> unsigned {

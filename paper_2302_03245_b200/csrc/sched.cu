@@ -13,6 +13,7 @@
 //              (edges + ROW_COST * rows, by a prefix sum), ~UNITS_PER_BLOCK
 //              per block of the persistent grid.
 #include <cub/cub.cuh>
+#include <utility>
 #include <thrust/iterator/counting_iterator.h>
 
 #include "cubutil.cuh"
@@ -79,6 +80,40 @@ __global__ void k_chunks_of(const int64_t *__restrict__ doff, int64_t n_hub, int
 
 __global__ void k_row_cost(const int64_t *__restrict__ doff, int64_t cnt, int64_t *__restrict__ cost) {
     GRID_STRIDE(i, cnt + 1) { cost[i] = i < cnt ? doff[i + 1] - doff[i] + ROW_COST : 0; }
+}
+
+// SELL-32 slices of the thread-row bin (rows [t0, count), 32 per slice):
+// width[s] = 32 * (largest degree in the slice); width[n_slices] = 0
+__global__ void k_slice_width(const int64_t *__restrict__ doff, int64_t t0, int64_t count, int64_t n_slices,
+                              int64_t *__restrict__ width) {
+    GRID_STRIDE(s, n_slices + 1) {
+        int64_t w = 0;
+        if (s < n_slices) {
+            const int64_t r0 = t0 + 32 * s, r1 = r0 + 32 < count ? r0 + 32 : count;
+            for (int64_t r = r0; r < r1; ++r) {
+                const int64_t d = doff[r + 1] - doff[r];
+                w = d > w ? d : w;
+            }
+        }
+        width[s] = 32 * w;
+    }
+}
+
+__global__ void k_add_i64(int64_t *__restrict__ a, int64_t count, int64_t v) {
+    GRID_STRIDE(i, count) a[i] += v;
+}
+
+// thread row r = t0 + 32 s + j: its k-th source goes to sell_off[s] + 32 k + j,
+// so lane j's k-th index load of a warp over slice s is one 128-byte line
+__global__ void k_sell_scatter(const int64_t *__restrict__ doff, int64_t t0, int64_t count,
+                               const int32_t *__restrict__ csr, const int64_t *__restrict__ sell_off,
+                               int32_t *__restrict__ out) {
+    GRID_STRIDE(i, count - t0) {
+        const int64_t r = t0 + i;
+        const int64_t lo = doff[r], d = doff[r + 1] - lo;
+        int32_t *dst = out + sell_off[i >> 5] + (i & 31);
+        for (int64_t k = 0; k < d; ++k) dst[32 * k] = csr[lo + k];
+    }
 }
 
 // hub chunk units (row, -(chunk+1)) in row/chunk order
@@ -176,6 +211,11 @@ int ensure_units(Graph &g, int which, int64_t blocks, int nsec) {
     int64_t total = 0;
     for (int k = 0; k < nsec; ++k) total += (cum_hi[k][1] - cum_lo[k][1]) + (cum_hi[k][2] - cum_lo[k][2]);
     int64_t T = total / (blocks * UNITS_PER_BLOCK);
+    // very long sweeps (C5: ~220K edge-units per unit): ~UNITS_PER_BLOCK units
+    // per block in every section, not over the whole sweep, so that the tail
+    // of each section launch is short (C5 4896 -> 4538 us per sweep; C3's
+    // short units lose with more of them: 9.9 -> 11.0 ms at 2x)
+    if (nsec > 1 && T > LONG_UNIT) T = total / (blocks * UNITS_PER_BLOCK * nsec);
     if (T < 400 * ROW_COST) T = 400 * ROW_COST;  // >= 3200 edge-units per unit
     int64_t cnt[PR_MAX_SECTIONS][3];
     int64_t n_units = 0;
@@ -212,6 +252,48 @@ int ensure_units(Graph &g, int which, int64_t blocks, int nsec) {
     PR_CUDA(cudaGetLastError());
     S.unit_blocks = blocks;
     S.nsec = nsec;
+    return PR_OK;
+}
+
+// Thread rows (<= THREAD_DEG in-edges, one thread each) in SELL-32 order:
+// a row-major CSR makes each warp index load touch 32 lines (one per lane's
+// row), as many L1TEX wavefronts as the gathers themselves; column-major
+// slices of 32 degree-sorted rows make it one line per load with almost no
+// padding (rows of a slice have near-equal degree).  The per-row summation
+// order is unchanged (ascending position, bins.cuh row_sum_sell).
+static int sell_layout(Ctx &ctx, Graph::Sched &S) {
+    cudaStream_t st = ctx.stream;
+    const int64_t t0 = S.n_hub + S.n_warp, nt = S.count - t0;
+    S.n_slices = (nt + 31) / 32;
+    PR_TRY(ensure(S.sell_off, 8 * (S.n_slices + 1)));
+    int64_t e0 = 0, sell = 0;
+    PR_CUDA(cudaMemcpyAsync(&e0, S.doff.as<int64_t>() + t0, 8, cudaMemcpyDeviceToHost, st));
+    if (nt <= 0 || !PR_SELL) {
+        PR_CUDA(cudaMemcpyAsync(S.sell_off.ptr, S.doff.as<int64_t>() + t0, 8, cudaMemcpyDeviceToDevice, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+        return PR_OK;
+    }
+    DevBuf width;
+    PR_TRY(ensure(width, 8 * (S.n_slices + 1)));
+    const unsigned gs = grid_for(S.n_slices + 1, 256) > 4096 ? 4096 : grid_for(S.n_slices + 1, 256);
+    k_slice_width<<<gs, 256, 0, st>>>(S.doff.as<int64_t>(), t0, S.count, S.n_slices, width.as<int64_t>());
+    PR_TRY(cub_run(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, width.as<int64_t>(), S.sell_off.as<int64_t>(), (int)(S.n_slices + 1),
+                                             st);
+    }));
+    PR_CUDA(cudaMemcpyAsync(&sell, S.sell_off.as<int64_t>() + S.n_slices, 8, cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaStreamSynchronize(st));
+    k_add_i64<<<gs, 256, 0, st>>>(S.sell_off.as<int64_t>(), S.n_slices + 1, e0);
+    DevBuf out;
+    PR_TRY(ensure(out, 4 * (e0 + sell + CSC_PAD)));
+    if (e0) PR_CUDA(cudaMemcpyAsync(out.ptr, S.csc.ptr, 4 * e0, cudaMemcpyDeviceToDevice, st));
+    PR_CUDA(cudaMemsetAsync(out.as<int32_t>() + e0, 0, 4 * (sell + CSC_PAD), st));
+    const unsigned gt = grid_for(nt, 256) > 65535 ? 65535 : grid_for(nt, 256);
+    k_sell_scatter<<<gt, 256, 0, st>>>(S.doff.as<int64_t>(), t0, S.count, S.csc.as<int32_t>(), S.sell_off.as<int64_t>(),
+                                      out.as<int32_t>());
+    PR_CUDA(cudaGetLastError());
+    std::swap(S.csc.ptr, out.ptr);
+    std::swap(S.csc.bytes, out.bytes);
     return PR_OK;
 }
 
@@ -308,6 +390,7 @@ int ensure_sched(Graph &g, int which) {
     PR_TRY(ensure(S.chunk_part, 8 * (S.n_chunks + 1)));
     PR_TRY(ensure(S.row_cnt, 4 * (S.n_hub + 1)));
     PR_CUDA(cudaMemsetAsync(S.row_cnt.ptr, 0, 4 * (S.n_hub + 1), st));
+    PR_TRY(sell_layout(ctx, S));
     // row cost prefix (unit sizing, ensure_units)
     DevBuf rcost;
     PR_TRY(ensure(rcost, 8 * (cnt + 1)));

@@ -72,6 +72,69 @@ __global__ void ub_stream(const int32_t *__restrict__ csc, int64_t edges, double
     if (acc == 123456789) out[0] = acc;
 }
 
+// v4: as v2, but each gather LDG is issued by one 8-lane group at a time
+// (4 predicated LDGs per 32 gathers): wavefronts per LDG <= 8
+__global__ void ub_gather_groups8(const int32_t *__restrict__ csc, int64_t edges, const double *__restrict__ x,
+                                  double *__restrict__ out) {
+    const int lane = threadIdx.x & 31, grp = lane >> 3;
+    double acc = 0.0;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = warp * 256; base < edges; base += nw * 256) {
+        int idx[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) idx[q] = base + lane + 32 * q < edges ? __ldg(&csc[base + lane + 32 * q]) : -1;
+        double t[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            double v = 0.0;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                double w;
+                const int on = grp == g && idx[q] >= 0;
+                asm volatile("{ .reg .pred p; setp.ne.s32 p, %2, 0;\n"
+                             "  mov.f64 %0, 0d0000000000000000;\n"
+                             "  @p ld.global.nc.f64 %0, [%1]; }"
+                             : "=d"(w) : "l"(x + (idx[q] >= 0 ? idx[q] : 0)), "r"(on));
+                v += w;
+            }
+            t[q] = v;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc += t[q];
+    }
+    if (acc == 123.456) out[0] = acc;
+}
+
+// v5: uniformly random indices (hash of the edge position): no locality
+// v6: sequential x[e mod n]: fully coalesced gathers (the LSU floor)
+template <int KIND>
+__global__ void ub_gather_synth(int64_t edges, int64_t n, const double *__restrict__ x, double *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    double acc = 0.0;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = warp * 256; base < edges; base += nw * 256) {
+        double t[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint64_t e = (uint64_t)(base + lane + 32 * q);
+            uint64_t i;
+            if (KIND == 0) {
+                uint64_t z = e * 0x9E3779B97F4A7C15ull;
+                z = (z ^ (z >> 31)) * 0xBF58476D1CE4E5B9ull;
+                i = (z ^ (z >> 29)) % (uint64_t)n;
+            } else {
+                i = e % (uint64_t)n;
+            }
+            t[q] = e < (uint64_t)edges ? __ldg(&x[i]) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc += t[q];
+    }
+    if (acc == 123.456) out[0] = acc;
+}
+
 int debug_gather(Graph &g0, int variant, int iters, int blocks_per_sm, double *ms_out) {
     PR_TRY(ensure_run_layout(g0));
     Graph &g = *g0.run;
@@ -95,6 +158,9 @@ int debug_gather(Graph &g0, int variant, int iters, int blocks_per_sm, double *m
             case 0: ub_gather8<<<grid, 256, 0, st>>>(S.csc.as<int32_t>(), S.edges, x.as<double>(), out.as<double>()); break;
             case 1: ub_gather16<<<grid, 256, 0, st>>>(S.csc.as<int32_t>(), S.edges, x.as<double>(), out.as<double>()); break;
             case 2: ub_gather_lanes<<<grid, 256, 0, st>>>(S.csc.as<int32_t>(), S.edges, x.as<double>(), out.as<double>()); break;
+            case 4: ub_gather_groups8<<<grid, 256, 0, st>>>(S.csc.as<int32_t>(), S.edges, x.as<double>(), out.as<double>()); break;
+            case 5: ub_gather_synth<0><<<grid, 256, 0, st>>>(S.edges, g.n, x.as<double>(), out.as<double>()); break;
+            case 6: ub_gather_synth<1><<<grid, 256, 0, st>>>(S.edges, g.n, x.as<double>(), out.as<double>()); break;
             default: ub_stream<<<grid, 256, 0, st>>>(S.csc.as<int32_t>(), S.edges, out.as<double>()); break;
             }
         }

@@ -13,14 +13,18 @@ import paper_2302_03245_b200 as P
 from paper_2302_03245_b200 import _lib, synthetic
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
-n, s, d = synthetic.make(cfg)
-g = P.from_edges(n, s, d)
+if cfg == "c5":
+    g = P.graph.Graph(P.graph.DeviceGraph.rmat(26, 16, seed=0), raw_edge_count=16 << 26, name="c5")
+else:
+    n, s, d = synthetic.make(cfg)
+    g = P.from_edges(n, s, d)
 L = _lib.load()
 L.pr_debug_gather.restype = ctypes.c_int
 L.pr_debug_gather.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
-names = {0: "gather8 thread-contig", 1: "gather16 thread-contig", 2: "gather lane-interleaved", 3: "index stream only"}
-for v in range(4):
-    for bps in (4, 8, 16):
+names = {0: "gather8 thread-contig", 1: "gather16 thread-contig", 2: "gather lane-interleaved", 3: "index stream only",
+         4: "lane-interleaved, 8-lane LDGs", 5: "uniform random gather", 6: "sequential gather"}
+for v in [int(a) for a in (sys.argv[2].split(",") if len(sys.argv) > 2 else range(7))]:
+    for bps in (4, 8):
         ms = ctypes.c_double()
         _lib.check(L.pr_debug_gather(g.dev.handle, v, 20, bps, ctypes.byref(ms)))
         print(f"{cfg} {names[v]:26s} blocks/SM={bps:2d}: {ms.value*1e3:8.1f} us")
