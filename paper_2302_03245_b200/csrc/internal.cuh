@@ -116,6 +116,9 @@ struct RunCtl {
     Partial sec_acc;
     int32_t gs;               // next pull round is a Gauss-Seidel sweep
     int32_t push_filter;      // next push round follows a GS sweep
+    // observed exact runs (sync_simulate on_iteration): states snapshotted
+    // into the ring since the batch began, and the round index of the first
+    int64_t obs_count, obs_t0;
 };
 
 
@@ -183,6 +186,7 @@ struct Graph {
     } sched[3];
     // run workspace
     DevBuf h, reserved, s2, act, in_d, frontier2, partials, ctl, rows;
+    DevBuf obs_ring;          // observed exact runs: K (reserved, pending) snapshots
     int64_t rows_cap = 0;
     int64_t max_blocks = 0;     // partial slots per region (partials holds 3 regions)
     int64_t n_dangling = -1;    // #(out_degree == 0), computed lazily

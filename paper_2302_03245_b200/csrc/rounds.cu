@@ -85,6 +85,10 @@ struct RunArgs {
     const uint8_t *sec_of;     // IFP1: section of each vertex's row (push filter); null for IFP2
     int64_t sec_row[PR_MAX_SECTIONS + 1];
     int64_t sec_unit[PR_MAX_SECTIONS + 1];
+    // observed exact runs: the device loop pauses after obs_batch rounds so
+    // the host can drain obs_ring (obs_batch x [reserved | pending]) in one copy
+    int64_t obs_batch;
+    double *obs_ring;
 };
 
 // every solve kernel counts its own launch once (block 0, thread 0), early
@@ -231,6 +235,8 @@ __device__ void finalize_row(const RunArgs &A, const Partial &tot, int64_t r, bo
     int done = 0;
     if (tot.nact == 0) done = 1;
     else if (r >= A.max_rounds) done = 2;
+    // observed exact run: leave the graph's loop once the ring is full
+    const bool pause = A.obs_batch > 0 && ctl->obs_count >= A.obs_batch;
     ctl->done = done;
     ctl->round = r;
     // push needs the frontier of this state, recorded only when predicted
@@ -263,7 +269,7 @@ __device__ void finalize_row(const RunArgs &A, const Partial &tot, int64_t r, bo
     ctl->blocks_done = 0;
     __threadfence();
     if (A.use_graph) {
-        cudaGraphSetConditional(A.h_loop, done ? 0u : 1u);
+        cudaGraphSetConditional(A.h_loop, (done || pause) ? 0u : 1u);
         if (A.has_mode) {
             cudaGraphSetConditional(A.h_pull, !done && mode == 0 ? 1u : 0u);
             cudaGraphSetConditional(A.h_push, !done && mode == 1 ? 1u : 0u);
@@ -680,6 +686,31 @@ __global__ void k_ex_pull(RunArgs A) {
     A.h[v] = __dadd_rn(base, acc);
 }
 
+// Observed exact runs (sync_simulate's on_iteration, engines.py:453-454):
+// a batch starts with an empty ring; after each round's update the state
+// (reserved, pending) goes to the next ring slot.
+__global__ void k_obs_begin(RunArgs A) {
+    count_launch(A);
+    A.ctl->obs_count = 0;
+    A.ctl->obs_t0 = A.ctl->rows - 1;
+}
+
+__global__ void k_obs_snap(RunArgs A) {
+    count_launch(A);
+    const int64_t j = A.ctl->obs_count;
+    double *dst = A.obs_ring + 2 * j * A.n;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < A.n; v += (int64_t)gridDim.x * blockDim.x) {
+        dst[v] = A.reserved[v];
+        dst[A.n + v] = A.h[v];
+    }
+}
+
+// one thread: the snapshot is complete (every k_obs_snap block ran), count it
+__global__ void k_obs_count(RunArgs A) {
+    count_launch(A);
+    A.ctl->obs_count += 1;
+}
+
 // ---------------------------------------------------------------- settle + normalise (K7)
 
 // engines.py:269-289: reserved[d] = h[d] + sum_{u in S(d)} (c*reserved[u])/deg[u]
@@ -942,6 +973,23 @@ static int build_graph(Plan &P, cudaGraph_t *out_g, cudaGraphExec_t *out_exec) {
     A.use_graph = 1;
     void *args[] = {&A};
     cudaGraphNode_t n_reset, n_init, n_seed, n_while, n_a, n_b;
+    if (P.exact && A.obs_batch > 0) {
+        // observed batches: the host ran reset/init/prep of state 0; each
+        // launch continues the loop until the ring is full (or done)
+        cudaGraphNode_t n_begin, n_c;
+        PR_TRY(add_kernel(G, &n_begin, nullptr, 0, (void *)k_obs_begin, 1, 1, args));
+        cudaGraph_t body;
+        PR_TRY(add_while(G, &n_while, &n_begin, A.h_loop, &body));
+        PR_TRY(add_kernel(body, &n_a, nullptr, 0, (void *)k_ex_pull, P.g_all, 256, args));
+        PR_TRY(add_kernel(body, &n_b, &n_a, 1, (void *)k_obs_snap, P.g_all, 256, args));
+        PR_TRY(add_kernel(body, &n_c, &n_b, 1, (void *)k_obs_count, 1, 1, args));
+        PR_TRY(add_kernel(body, &n_a, &n_c, 1, (void *)k_ex_prep, P.g_all, 256, args));
+        cudaGraphExec_t ex;
+        PR_CUDA(cudaGraphInstantiate(&ex, G, 0));
+        *out_g = G;
+        *out_exec = ex;
+        return PR_OK;
+    }
     PR_TRY(add_kernel(G, &n_reset, nullptr, 0, (void *)k_reset, 1, 1, args));
     if (P.exact) {
         PR_TRY(add_kernel(G, &n_init, &n_reset, 1, (void *)k_ex_init, P.g_all, 256, args));
@@ -1081,7 +1129,12 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     if (p.max_rounds < 0) return fail(PR_ERR_ARG, "max_rounds must be non-negative");
     const bool exact = p.mode == PR_MODE_EXACT;
     if (p.on_round && !exact) return fail(PR_ERR_ARG, "on_round observers need PR_MODE_EXACT");
-    const bool host_loop = p.host_loop || p.on_round;
+    // on_round observers: the device loop runs in batches that snapshot
+    // every state into a ring the host drains once per batch (one copy, no
+    // host round trip per round); PUSHRANK_HOST_LOOP=1 / host_loop keep the
+    // round-by-round form
+    const bool observed = p.on_round && !p.host_loop && !getenv("PUSHRANK_HOST_LOOP");
+    const bool host_loop = p.host_loop || (p.on_round && !observed);
     if (algo == PR_ALGO_IFP2 && !g_in.has_ifp2 && !g_in.ifp2_counted) return fail(PR_ERR_STATE, "IFP2 needs pr_preprocess_ifp2 first");
     // fast engines run on the relabelled layout; exact mode on the original
     Graph *gp = &g_in;
@@ -1274,6 +1327,21 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     PR_CUDA(cudaEventCreate(&e1));
     PR_CUDA(cudaEventCreate(&e2));
     PR_CUDA(cudaEventRecord(e0, st));
+    int64_t obs_k = 0;
+    if (observed) {
+        // ring of K states (reserved | pending), K <= 64, within ~1 GiB
+        obs_k = ((int64_t)1 << 30) / (16 * (n > 0 ? n : 1));
+        if (obs_k > 64) obs_k = 64;
+        if (obs_k < 1) obs_k = 1;
+        PR_TRY(ensure(g.obs_ring, 16 * n * obs_k));
+        A.obs_batch = obs_k;
+        A.obs_ring = g.obs_ring.as<double>();
+        A.use_graph = 0;
+        k_reset<<<1, 1, 0, st>>>(A);
+        k_ex_init<<<P.g_all, 256, 0, st>>>(A);
+        k_ex_prep<<<P.g_all, 256, 0, st>>>(A);
+        PR_CUDA(cudaGetLastError());
+    }
     if (!host_loop) {
         // the plan's bytes (graph-owned conditional handles still zero) key
         // the context's executable-graph cache
@@ -1300,7 +1368,27 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
             phase_mark(ctx.stream, "run: graph instantiate");
         }
         slot->used = ++ctx.exec_tick;
-        PR_CUDA(cudaGraphLaunch(slot->exec, st));
+        if (!observed) {
+            PR_CUDA(cudaGraphLaunch(slot->exec, st));
+        } else {
+            std::vector<double> ring((size_t)(2 * n * obs_k));
+            RunCtl hc;
+            for (;;) {
+                PR_CUDA(cudaMemcpyAsync(&hc, A.ctl, sizeof(hc), cudaMemcpyDeviceToHost, st));
+                PR_CUDA(cudaStreamSynchronize(st));
+                if (hc.done) break;
+                PR_CUDA(cudaGraphLaunch(slot->exec, st));
+                PR_CUDA(cudaMemcpyAsync(&hc, A.ctl, sizeof(hc), cudaMemcpyDeviceToHost, st));
+                PR_CUDA(cudaStreamSynchronize(st));
+                if (hc.obs_count > 0)
+                    PR_CUDA(cudaMemcpyAsync(ring.data(), A.obs_ring, 16 * n * hc.obs_count, cudaMemcpyDeviceToHost,
+                                            st));
+                PR_CUDA(cudaStreamSynchronize(st));
+                // reference semantics: called after round t's update (engines.py:453-454)
+                for (int64_t j = 0; j < hc.obs_count; ++j)
+                    p.on_round(p.user, hc.obs_t0 + j, ring.data() + 2 * j * n, ring.data() + (2 * j + 1) * n);
+            }
+        }
     } else {
         A.use_graph = 0;
         RunCtl hc;

@@ -26,6 +26,7 @@ from __future__ import annotations
 import math
 import os
 import time
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -54,12 +55,103 @@ def _mode(mode: str | None) -> str:
     return mode
 
 
-def _keep_rows(rows, sample_every):
-    # sample_every=inf: the reference records only the final sample
-    # (engines.py:199-215); otherwise one row per device round
-    if sample_every is not None and math.isinf(sample_every):
+@dataclass
+class MassState:
+    """Reserved and pending mass per vertex (engines.py:44-54): a fresh
+    state reserves nothing and holds one raw unit of pending mass on every
+    vertex.  The device engines keep this state in HBM (``h`` / ``reserved``
+    of the run workspace, initialised by ``k_init``); the host class stays
+    for callers that build or inspect states themselves."""
+
+    reserved: np.ndarray
+    pushing: np.ndarray
+
+    @classmethod
+    def fresh(cls, n: int) -> "MassState":
+        return cls(reserved=np.zeros(n, dtype=np.float64), pushing=np.ones(n, dtype=np.float64))
+
+
+@dataclass
+class Partition:
+    """Vertex-to-worker assignment (engines.py:57-73): disjoint ascending id
+    sets per CPU worker over the scan universe, plus the dangling side for
+    the two-phase settle.  The device engines schedule by degree bins
+    instead (csrc/sched.cu); ``workers`` / ``strategy`` of the entry points
+    are validated through the same rules and recorded in ``trace.meta``."""
+
+    strategy: str
+    worker_vertices: list
+    worker_dangling: list | None = None
+
+    @property
+    def workers(self) -> int:
+        return len(self.worker_vertices)
+
+
+def _assign(ids: np.ndarray, weights: np.ndarray, workers: int, strategy: str) -> list:
+    """One worker set per worker, each sorted ascending (engines.py:76-89):
+    contiguous blocks (np.array_split sizes), every workers-th id, or
+    heaviest-first round-robin (weight descending, ties by id)."""
+    if strategy == "contiguous":
+        sets = np.array_split(ids, workers)
+    elif strategy == "strided":
+        sets = [ids[k::workers] for k in range(workers)]
+    elif strategy == "degree-balanced":
+        by_weight = np.lexsort((ids, -weights))
+        sets = [ids[by_weight[k::workers]] for k in range(workers)]
+    else:
+        raise ValueError(f"unknown partition strategy {strategy!r}")
+    return [np.sort(np.asarray(s)).astype(np.int64) for s in sets]
+
+
+def partition_vertices(g, workers: int, strategy: str = "degree-balanced",
+                       cls: VertexClassification | None = None) -> Partition:
+    """Split the vertices among CPU workers (engines.py:92-117).
+
+    With ``cls``: the non-dangling vertices (weight out-degree + 1) and,
+    separately, the dangling ones (weight in-degree + 1).  Without it: all
+    vertices by out-degree + 1."""
+    if workers < 1:
+        raise ValueError(f"worker count must be >= 1, got {workers}")
+    out_deg = np.asarray(g.out_degree, np.int64)
+    if cls is None:
+        every = np.arange(g.n, dtype=np.int64)
+        return Partition(strategy, _assign(every, out_deg + 1, workers, strategy))
+    dang = cls.dangling_mask(g.n)
+    live = np.flatnonzero(~dang)
+    dead = np.flatnonzero(dang)
+    in_deg = np.asarray(g.in_degree, np.int64)
+    return Partition(strategy, _assign(live, out_deg[live] + 1, workers, strategy),
+                     _assign(dead, in_deg[dead] + 1, workers, strategy))
+
+
+def _sample_period(n: int, sample_every: float | None) -> float:
+    """The reference's default trace period: 10 ms up to 1e5 vertices,
+    250 ms above (engines.py:219-222)."""
+    if sample_every is not None:
+        return sample_every
+    return 0.01 if n <= 100_000 else 0.25
+
+
+def _keep_rows(rows, sample_every, n):
+    """Time-based trace sampling as in _run_phase (engines.py:199-215): the
+    device writes one row per round with its device timestamp (wall_ms);
+    keep a row whenever ``period`` seconds have passed since the last kept
+    one (the first row always), and always the final row.  ``inf`` keeps
+    only the final row, 0 every round."""
+    period = _sample_period(n, sample_every)
+    if len(rows) == 0:
+        return rows
+    if math.isinf(period):
         return rows[-1:]
-    return rows
+    keep, last = [], -math.inf
+    wall_s = np.asarray(rows["wall_ms"], np.float64) * 1e-3
+    for i in range(len(rows) - 1):
+        if wall_s[i] - last >= period:
+            keep.append(i)
+            last = wall_s[i]
+    keep.append(len(rows) - 1)
+    return rows[np.asarray(keep)]
 
 
 def ifp1_run(g, cls: VertexClassification | None, cfg: SolverConfig, workers: int = 1,
@@ -81,7 +173,7 @@ def ifp1_run(g, cls: VertexClassification | None, cfg: SolverConfig, workers: in
     values, rows, res, _, _ = dev.run("ifp1", mode, cfg.damping, cfg.threshold, DEFAULT_MAX_ROUNDS,
                                       _lib.CONV_SCAN)
     wall = time.perf_counter() - start
-    trace = RunTrace(samples=samples_from_rows(_keep_rows(rows, sample_every)),
+    trace = RunTrace(samples=samples_from_rows(_keep_rows(rows, sample_every, g.n)),
                      meta={"algorithm": "ifp1", "threshold": cfg.threshold, "workers": workers,
                            "strategy": strategy, "backend": kern.NAME, "mode": mode, "rounds": int(res.rounds),
                            "pull_rounds": int(res.pull_rounds), "push_rounds": int(res.push_rounds),
@@ -109,7 +201,7 @@ def ifp2_run(pg: IFP2Graph, cfg: SolverConfig, workers: int = 1, strategy: str =
                                       _lib.CONV_SCAN)
     wall = time.perf_counter() - start
     phase1, settle_row = rows[:-1], rows[-1:]
-    kept = np.concatenate([_keep_rows(phase1, sample_every), settle_row])
+    kept = np.concatenate([_keep_rows(phase1, sample_every, g.n), settle_row])
     trace = RunTrace(samples=samples_from_rows(kept),
                      meta={"algorithm": "ifp2", "threshold": cfg.threshold, "workers": workers,
                            "strategy": strategy, "backend": kern.NAME, "mode": mode, "rounds": int(res.rounds),

@@ -314,6 +314,30 @@ class VertexClassification:
         return mask
 
 
+@dataclass
+class StatsRow:
+    """Dataset summary row (graph.py:113-127): counts and dangling structure."""
+
+    name: str
+    n: int
+    m: int
+    dangling_vertices: int
+    dangling_edges: int
+    avg_degree: float
+    raw_edge_count: int
+
+    def as_csv_row(self) -> list:
+        return [self.name, self.n, self.m, self.dangling_vertices, self.dangling_edges, f"{self.avg_degree:.6g}"]
+
+
+def stats(g, cls: VertexClassification) -> StatsRow:
+    """Summary counts of a graph and its classification (graph.py:321-331);
+    the counts come from the device classification, no host arrays."""
+    return StatsRow(name=g.name, n=int(g.n), m=int(g.m), dangling_vertices=int(len(cls.dangling)),
+                    dangling_edges=int(cls.dangling_edge_count), avg_degree=g.m / g.n,
+                    raw_edge_count=int(g.raw_edge_count))
+
+
 class IFP2Graph:
     """Graph split for two-phase pushing (graph.py:92-110), on the device.
 

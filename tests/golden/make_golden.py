@@ -30,6 +30,9 @@ Fixtures
               fixed estimates, _power_iterations_to_target hits, sweep_xi
               errors of the deterministic engines, compare_algorithms
               settings, and formatted CSV rows.  ``--only harness``.
+  suite.npz   the seeded corpora of the reference's test_engines.py /
+              test_graph.py / test_solvers.py (edges + dense oracle) and its
+              partition_vertices outputs.  ``--only suite``.
   serialize.npz  write_ranking_csv (serialize.py:14-21) output bytes for
               reference vectors on edge-list graphs with sparse original ids,
               a uniform vector (all ties) and the C1 power vector.
@@ -241,10 +244,53 @@ def harness_cases(P) -> None:
     print("harness.npz")
 
 
+# seeded corpora the reference's own test files draw (tests/test_engines.py,
+# test_graph.py, test_solvers.py): (seed, count)
+SUITE_CORPORA = ((23, 10), (31, 12), (41, 1), (55, 1), (61, 8), (71, 5), (77, 1), (83, 1), (91, 8),
+                 (20260811, 20), (3, 8), (5, 1), (9, 1), (17, 10))
+
+
+def suite_cases(P, corpus) -> None:
+    """suite.npz: the graphs of the reference test suite's seeded corpora
+    (edges), the reference's dense oracle on each, and the reference's
+    partition_vertices outputs (engines.py:92-117) for the partition tests
+    (test_engines.py:35-96), so tests/test_reference_suite.py restates those
+    tests against this package without the reference installed."""
+    out = {}
+    for seed, count in SUITE_CORPORA:
+        for i, g in enumerate(corpus.random_corpus(count, seed=seed)):
+            pre = f"s{seed}_{i}_"
+            out[pre + "n"] = np.int64(g.n)
+            out[pre + "src"] = np.repeat(np.arange(g.n), np.diff(g.out_offsets)).astype(np.int64)
+            out[pre + "dst"] = np.asarray(g.out_targets, np.int64)
+            out[pre + "dense"] = P.dense_oracle(g, P.SolverConfig()).values
+            if seed == 23:
+                cls = P.classify(g)
+                for strat in ("contiguous", "strided", "degree-balanced"):
+                    part = P.partition_vertices(g, 3, strat, cls)
+                    out[pre + f"part_{strat}_v"] = np.concatenate(part.worker_vertices)
+                    out[pre + f"part_{strat}_vlen"] = np.array([x.size for x in part.worker_vertices], np.int64)
+                    out[pre + f"part_{strat}_d"] = np.concatenate(part.worker_dangling)
+                    out[pre + f"part_{strat}_dlen"] = np.array([x.size for x in part.worker_dangling], np.int64)
+    rng = np.random.default_rng(4)
+    for k in range(5):
+        n = 400
+        src = rng.integers(0, n, size=4000)
+        dst = rng.integers(0, n, size=4000)
+        g = P.from_edges(n, src, dst)
+        part = P.partition_vertices(g, 4, "degree-balanced")
+        out[f"bal{k}_src"] = src.astype(np.int64)
+        out[f"bal{k}_dst"] = dst.astype(np.int64)
+        out[f"bal{k}_v"] = np.concatenate(part.worker_vertices)
+        out[f"bal{k}_vlen"] = np.array([x.size for x in part.worker_vertices], np.int64)
+    np.savez_compressed(os.path.join(HERE, "suite.npz"), **out)
+    print("suite.npz:", sum(c for _, c in SUITE_CORPORA), "graphs")
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref-src", default="/tmp/refpkg/src")
-    ap.add_argument("--only", default=None, choices=["edge_lists", "serialize", "harness"])
+    ap.add_argument("--only", default=None, choices=["edge_lists", "serialize", "harness", "suite"])
     args = ap.parse_args()
     ensure_reference(args.ref_src)
     import pushrank as P
@@ -260,7 +306,11 @@ def main() -> None:
     if args.only == "harness":
         harness_cases(P)
         return
+    if args.only == "suite":
+        suite_cases(P, corpus)
+        return
     edge_lists(P)
+    suite_cases(P, corpus)
     serialize_cases(P)
     harness_cases(P)
 
