@@ -435,9 +435,12 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
     import torch
     import torch.distributed as dist
     from paper_2302_03245_b200 import distributed as D
-    # partitions of the engines' run layout (hot sources at low ids)
-    order = D.run_order(np.diff(g.out_offsets), np.diff(g.in_offsets))
-    part = D.partition_graph(g, world, rank, args.algo, order=order)
+    # this rank's partition of the engines' run layout (hot sources at low
+    # ids), built on its own GPU from its device graph: no host export of the
+    # graph (pr_part_from_graph); the host copy of the rows is what the e2e
+    # leg uploads every step
+    part = D.partition_device(g, world, rank, args.algo, DAMPING, XI)
+    host_part = part.to_host()
     comm = D.Comm(device=torch.device("cpu") if dist.get_backend() == "gloo" else torch.device("cuda", local))
     # the partition is uploaded once (inputs resident in HBM for `value`);
     # pr_part_init resets the round state of every solve.  Fast local step
@@ -484,7 +487,7 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
         # (the all-gather form: a fresh partition per step would otherwise pay
         # the replicas' cudaMalloc/IPC mapping every step, which a resident
         # partition does once)
-        s2 = D.CudaLocalStep(part, DAMPING, XI, args.algo, device=local, fast=True)
+        s2 = D.CudaLocalStep(host_part, DAMPING, XI, args.algo, device=local, fast=True)
         solve(s2, host_values=True, fused=False)
         del s2
     torch.cuda.synchronize()
@@ -497,7 +500,7 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
     # edges) over the whole solve's device time, per GPU, against the HBM peak
     peak = float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)) \
         if os.path.exists(os.path.join(REPO, "MEASURED_PEAKS.json")) else 6650.0
-    n_scan = float(np.count_nonzero(np.diff(np.asarray(g.out_offsets)) > 0))
+    n_scan = float(g.n - int(g.dev.classify().dangling))
     bytes_solve = 12.0 * info["push_ops"] + 40.0 * info.get("drained", 0) + 8.0 * n_scan * (info["rounds"] + 1)
     achieved = bytes_solve * args.steps / total_s / world / 1e9
     if rank == 0:
@@ -507,7 +510,10 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
                 "config": dict(config_desc(args, g.n, g.m), parallelism=f"vertex-range x{world}"),
                 "rounds": info["rounds"], "push_ops_per_step": info["push_ops"], "preprocess_s": preprocess_s,
                 "e2e": {"value": info["push_ops"] / e2e_s / 1e9, "unit": "GTEPS",
-                        "h2d_bytes_per_step": int(part.in_sources.nbytes + part.in_offsets.nbytes),
+                        # bytes pr_part_create copies: int64 offsets, int32 sources / degrees /
+                        # row lengths / dangling-target counts, uint8 flags
+                        "h2d_bytes_per_step": int(8 * (host_part.owned + 1) + 4 * host_part.in_sources.size
+                                                  + 12 * host_part.owned + 2 * host_part.owned),
                         "d2h_bytes_per_step": int(8 * part.owned), "ms_per_step": 1e3 * e2e_s,
                         "path": "per step: partition upload (pr_part_create) + rounds (all-gather exchange) + owned values D2H"},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -523,6 +529,7 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
                 "clocks": clocks.summary(),
                 "exchange": ("fused: round kernel stores shares into every rank's replica (peer memory)"
                              if fused else "NCCL all-gather of shares per round"),
+                "partition_build": "on each rank's GPU from its device graph's run layout (pr_part_from_graph)",
                 "note": ("partitioned rounds queued on the device and graph-captured (statistics read back "
                          "every 8 rounds); local step = binned dense-round gather (k_part_pull); "
                          "all-reduce of 9 statistics per round (the round barrier)")}

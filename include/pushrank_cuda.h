@@ -280,6 +280,24 @@ int pr_part_round(pr_part *p, const double *d_shares_full, double *d_shares_mine
  * the fast form before the first round (rank-local Gauss-Seidel sections);
  * the fused-exchange setup sets it too. */
 int pr_part_set_rank(pr_part *p, int32_t parts, int32_t rank);
+/* Rank `rank`'s partition built on the device from a device graph, with no
+ * host arrays: vertex ranges of the engines' run layout
+ * (graph.cu; distributed.run_order) with edge-balanced bounds (in-degree + 8
+ * per row, distributed.edge_balanced_ranges), padded source ids, global
+ * out-degrees, push-row lengths (IFP2: live degree), dangling-target counts
+ * and flags -- the content of distributed.partition_graph(g, parts, rank,
+ * algorithm, order=run_order(...)).  bounds (parts+1 int64, run ids) may be
+ * NULL.  The partition lives on the graph's device and stays valid after
+ * the graph is destroyed.  The rank is set (pr_part_set_rank). */
+int pr_part_from_graph(pr_graph *g, int32_t parts, int32_t rank, int32_t algorithm, double damping,
+                       double threshold, int64_t *bounds, pr_part **out);
+/* A partition's sizes (owned rows, padded slot, edges) and its rows as host
+ * arrays in pr_part_create's layout (int64 offsets[owned+1], padded
+ * sources[edges], degrees / row lengths / dangling-target counts[owned],
+ * uint8 flags[owned]); any output pointer may be NULL. */
+int pr_part_sizes(pr_part *p, int64_t *owned, int64_t *slot, int64_t *edges);
+int pr_part_export_rows(pr_part *p, int64_t *in_offsets, int64_t *in_sources, int64_t *out_degree,
+                        int64_t *row_len, int64_t *dangling_target_counts, uint8_t *dangling, uint8_t *receives);
 /* Kernel launches of one fast round (one per Gauss-Seidel section; the
  * last section's launch also reduces the statistics). */
 int pr_part_launches_per_round(pr_part *p, int32_t *launches);

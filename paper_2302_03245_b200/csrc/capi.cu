@@ -66,6 +66,10 @@ int part_share_buffers(Part &P, int parts, int rank, void **d_full, void *ipc);
 int part_set_peers(Part &P, const void *handles);
 int part_set_peer_ptrs(Part &P, int parts, int rank, void *const *ptrs);
 int part_set_rank(Part &P, int parts, int rank);
+int part_from_graph(Graph &g, int parts, int rank, int algorithm, double c, double xi, int64_t *bounds, Part **out);
+int part_export_rows(Part &P, int64_t *in_off, int64_t *in_src, int64_t *deg, int64_t *row_len, int64_t *dtc,
+                     uint8_t *dang, uint8_t *recv);
+int part_sizes(Part &P, int64_t *owned, int64_t *slot, int64_t *edges);
 int part_launches_per_round(Part &P, int *out);
 int part_close_peers(Part &P);
 int part_init_fused(Part &P, double *d_stats9);
@@ -550,9 +554,32 @@ int pr_part_create(pr_ctx *ctx, int64_t owned, int64_t slot, const int64_t *in_o
     return PR_OK;
 }
 
+int pr_part_from_graph(pr_graph *g, int32_t parts, int32_t rank, int32_t algorithm, double damping,
+                       double threshold, int64_t *bounds, pr_part **out) {
+    CHECK_PTR(g, "graph");
+    CHECK_PTR(out, "out");
+    PR_TRY(set_device(*g->g->ctx));
+    Part *P = nullptr;
+    PR_TRY(part_from_graph(*g->g, parts, rank, algorithm, damping, threshold, bounds, &P));
+    *out = new pr_part{P};
+    return PR_OK;
+}
+
 #define PART_ENTER(p)            \
     CHECK_PTR(p, "partition");   \
     PR_TRY(set_device(part_ctx(*(p)->p)))
+
+int pr_part_sizes(pr_part *p, int64_t *owned, int64_t *slot, int64_t *edges) {
+    PART_ENTER(p);
+    return part_sizes(*p->p, owned, slot, edges);
+}
+
+int pr_part_export_rows(pr_part *p, int64_t *in_offsets, int64_t *in_sources, int64_t *out_degree,
+                        int64_t *row_len, int64_t *dangling_target_counts, uint8_t *dangling, uint8_t *receives) {
+    PART_ENTER(p);
+    return part_export_rows(*p->p, in_offsets, in_sources, out_degree, row_len, dangling_target_counts, dangling,
+                            receives);
+}
 
 int pr_part_init(pr_part *p, double *d_shares_mine, int64_t *ints, double *floats) {
     PART_ENTER(p);

@@ -518,6 +518,206 @@ int part_create(Ctx &ctx, int64_t owned, int64_t slot, const int64_t *in_off, co
     return PR_OK;
 }
 
+// ---------------------------------------------------------------- partitions built on the device
+// A rank's partition of a device graph's run layout (graph.cu
+// ensure_run_layout), without host arrays: the same content as
+// distributed.partition_graph(g, parts, rank, order=run_order(...)) -- the
+// bounds bit-identical (edge_balanced_ranges), each row's sources the same
+// set in the run layout's row order (the fast local step's schedule does not
+// depend on it).
+
+// w[v] = in_degree(v) + ROW_COST; w[n] = 0 (exclusive scan -> cum[0..n])
+__global__ void k_part_weights(const int64_t *__restrict__ in_off, int64_t n, int64_t *__restrict__ w) {
+    GRID_STRIDE(v, n + 1) w[v] = v < n ? in_off[v + 1] - in_off[v] + ROW_COST : 0;
+}
+
+// b[k] = first v with cum[v] >= floor(cum[n] * k / parts) (np.searchsorted
+// side="left"), b[0] = 0, b[parts] = n, then a running maximum
+__global__ void k_part_bounds(const int64_t *__restrict__ cum, int64_t n, int parts, int64_t *__restrict__ b) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int64_t prev = 0;
+    for (int k = 0; k <= parts; ++k) {
+        int64_t x;
+        if (k == 0) x = 0;
+        else if (k == parts) x = n;
+        else {
+            const int64_t target = (int64_t)((__int128)cum[n] * k / parts);
+            int64_t lo = 0, hi = n + 1;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (cum[mid] >= target) hi = mid;
+                else lo = mid + 1;
+            }
+            x = lo;
+        }
+        prev = x > prev ? x : prev;
+        b[k] = prev;
+    }
+}
+
+struct PadMap {
+    int64_t b[PR_MAX_PEERS + 1];
+    int parts;
+    int64_t slot;
+    __device__ __forceinline__ int32_t operator()(int32_t u) const {
+        int r = 0;
+        while (r + 1 < parts && u >= b[r + 1]) ++r;
+        return (int32_t)(r * slot + (u - b[r]));
+    }
+};
+
+__global__ void k_part_rows(const int64_t *__restrict__ in_off, int64_t lo, int64_t owned, int64_t *__restrict__ out) {
+    GRID_STRIDE(i, owned + 1) out[i] = in_off[lo + i] - in_off[lo];
+}
+
+__global__ void k_part_sources(const int32_t *__restrict__ in_src, int64_t e0, int64_t edges, PadMap map,
+                               int32_t *__restrict__ out) {
+    GRID_STRIDE(e, edges) out[e] = map(in_src[e0 + e]);
+}
+
+__global__ void k_part_vertex(const int32_t *__restrict__ out_deg, const int32_t *__restrict__ dtc, int64_t lo,
+                              int64_t owned, int ifp2, int32_t *__restrict__ deg, int32_t *__restrict__ row_len,
+                              int32_t *__restrict__ pdtc, uint8_t *__restrict__ dang, uint8_t *__restrict__ recv) {
+    GRID_STRIDE(i, owned) {
+        const int32_t d = out_deg[lo + i], t = dtc ? dtc[lo + i] : 0;
+        deg[i] = d;
+        row_len[i] = ifp2 ? d - t : d;           // live degree (graph.py:353-356) / out-degree
+        pdtc[i] = ifp2 ? 0 : t;
+        dang[i] = d == 0;
+        recv[i] = ifp2 ? d > 0 : 1;
+    }
+}
+
+int part_from_graph(Graph &g_in, int parts, int rank, int algorithm, double c, double xi, int64_t *bounds_out,
+                    Part **out) {
+    if (parts < 1 || parts > PR_MAX_PEERS || rank < 0 || rank >= parts)
+        return fail(PR_ERR_ARG, "partition: need 1 <= parts <= " + std::to_string(PR_MAX_PEERS) +
+                                    " and 0 <= rank < parts");
+    if (algorithm != PR_ALGO_IFP1 && algorithm != PR_ALGO_IFP2)
+        return fail(PR_ERR_ARG, "partition: algorithm must be ifp1 or ifp2");
+    if (!(c > 0.0 && c < 1.0)) return fail(PR_ERR_ARG, "damping must be in (0,1)");
+    if (!(xi > 0.0)) return fail(PR_ERR_ARG, "threshold must be positive");
+    PR_TRY(ensure_run_layout(g_in));
+    Graph &r = *g_in.run;
+    Ctx &ctx = *r.ctx;
+    cudaStream_t st = ctx.stream;
+    const int64_t n = r.n;
+    PR_TRY(ensure_dtc(r));
+    int64_t b[PR_MAX_PEERS + 1];
+    {
+        DevBuf w, cum, db;
+        PR_TRY(ensure(w, 8 * (n + 1)));
+        PR_TRY(ensure(cum, 8 * (n + 1)));
+        PR_TRY(ensure(db, 8 * (PR_MAX_PEERS + 1)));
+        k_part_weights<<<grid_for(n + 1, 256) > 4096 ? 4096 : grid_for(n + 1, 256), 256, 0, st>>>(
+            r.in_off.as<int64_t>(), n, w.as<int64_t>());
+        PR_TRY(cub_run(ctx, [&](void *t, size_t &bytes) {
+            return cub::DeviceScan::ExclusiveSum(t, bytes, w.as<int64_t>(), cum.as<int64_t>(), (int)(n + 1), st);
+        }));
+        k_part_bounds<<<1, 32, 0, st>>>(cum.as<int64_t>(), n, parts, db.as<int64_t>());
+        PR_CUDA(cudaMemcpyAsync(b, db.ptr, 8 * (parts + 1), cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+    }
+    int64_t slot = 1;
+    for (int k = 0; k < parts; ++k) slot = b[k + 1] - b[k] > slot ? b[k + 1] - b[k] : slot;
+    const int64_t lo = b[rank], hi = b[rank + 1], owned = hi - lo;
+    int64_t e_lo = 0, e_hi = 0;
+    PR_CUDA(cudaMemcpyAsync(&e_lo, r.in_off.as<int64_t>() + lo, 8, cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaMemcpyAsync(&e_hi, r.in_off.as<int64_t>() + hi, 8, cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaStreamSynchronize(st));
+    const int64_t edges = e_hi - e_lo;
+    Part *P = new Part();
+    P->ctx = &ctx;
+    P->owned = owned;
+    P->slot = slot;
+    P->edges = edges;
+    P->algorithm = algorithm;
+    P->c = c;
+    P->xi = xi;
+    int rc = PR_OK;
+    do {
+        const int64_t k1 = owned ? owned : 1;
+        if ((rc = ensure(P->in_off, 8 * (owned + 1)))) break;
+        if ((rc = ensure(P->in_src, 4 * (edges ? edges : 1)))) break;
+        if ((rc = ensure(P->deg, 4 * k1)) || (rc = ensure(P->row_len, 4 * k1)) || (rc = ensure(P->dtc, 4 * k1)) ||
+            (rc = ensure(P->dang, k1)) || (rc = ensure(P->recv, k1)))
+            break;
+        const unsigned gv = grid_for(owned + 1, 256) > 4096 ? 4096 : grid_for(owned + 1, 256);
+        k_part_rows<<<gv, 256, 0, st>>>(r.in_off.as<int64_t>(), lo, owned, P->in_off.as<int64_t>());
+        PadMap map;
+        for (int k = 0; k <= PR_MAX_PEERS; ++k) map.b[k] = k <= parts ? b[k] : n;
+        map.parts = parts;
+        map.slot = slot;
+        if (edges)
+            k_part_sources<<<grid_for(edges, 256) > 65535 ? 65535 : grid_for(edges, 256), 256, 0, st>>>(
+                r.in_src.as<int32_t>(), e_lo, edges, map, P->in_src.as<int32_t>());
+        if (owned)
+            k_part_vertex<<<gv, 256, 0, st>>>(r.out_deg.as<int32_t>(), r.dtc.as<int32_t>(), lo, owned,
+                                              algorithm == PR_ALGO_IFP2, P->deg.as<int32_t>(),
+                                              P->row_len.as<int32_t>(), P->dtc.as<int32_t>(), P->dang.as<uint8_t>(),
+                                              P->recv.as<uint8_t>());
+        if ((rc = ensure(P->h, 8 * k1)) || (rc = ensure(P->reserved, 8 * k1)) || (rc = ensure(P->act, k1))) break;
+        if ((rc = ensure(P->partials, sizeof(Partial) * (grid_for(owned, 256) +
+                                                         (int64_t)ctx.sm_count * 4 * PR_MAX_SECTIONS + 1))))
+            break;
+        if ((rc = ensure(P->stats, sizeof(Partial) + 32 + 8 * PR_MAX_SECTIONS + 16))) break;
+        P->unit_ctr = (unsigned long long *)(P->stats.as<char>() + sizeof(Partial) + 32);
+        P->done = (unsigned *)(P->unit_ctr + PR_MAX_SECTIONS);
+        cudaMemsetAsync(P->unit_ctr, 0, 8 * PR_MAX_SECTIONS + 16, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess)
+            rc = fail(PR_ERR_CUDA, "partition build");
+    } while (0);
+    if (rc) {
+        delete P;
+        return rc;
+    }
+    P->parts = parts;
+    P->rank = rank;
+    if (bounds_out)
+        for (int k = 0; k <= parts; ++k) bounds_out[k] = b[k];
+    *out = P;
+    return PR_OK;
+}
+
+__global__ void k_part_widen(const int32_t *__restrict__ a, int64_t count, int64_t *__restrict__ out) {
+    GRID_STRIDE(i, count) out[i] = a[i];
+}
+
+// the partition's rows as host arrays in partition_graph's layout (int64
+// offsets / padded sources / degrees, uint8 flags); any pointer may be NULL
+int part_export_rows(Part &P, int64_t *in_off, int64_t *in_src, int64_t *deg, int64_t *row_len, int64_t *dtc,
+                     uint8_t *dang, uint8_t *recv) {
+    Ctx &ctx = *P.ctx;
+    cudaStream_t st = ctx.stream;
+    const int64_t k = P.owned, m = P.edges;
+    DevBuf wide;
+    PR_TRY(ensure(wide, 8 * ((m > k ? m : k) + 1)));
+    if (in_off) PR_CUDA(cudaMemcpyAsync(in_off, P.in_off.ptr, 8 * (k + 1), cudaMemcpyDeviceToHost, st));
+    auto widen = [&](const DevBuf &src, int64_t count, int64_t *dst) -> int {
+        if (!dst || !count) return PR_OK;
+        k_part_widen<<<grid_for(count, 256) > 65535 ? 65535 : grid_for(count, 256), 256, 0, st>>>(src.as<int32_t>(), count,
+                                                                                         wide.as<int64_t>());
+        PR_CUDA(cudaMemcpyAsync(dst, wide.ptr, 8 * count, cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+        return PR_OK;
+    };
+    PR_TRY(widen(P.in_src, m, in_src));
+    PR_TRY(widen(P.deg, k, deg));
+    PR_TRY(widen(P.row_len, k, row_len));
+    PR_TRY(widen(P.dtc, k, dtc));
+    if (dang && k) PR_CUDA(cudaMemcpyAsync(dang, P.dang.ptr, k, cudaMemcpyDeviceToHost, st));
+    if (recv && k) PR_CUDA(cudaMemcpyAsync(recv, P.recv.ptr, k, cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaStreamSynchronize(st));
+    return PR_OK;
+}
+
+int part_sizes(Part &P, int64_t *owned, int64_t *slot, int64_t *edges) {
+    if (owned) *owned = P.owned;
+    if (slot) *slot = P.slot;
+    if (edges) *edges = P.edges;
+    return PR_OK;
+}
+
 __global__ void k_ids_identity(const int32_t *ids, int64_t count, unsigned long long *bad) {
     GRID_STRIDE(i, count) if (ids[i] != (int32_t)i) atomicAdd(bad, 1ull);
 }

@@ -149,6 +149,80 @@ def partition_graph(g, parts: int, rank: int, algorithm: str = "ifp1", order: np
 
 
 @dataclass
+class DevicePartition:
+    """A rank's partition built on the device (``pr_part_from_graph``): the
+    metadata of ``Partition`` without the host arrays, and the library
+    handle of the device-resident rows (CudaLocalStep takes it over)."""
+
+    rank: int
+    parts: int
+    n: int
+    bounds: np.ndarray          # run-layout boundaries [parts+1]
+    slot: int
+    lo: int
+    hi: int
+    algorithm: str
+    damping: float
+    threshold: float
+    handle: object = None
+
+    @property
+    def owned(self) -> int:
+        return self.hi - self.lo
+
+    def to_host(self) -> Partition:
+        """The rows as a host ``Partition`` (pr_part_export_rows), e.g. to
+        upload them again through pr_part_create or to compare with
+        partition_graph.  Needs the handle (before a CudaLocalStep takes it)."""
+        import ctypes
+
+        from . import _lib
+        L = _lib.load()
+        e = ctypes.c_int64()
+        _lib.check(L.pr_part_sizes(self.handle, None, None, ctypes.byref(e)), "pr_part_sizes")
+        k, m = self.owned, int(e.value)
+        arr = {"off": np.empty(k + 1, np.int64), "src": np.empty(max(m, 1), np.int64),
+               "deg": np.empty(max(k, 1), np.int64), "len": np.empty(max(k, 1), np.int64),
+               "dtc": np.empty(max(k, 1), np.int64), "dang": np.empty(max(k, 1), np.uint8),
+               "recv": np.empty(max(k, 1), np.uint8)}
+        _lib.check(L.pr_part_export_rows(self.handle, *[_lib.ptr(arr[x]) for x in
+                                                        ("off", "src", "deg", "len", "dtc", "dang", "recv")]),
+                   "pr_part_export_rows")
+        return Partition(rank=self.rank, parts=self.parts, n=self.n, bounds=self.bounds, slot=self.slot, lo=self.lo,
+                         hi=self.hi, in_offsets=arr["off"], in_sources=arr["src"][:m], out_degree=arr["deg"][:k],
+                         row_len=arr["len"][:k], dtc=arr["dtc"][:k], dangling=arr["dang"][:k].astype(bool),
+                         receives=arr["recv"][:k].astype(bool))
+
+    def release(self) -> None:
+        """Destroy the device rows if no local step took them."""
+        if self.handle is not None:
+            from . import _lib
+            _lib.load().pr_part_destroy(self.handle)
+            self.handle = None
+
+
+def partition_device(g, parts: int, rank: int, algorithm: str, damping: float, threshold: float) -> DevicePartition:
+    """``partition_graph(g, parts, rank, algorithm, order=run_order(...))``
+    built on the graph's device from its run layout (csrc/part.cu
+    part_from_graph): no host export of the graph -- what every rank of the
+    C5 bench does with its own copy of the graph."""
+    import ctypes
+
+    from . import _lib
+    from .graph import device_graph
+    dev = device_graph(g)
+    bounds = np.zeros(parts + 1, np.int64)
+    h = ctypes.c_void_p()
+    _lib.check(_lib.load().pr_part_from_graph(dev.handle, int(parts), int(rank), _lib.ALGO[algorithm],
+                                              float(damping), float(threshold), _lib.ptr(bounds), ctypes.byref(h)),
+               "pr_part_from_graph")
+    slot = max(int(np.max(np.diff(bounds))), 1)
+    return DevicePartition(rank=rank, parts=parts, n=int(g.n), bounds=bounds, slot=slot, lo=int(bounds[rank]),
+                           hi=int(bounds[rank + 1]), algorithm=algorithm, damping=float(damping),
+                           threshold=float(threshold), handle=h)
+
+
+@dataclass
 class RoundRow:
     ints: dict
     floats: dict
@@ -520,6 +594,16 @@ class CudaLocalStep:
         L = _lib.load()
         self.L = L
         k = part.owned
+        if isinstance(part, DevicePartition):
+            # built on the device (pr_part_from_graph): take the handle over
+            if part.handle is None:
+                raise ValueError("device partition already taken by another local step")
+            if (part.algorithm, part.damping, part.threshold) != (algorithm, float(damping), float(threshold)):
+                raise ValueError("device partition was built for another algorithm / damping / threshold")
+            self.h, part.handle = part.handle, None
+            self.s_full = torch.zeros(part.slot * part.parts, dtype=torch.float64, device=self.dev)
+            self.s_mine = torch.zeros(part.slot, dtype=torch.float64, device=self.dev)
+            return
         arr = {
             "off": np.ascontiguousarray(part.in_offsets, np.int64),
             "src": np.ascontiguousarray(part.in_sources if part.in_sources.size else np.zeros(1), np.int64),
@@ -694,7 +778,7 @@ class CudaLocalStep:
 
 
 def run_emulated(g, parts: int, algorithm: str, damping: float = 0.85, threshold: float = 1e-10,
-                 fused: bool = True, device: int = 0, max_rounds: int = 1_000_000):
+                 fused: bool = True, device: int = 0, max_rounds: int = 1_000_000, build: str = "host"):
     """The partitioned fast path with ``parts`` ranks emulated in one process
     on one device (B200_PROFILING.md: ranks sharing a GPU must not wait on
     each other): every rank's round is its own launch on the shared library
@@ -702,11 +786,16 @@ def run_emulated(g, parts: int, algorithm: str, damping: float = 0.85, threshold
     previous one.  ``fused``: shares stored into every rank's replica by the
     round kernel (pr_part_set_peer_ptrs); else each rank's slot of one shared
     full vector (what the all-gather produces).  Returns (values in original
-    ids, rounds).  For tests and smoke checks on a single GPU."""
+    ids, rounds).  ``build="device"``: partitions built on the device from
+    the graph's run layout (pr_part_from_graph) instead of on the host.  For
+    tests and smoke checks on a single GPU."""
     import torch
     n = int(g.n)
     order = run_order(np.diff(np.asarray(g.out_offsets)), np.diff(np.asarray(g.in_offsets)))
-    plist = [partition_graph(g, parts, r, algorithm, order=order) for r in range(parts)]
+    if build == "device":
+        plist = [partition_device(g, parts, r, algorithm, damping, threshold) for r in range(parts)]
+    else:
+        plist = [partition_graph(g, parts, r, algorithm, order=order) for r in range(parts)]
     steps = [CudaLocalStep(p, damping, threshold, algorithm, device=device, fast=True) for p in plist]
     S = plist[0].slot
     dev = torch.device("cuda", device)

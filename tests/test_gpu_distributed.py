@@ -152,3 +152,92 @@ def test_rank_local_gauss_seidel_emulated(sections, algorithm, monkeypatch):
     assert np.array_equal(top(fused), top(o.values))
     assert abs(fused.sum() - 1.0) <= 1e-12
     assert r1 < o.iterations, (r1, o.iterations)
+
+
+def _worker_ipc(rank, world, port, algorithm, fused, q):
+    """One rank of a real multi-process run on cuda:0: the partition built on
+    the device from the rank's own device graph (pr_part_from_graph), the
+    shares exchanged through CUDA IPC peer mappings of the other process's
+    replicas (pr_part_share_buffers / pr_part_set_peers ->
+    cudaIpcOpenMemHandle) or the all-gather; gloo collectives."""
+    import torch.distributed as dist
+    import paper_2302_03245_b200 as P
+    from paper_2302_03245_b200 import distributed as D
+    from paper_2302_03245_b200 import synthetic
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, src, dst = synthetic.make("c2", seed=0)
+        g = P.from_edges(n, src, dst)
+        part = D.partition_device(g, world, rank, algorithm, 0.85, 1e-10)
+        step = D.CudaLocalStep(part, 0.85, 1e-10, algorithm, device=0, fast=True)
+        comm = D.Comm()
+        ok = step.setup_fused(comm) if fused else False
+        vals, rows, info = D.run_partitioned_queued(step, comm, part, algorithm, 0.85, 1e-10, batch=6, fused=ok)
+        if ok:
+            step.close_fused(comm)
+        q.put((rank, ok, part.bounds.tolist(), part.lo, part.hi, vals, info["rounds"]))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_ipc(algorithm, fused):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker_ipc, args=(r, 2, port, algorithm, fused, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=900) for _ in range(2)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("algorithm", ["ifp2", "ifp1"])
+def test_two_process_ipc_fused_exchange(algorithm):
+    """Two processes, one device, C2: partitions built on the device (bounds
+    identical to the host rule over the run layout), the fused exchange over
+    CUDA IPC mappings between the processes bit-identical to the all-gather
+    form, and the sync twin's fixed point (L1 <= 1e-9, identical top-100)."""
+    from paper_2302_03245_b200 import distributed as D
+    from paper_2302_03245_b200 import synthetic
+    fused = _run_ipc(algorithm, True)
+    assert all(r[1] for r in fused), "CUDA IPC mapping refused"
+    gathered = _run_ipc(algorithm, False)
+    n, src, dst = synthetic.make("c2", seed=0)
+    g = oracle.from_edges(n, src, dst)
+    order = D.run_order(np.diff(g.out_offsets), np.diff(g.in_offsets))
+    host_bounds = D.edge_balanced_ranges(np.diff(g.in_offsets)[order], 2)
+    assert fused[0][2] == host_bounds.tolist()
+    vals = {}
+    for name, res in (("fused", fused), ("gathered", gathered)):
+        v = np.empty(n)
+        for r in res:
+            v[order[r[3]:r[4]]] = r[5]
+        vals[name] = v
+    assert np.array_equal(vals["fused"], vals["gathered"])
+    o = oracle.sync_simulate(g, algorithm, threshold=1e-10)
+    assert np.abs(vals["fused"] - o.values).sum() <= 1e-9
+    top = lambda v: np.lexsort((np.arange(v.size), -v))[:100]   # noqa: E731
+    assert np.array_equal(top(vals["fused"]), top(o.values))
+
+
+@pytest.mark.parametrize("algorithm", ["ifp2", "ifp1"])
+def test_device_partitions_emulated(algorithm):
+    """Partitions built on the device (pr_part_from_graph) against the host
+    builder, 3 emulated ranks at C2: the same fixed point (L1 <= 1e-9 between
+    the two, identical top-100) and round count."""
+    import paper_2302_03245_b200 as P
+    from paper_2302_03245_b200 import distributed as D
+    from paper_2302_03245_b200 import synthetic
+    n, src, dst = synthetic.make("c2", seed=0)
+    g = P.from_edges(n, src, dst)
+    vd, rd = D.run_emulated(g, 3, algorithm, build="device")
+    vh, rh = D.run_emulated(g, 3, algorithm, build="host")
+    assert np.abs(vd - vh).sum() <= 1e-9 and rd == rh
+    top = lambda v: np.lexsort((np.arange(v.size), -v))[:100]   # noqa: E731
+    assert np.array_equal(top(vd), top(vh))
