@@ -454,7 +454,7 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
     fused = want_fused and step.setup_fused(comm)
 
     def solve(s, host_values=False, fused=fused):
-        vals, rows, info = D.run_partitioned_queued(s, comm, part, args.algo, DAMPING, XI, batch=8,
+        vals, rows, info = D.run_partitioned_queued(s, comm, part, args.algo, DAMPING, XI, batch=16,
                                                     host_values=host_values, fused=fused)
         return vals, info
 
@@ -531,7 +531,7 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
                              if fused else "NCCL all-gather of shares per round"),
                 "partition_build": "on each rank's GPU from its device graph's run layout (pr_part_from_graph)",
                 "note": ("partitioned rounds queued on the device and graph-captured (statistics read back "
-                         "every 8 rounds); local step = binned dense-round gather (k_part_pull); "
+                         "every 16 rounds; rounds queued past termination skip their sweep); local step = binned dense-round gather (k_part_pull); "
                          "all-reduce of 9 statistics per round (the round barrier)")}
         print(json.dumps(line), flush=True)
     if fused:

@@ -296,6 +296,12 @@ int pr_part_from_graph(pr_graph *g, int32_t parts, int32_t rank, int32_t algorit
  * sources[edges], degrees / row lengths / dangling-target counts[owned],
  * uint8 flags[owned]); any output pointer may be NULL. */
 int pr_part_sizes(pr_part *p, int64_t *owned, int64_t *slot, int64_t *edges);
+/* The next fast round (pr_part_round_device fast = 1 / pr_part_round_fused)
+ * reads d_prev_stats9, the previous round's all-reduced statistics row, on
+ * the device and skips its sweep when it shows no active vertex (the state
+ * is final): rounds queued past termination cost a launch, not a sweep.
+ * Applies to one round; NULL clears it. */
+int pr_part_skip_if_done(pr_part *p, const double *d_prev_stats9);
 int pr_part_export_rows(pr_part *p, int64_t *in_offsets, int64_t *in_sources, int64_t *out_degree,
                         int64_t *row_len, int64_t *dangling_target_counts, uint8_t *dangling, uint8_t *receives);
 /* Kernel launches of one fast round (one per Gauss-Seidel section; the

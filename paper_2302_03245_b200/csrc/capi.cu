@@ -70,6 +70,7 @@ int part_from_graph(Graph &g, int parts, int rank, int algorithm, double c, doub
 int part_export_rows(Part &P, int64_t *in_off, int64_t *in_src, int64_t *deg, int64_t *row_len, int64_t *dtc,
                      uint8_t *dang, uint8_t *recv);
 int part_sizes(Part &P, int64_t *owned, int64_t *slot, int64_t *edges);
+int part_skip_if_done(Part &P, const double *d_prev9);
 int part_launches_per_round(Part &P, int *out);
 int part_close_peers(Part &P);
 int part_init_fused(Part &P, double *d_stats9);
@@ -568,6 +569,11 @@ int pr_part_from_graph(pr_graph *g, int32_t parts, int32_t rank, int32_t algorit
 #define PART_ENTER(p)            \
     CHECK_PTR(p, "partition");   \
     PR_TRY(set_device(part_ctx(*(p)->p)))
+
+int pr_part_skip_if_done(pr_part *p, const double *d_prev_stats9) {
+    PART_ENTER(p);
+    return part_skip_if_done(*p->p, d_prev_stats9);
+}
 
 int pr_part_sizes(pr_part *p, int64_t *owned, int64_t *slot, int64_t *edges) {
     PART_ENTER(p);

@@ -75,6 +75,10 @@ struct Part {
     // the replicas of every rank are mapped (set_peers / set_peer_ptrs) and
     // not yet closed: the fused entry points refuse to run otherwise
     bool fused_ready = false;
+    const double *prev9 = nullptr;   // next fast round: skip it if this row shows no active vertex
+    DevBuf cst;               // Partial: statistics of the outside vertices from round 1 on
+    DevBuf big_dang;          // int32: dangling rows with > 32 sources (fast settle: a warp each)
+    int64_t n_big = -1;
     unsigned long long *unit_ctr = nullptr;
     unsigned *done = nullptr;   // last-block counter of the fast round's last section
     ~Part() {
@@ -267,6 +271,17 @@ struct PullSec {
     Partial *stats;          // the reduced statistics
     double *out9;            // and as 9 doubles (may be null)
     unsigned long long *ctr; // unit counters to reset (PR_MAX_SECTIONS)
+    // the previous round's all-reduced statistics (may be null): with no
+    // active vertex anywhere the state is final and this queued round is a
+    // no-op -- skip its sweep (rounds queued past termination in a batch)
+    const double *prev9;
+    // the round's sweep kind regardless of sections (distributed.sweep_kind:
+    // 0 round 0, 1 round 1, 2 later): the owned vertices outside the
+    // schedule (no inflow) are drained in rounds 0 and 1 only -- round 1
+    // clears their round-0 shares -- and their statistics, constant from
+    // then on, are recorded in round 1 (*cst) and added in later rounds
+    int round_kind;
+    Partial *cst;
 };
 
 template <bool STREAM, bool PREFETCH, int SRC>
@@ -288,19 +303,32 @@ template <bool STREAM, bool PREFETCH>
 __global__ void __launch_bounds__(256, PREFETCH ? 3 : 4) k_part_pull(PartArgs A, BinView T, const int32_t *outside,
                                                                     int64_t n_outside, const PullSec S,
                                                                     const ShareOut s_mine) {
+    if (S.prev9 && S.prev9[3] == 0.0) {
+        // terminated: leave the state as it is; a zero statistics row (never
+        // read: the host stops at the previous one)
+        if (S.last && blockIdx.x == 0 && threadIdx.x < 9 && S.out9) S.out9[threadIdx.x] = 0.0;
+        return;
+    }
     Partial p;
     zero(p);
     if (S.kind == 0) part_bins<STREAM, PREFETCH, 0>(A, T, S, s_mine, p);
     else if (S.kind == 1) part_bins<STREAM, PREFETCH, 2>(A, T, S, s_mine, p);
     else part_bins<STREAM, PREFETCH, 1>(A, T, S, s_mine, p);
-    if (S.last)
+    Partial q;   // the outside vertices' share of the statistics
+    zero(q);
+    if (S.last && S.round_kind < 2)
         for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_outside;
              i += (int64_t)gridDim.x * blockDim.x)
-            part_finish(A, part_load(A, __ldg(&outside[i])), 0.0, s_mine, p);
+            part_finish(A, part_load(A, __ldg(&outside[i])), 0.0, s_mine, q);
+    add(p, q);
     if (s_mine.n) __threadfence_system();   // peer stores performed before the round's barrier
     block_reduce(p);
     if (threadIdx.x == 0) A.partials[(int64_t)S.region * gridDim.x + blockIdx.x] = p;
     if (!S.last) return;
+    if (S.round_kind == 1) {
+        block_reduce(q);
+        if (threadIdx.x == 0) A.partials[(int64_t)PR_MAX_SECTIONS * gridDim.x + blockIdx.x] = q;
+    }
     __shared__ bool is_last;
     if (threadIdx.x == 0) {
         __threadfence();
@@ -314,7 +342,16 @@ __global__ void __launch_bounds__(256, PREFETCH ? 3 : 4) k_part_pull(PartArgs A,
     const int64_t total = (int64_t)(S.region + 1) * gridDim.x;
     for (int64_t b = threadIdx.x; b < total; b += blockDim.x) add(acc, load_partial(A.partials + b));
     block_reduce(acc);
+    if (S.round_kind == 1) {
+        Partial c;
+        zero(c);
+        for (int64_t b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+            add(c, load_partial(A.partials + (int64_t)PR_MAX_SECTIONS * gridDim.x + b));
+        block_reduce(c);
+        if (threadIdx.x == 0) *S.cst = c;
+    }
     if (threadIdx.x == 0) {
+        if (S.round_kind >= 2) add(acc, *S.cst);
         *S.stats = acc;
         if (S.out9) {
             S.out9[0] = acc.l1;
@@ -367,6 +404,62 @@ __global__ void __launch_bounds__(256) k_part_settle(PartArgs A, const double *_
             p.push_ops = A.in_off[v + 1] - A.in_off[v];
             A.reserved[v] = __dadd_rn(A.h[v], acc);
             A.h[v] = 0.0;
+        }
+        const double hv = A.h[v];
+        const bool above = hv > A.xi, scan = !A.dang[v];
+        p.l1 = hv;
+        if (above) {
+            p.above = hv;
+            if (scan) p.nd_above = hv;
+        } else {
+            p.conv_all = 1;
+            if (scan) p.conv_scan = 1;
+        }
+    }
+    block_reduce(p);
+    if (threadIdx.x == 0) A.partials[blockIdx.x] = p;
+}
+
+// The settle of the fast local step, as the engine's (rounds.cu
+// k_settle_fast): every dangling row with more than 32 sources gets a warp of
+// its own (8 gathers in flight per lane, fixed shuffle tree), launched first
+// over the list of those rows; then a thread per owned vertex sums the short
+// rows (8 in flight, ascending) and reduces the statistics.  Deterministic;
+// k_part_settle keeps the sequential ascending-source sums of the exact form.
+struct BigDang {
+    const int64_t *in_off;
+    const uint8_t *dang;
+    __host__ __device__ bool operator()(int32_t v) const { return dang[v] && in_off[v + 1] - in_off[v] > 32; }
+};
+
+__global__ void __launch_bounds__(256) k_part_settle_big(PartArgs A, const double *__restrict__ x_full,
+                                                         const int32_t *__restrict__ big, int64_t n_big) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n_big; i += nwarps) {
+        const int32_t v = big[i];
+        const double acc = span_sum_warp<false, 0>(A.in_src, A.in_off[v], A.in_off[v + 1], Src{x_full, x_full, 0, 0});
+        if (lane == 0) {
+            A.reserved[v] = __dadd_rn(A.h[v], acc);
+            A.h[v] = 0.0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_part_settle_fast(PartArgs A, const double *__restrict__ x_full) {
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    Partial p;
+    zero(p);
+    if (v < A.owned) {
+        if (A.dang[v]) {
+            const int64_t lo = A.in_off[v], hi = A.in_off[v + 1];
+            p.push_ops = hi - lo;
+            if (hi - lo <= 32) {   // longer rows: k_part_settle_big
+                const double acc = row_sum_thread<false, 0>(A.in_src, lo, hi, Src{x_full, x_full, 0, 0});
+                A.reserved[v] = __dadd_rn(A.h[v], acc);
+                A.h[v] = 0.0;
+            }
         }
         const double hv = A.h[v];
         const bool above = hv > A.xi, scan = !A.dang[v];
@@ -505,9 +598,10 @@ int part_create(Ctx &ctx, int64_t owned, int64_t slot, const int64_t *in_off, co
         if ((rc = ensure(P->reserved, 8 * (owned ? owned : 1)))) break;
         if ((rc = ensure(P->act, owned ? owned : 1))) break;
         if ((rc = ensure(P->partials, sizeof(Partial) * (grid_for(owned, 256) +
-                                                         (int64_t)ctx.sm_count * 4 * PR_MAX_SECTIONS + 1))))
+                                                         (int64_t)ctx.sm_count * 4 * (PR_MAX_SECTIONS + 1) + 1))))
             break;
         if ((rc = ensure(P->stats, sizeof(Partial) + 32 + 8 * PR_MAX_SECTIONS + 16))) break;
+        if ((rc = ensure(P->cst, sizeof(Partial)))) break;
         P->unit_ctr = (unsigned long long *)(P->stats.as<char>() + sizeof(Partial) + 32);
         P->done = (unsigned *)(P->unit_ctr + PR_MAX_SECTIONS);
         cudaMemsetAsync(P->unit_ctr, 0, 8 * PR_MAX_SECTIONS + 16, ctx.stream);
@@ -658,9 +752,10 @@ int part_from_graph(Graph &g_in, int parts, int rank, int algorithm, double c, d
                                               P->recv.as<uint8_t>());
         if ((rc = ensure(P->h, 8 * k1)) || (rc = ensure(P->reserved, 8 * k1)) || (rc = ensure(P->act, k1))) break;
         if ((rc = ensure(P->partials, sizeof(Partial) * (grid_for(owned, 256) +
-                                                         (int64_t)ctx.sm_count * 4 * PR_MAX_SECTIONS + 1))))
+                                                         (int64_t)ctx.sm_count * 4 * (PR_MAX_SECTIONS + 1) + 1))))
             break;
         if ((rc = ensure(P->stats, sizeof(Partial) + 32 + 8 * PR_MAX_SECTIONS + 16))) break;
+        if ((rc = ensure(P->cst, sizeof(Partial)))) break;
         P->unit_ctr = (unsigned long long *)(P->stats.as<char>() + sizeof(Partial) + 32);
         P->done = (unsigned *)(P->unit_ctr + PR_MAX_SECTIONS);
         cudaMemsetAsync(P->unit_ctr, 0, 8 * PR_MAX_SECTIONS + 16, st);
@@ -916,6 +1011,9 @@ static void launch_part_pull(Part &P, const double *s_full, const double *x_new,
         S.stats = P.stats.as<Partial>();
         S.out9 = out9;
         S.ctr = P.unit_ctr;
+        S.prev9 = P.prev9;
+        S.round_kind = kind;
+        S.cst = P.cst.as<Partial>();
         BinView T = part_view(P);
         T.unit_ctr = P.unit_ctr + k;
         if (P.stream_csc) {
@@ -926,6 +1024,7 @@ static void launch_part_pull(Part &P, const double *s_full, const double *x_new,
             else k_part_pull<false, false><<<g, 256, 0, st>>>(args_of(P), T, out, no, S, so);
         }
     }
+    P.prev9 = nullptr;   // one round only
 }
 
 // ---- fused exchange: share replicas in peer memory ----------------------
@@ -978,6 +1077,11 @@ int part_launches_per_round(Part &P, int *out) {
 
 // this partition's place among the ranks (the padded slot it owns: the
 // rank-local Gauss-Seidel test and the fused exchange's store offset)
+int part_skip_if_done(Part &P, const double *d_prev9) {
+    P.prev9 = d_prev9;
+    return PR_OK;
+}
+
 int part_set_rank(Part &P, int parts, int rank) {
     if (parts < 1 || parts > PR_MAX_PEERS || rank < 0 || rank >= parts)
         return fail(PR_ERR_ARG, "partition: need 1 <= parts <= 8 and 0 <= rank < parts");
@@ -1093,7 +1197,27 @@ int part_settle_shares(Part &P, double *d_x_mine) {
 
 int part_settle(Part &P, const double *d_x_full, int64_t *settled, int64_t *ints, double *floats) {
     unsigned g = grid_for(P.owned, 256);
-    k_part_settle<<<g, 256, 0, P.ctx->stream>>>(args_of(P), d_x_full);
+    cudaStream_t st = P.ctx->stream;
+    if (P.sg) {
+        if (P.n_big < 0) {
+            DevBuf cnt;
+            PR_TRY(ensure(cnt, 8));
+            PR_TRY(ensure(P.big_dang, 4 * (P.owned > 0 ? P.owned : 1)));
+            auto first = thrust::make_counting_iterator<int32_t>(0);
+            PR_TRY(cub_run(*P.ctx, [&](void *t, size_t &b) {
+                return cub::DeviceSelect::If(t, b, first, P.big_dang.as<int32_t>(), cnt.as<int64_t>(), (int)P.owned,
+                                             BigDang{P.in_off.as<int64_t>(), P.dang.as<uint8_t>()}, st);
+            }));
+            PR_CUDA(cudaMemcpyAsync(&P.n_big, cnt.ptr, 8, cudaMemcpyDeviceToHost, st));
+            PR_CUDA(cudaStreamSynchronize(st));
+        }
+        if (P.n_big > 0)
+            k_part_settle_big<<<grid_for(P.n_big * 32, 256) > 4096 ? 4096 : grid_for(P.n_big * 32, 256), 256, 0, st>>>(
+                args_of(P), d_x_full, P.big_dang.as<int32_t>(), P.n_big);
+        k_part_settle_fast<<<g, 256, 0, st>>>(args_of(P), d_x_full);
+    } else {
+        k_part_settle<<<g, 256, 0, st>>>(args_of(P), d_x_full);
+    }
     int64_t tmp[6];
     PR_TRY(finish_stats(P, g, tmp, floats));
     if (settled) *settled = tmp[2];

@@ -239,6 +239,9 @@ class Comm:
         import torch.distributed as dist
         self.torch, self.dist = torch, dist
         self.device = device
+        # one rank: every collective is the identity (all-gather of the own
+        # slice into itself, sum over one rank) -- issue none
+        self.solo = dist.get_world_size() == 1
 
     def _staged(self, t) -> bool:
         # gloo has no CUDA all-gather: device tensors go through host copies
@@ -246,6 +249,8 @@ class Comm:
 
     def allgather_slots(self, full, mine_view) -> None:
         # `mine_view` aliases this rank's slice of `full`: in-place all-gather
+        if self.solo:
+            return
         if self._staged(full):
             host = full.cpu()
             self.dist.all_gather_into_tensor(host, mine_view.cpu())
@@ -255,6 +260,8 @@ class Comm:
 
     def allreduce_row(self, row) -> None:
         """In-place sum of a statistics row (device or host tensor)."""
+        if self.solo:
+            return
         if self._staged(row):
             host = row.cpu()
             self.dist.all_reduce(host)
@@ -398,9 +405,15 @@ def run_partitioned_queued(step, comm, part: Partition, algorithm: str, damping:
                 step._queued = cache
         full, mine, stats = cache["full"], cache["mine"], cache["stats"]
 
+        skip = getattr(step, "skip_if_done", None)
+
         def queue_batch(nb, t0):
             for j in range(nb):
                 tt = t0 + j
+                # a round queued past termination skips its sweep on the device
+                # (the previous round's all-reduced row shows no active vertex)
+                if skip is not None and (j > 0 or t0 > 0):
+                    skip(stats[j - 1] if j > 0 else stats[batch - 1])
                 if fused:
                     step.round_fused(tt, stats[j])
                 else:
@@ -735,6 +748,13 @@ class CudaLocalStep:
     def init_fused(self, stats_row):
         self._lib.check(self.L.pr_part_init_fused(self.h, self._ct.c_void_p(stats_row.data_ptr())),
                         "pr_part_init_fused")
+
+    def skip_if_done(self, prev_row):
+        """The next fast round skips its sweep if ``prev_row`` (the previous
+        round's all-reduced statistics, device memory) has no active vertex."""
+        if self.fast:
+            self._lib.check(self.L.pr_part_skip_if_done(self.h, self._ct.c_void_p(prev_row.data_ptr())),
+                            "pr_part_skip_if_done")
 
     def round_fused(self, t: int, stats_row):
         self._lib.check(self.L.pr_part_round_fused(self.h, int(t) & 1, sweep_kind(t),
