@@ -527,8 +527,11 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
                 "gpu_launches": int((step.launches_per_round() * info.get("queued_rounds", info["rounds"]) + 6)
                                     * args.steps),
                 "clocks": clocks.summary(),
-                "exchange": ("fused: round kernel stores shares into every rank's replica (peer memory)"
-                             if fused else "NCCL all-gather of shares per round"),
+                "exchange": ("fused: the round kernel stores each share into the replicas of the ranks that read "
+                             "it (peer memory; sparse boundary exchange)" if fused
+                             else "NCCL all-gather of shares per round"),
+                "exchange_entries_per_round": {"sparse": step.exchange_entries(),
+                                               "dense": int(part.owned) * world},
                 "partition_build": "on each rank's GPU from its device graph's run layout (pr_part_from_graph)",
                 "note": ("partitioned rounds queued on the device and graph-captured (statistics read back "
                          "every 16 rounds; rounds queued past termination skip their sweep); local step = binned dense-round gather (k_part_pull); "

@@ -302,6 +302,12 @@ int pr_part_sizes(pr_part *p, int64_t *owned, int64_t *slot, int64_t *edges);
  * is final): rounds queued past termination cost a launch, not a sweep.
  * Applies to one round; NULL clears it. */
 int pr_part_skip_if_done(pr_part *p, const double *d_prev_stats9);
+/* Shares the fused exchange sends per dense round at most: the sum over
+ * owned vertices of the ranks reading each (a partition built by
+ * pr_part_from_graph with parts > 1 stores a vertex's share only into the
+ * replicas of ranks that have one of its out-edges -- the sparse boundary
+ * exchange, PUSHRANK_SPARSE_EXCHANGE=0 disables it); owned * parts otherwise. */
+int pr_part_exchange_entries(pr_part *p, int64_t *entries);
 int pr_part_export_rows(pr_part *p, int64_t *in_offsets, int64_t *in_sources, int64_t *out_degree,
                         int64_t *row_len, int64_t *dangling_target_counts, uint8_t *dangling, uint8_t *receives);
 /* Kernel launches of one fast round (one per Gauss-Seidel section; the

@@ -127,6 +127,7 @@ SIGNATURES = {
     "pr_part_from_graph": (ctypes.c_int, [c_vp, c_i32, c_i32, c_i32, c_f64, c_f64, c_vp, _PP]),
     "pr_part_sizes": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "pr_part_skip_if_done": (ctypes.c_int, [c_vp, c_vp]),
+    "pr_part_exchange_entries": (ctypes.c_int, [c_vp, c_vp]),
     "pr_part_export_rows": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pr_part_launches_per_round": (ctypes.c_int, [c_vp, ctypes.POINTER(c_i32)]),
     "pr_part_init_fused": (ctypes.c_int, [c_vp, c_vp]),

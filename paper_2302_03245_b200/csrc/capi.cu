@@ -71,6 +71,7 @@ int part_export_rows(Part &P, int64_t *in_off, int64_t *in_src, int64_t *deg, in
                      uint8_t *dang, uint8_t *recv);
 int part_sizes(Part &P, int64_t *owned, int64_t *slot, int64_t *edges);
 int part_skip_if_done(Part &P, const double *d_prev9);
+int part_exchange_entries(Part &P, int64_t *entries);
 int part_launches_per_round(Part &P, int *out);
 int part_close_peers(Part &P);
 int part_init_fused(Part &P, double *d_stats9);
@@ -573,6 +574,12 @@ int pr_part_from_graph(pr_graph *g, int32_t parts, int32_t rank, int32_t algorit
 int pr_part_skip_if_done(pr_part *p, const double *d_prev_stats9) {
     PART_ENTER(p);
     return part_skip_if_done(*p->p, d_prev_stats9);
+}
+
+int pr_part_exchange_entries(pr_part *p, int64_t *entries) {
+    PART_ENTER(p);
+    CHECK_PTR(entries, "entries");
+    return part_exchange_entries(*p->p, entries);
 }
 
 int pr_part_sizes(pr_part *p, int64_t *owned, int64_t *slot, int64_t *edges) {

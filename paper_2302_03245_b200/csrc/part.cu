@@ -77,6 +77,8 @@ struct Part {
     bool fused_ready = false;
     const double *prev9 = nullptr;   // next fast round: skip it if this row shows no active vertex
     DevBuf cst;               // Partial: statistics of the outside vertices from round 1 on
+    DevBuf dmask;             // uint8 [owned]: destination ranks of each vertex's out-edges (empty: all)
+    int64_t exch_entries = -1;   // sum over owned vertices of popcount(dmask): shares sent per dense round
     DevBuf big_dang;          // int32: dangling rows with > 32 sources (fast settle: a warp each)
     int64_t n_big = -1;
     unsigned long long *unit_ctr = nullptr;
@@ -95,6 +97,9 @@ struct PartArgs {
     const int32_t *in_src;
     const int32_t *deg, *row_len, *dtc;
     const uint8_t *dang, *recv;
+    // sparse boundary exchange: bit k set iff the vertex has an out-edge into
+    // rank k's range (only those ranks' replicas receive its share); null = all
+    const uint8_t *dmask;
     double *h, *reserved;
     uint8_t *act;
     Partial *partials;
@@ -112,14 +117,14 @@ struct ShareOut {
     double *peer[PR_MAX_PEERS];
     int n;
     int64_t off;   // rank * slot
-    __device__ __forceinline__ void store(int64_t v, double x) const {
+    __device__ __forceinline__ void store(int64_t v, double x, unsigned mask) const {
         if (n == 0) {
             mine[v] = x;
             return;
         }
 #pragma unroll
         for (int k = 0; k < PR_MAX_PEERS; ++k)
-            if (k < n) peer[k][off + v] = x;
+            if (k < n && (mask >> k & 1u)) peer[k][off + v] = x;
     }
 };
 
@@ -130,6 +135,7 @@ struct PartIn {
     int32_t v, dv;
     double h, rv;
     bool act, dang;
+    unsigned mask;   // replicas that receive this vertex's share
 };
 
 __device__ __forceinline__ PartIn part_load(const PartArgs &A, int32_t v) {
@@ -140,6 +146,7 @@ __device__ __forceinline__ PartIn part_load(const PartArgs &A, int32_t v) {
     q.rv = A.reserved[v];
     q.act = A.act[v] != 0;
     q.dang = __ldg(&A.dang[v]) != 0;
+    q.mask = A.dmask ? (unsigned)__ldg(&A.dmask[v]) : 0xFFu;
     return q;
 }
 
@@ -164,14 +171,14 @@ __device__ __forceinline__ void part_finish(const PartArgs &A, const PartIn &q, 
         const int32_t len = __ldg(&A.row_len[v]);
         A.reserved[v] = __dadd_rn(q.rv, hv);
         A.h[v] = hv;
-        out.store(v, len > 0 ? __ddiv_rn(__dmul_rn(A.c, hv), (double)q.dv) : 0.0);
+        out.store(v, len > 0 ? __ddiv_rn(__dmul_rn(A.c, hv), (double)q.dv) : 0.0, q.mask);
         p.nact += 1;
         p.work += (int64_t)q.dv + 1;
         p.push_ops += len;
         p.push_dang += __ldg(&A.dtc[v]);
     } else {
         A.h[v] = hv;
-        out.store(v, 0.0);
+        out.store(v, 0.0, q.mask);
     }
 }
 
@@ -521,6 +528,7 @@ static PartArgs args_of(Part &P) {
     A.dtc = P.dtc.as<int32_t>();
     A.dang = P.dang.as<uint8_t>();
     A.recv = P.recv.as<uint8_t>();
+    A.dmask = P.dmask.ptr ? P.dmask.as<uint8_t>() : nullptr;
     A.h = P.h.as<double>();
     A.reserved = P.reserved.as<double>();
     A.act = P.act.as<uint8_t>();
@@ -682,6 +690,35 @@ __global__ void k_part_vertex(const int32_t *__restrict__ out_deg, const int32_t
     }
 }
 
+// dmask[u - lo] |= 1 << rank(t) for every edge u -> t with u owned (one pass
+// over the run layout's CSC: row t, source u)
+__global__ void k_part_dmask(const int64_t *__restrict__ in_off, const int32_t *__restrict__ in_src, int64_t n,
+                             int64_t m, PadMap map, int64_t lo, int64_t hi, unsigned *__restrict__ mask32) {
+    // edge-parallel (hub rows hold up to ~1e6 edges): an edge whose source
+    // is owned finds its row -- and so the target's rank -- by binary search
+    GRID_STRIDE(e, m) {
+        const int64_t u = in_src[e];
+        if (u < lo || u >= hi) continue;
+        int64_t a = 0, b = n;   // last row t with in_off[t] <= e
+        while (b - a > 1) {
+            const int64_t mid = (a + b) >> 1;
+            if (in_off[mid] <= e) a = mid;
+            else b = mid;
+        }
+        int r = 0;
+        while (r + 1 < map.parts && a >= map.b[r + 1]) ++r;
+        atomicOr(&mask32[u - lo], 1u << r);
+    }
+}
+
+__global__ void k_part_mask8(const unsigned *__restrict__ m32, int64_t owned, uint8_t *__restrict__ m8,
+                             unsigned long long *__restrict__ pop) {
+    GRID_STRIDE(i, owned) {
+        m8[i] = (uint8_t)m32[i];
+        atomicAdd(pop, (unsigned long long)__popc(m32[i]));
+    }
+}
+
 int part_from_graph(Graph &g_in, int parts, int rank, int algorithm, double c, double xi, int64_t *bounds_out,
                     Part **out) {
     if (parts < 1 || parts > PR_MAX_PEERS || rank < 0 || rank >= parts)
@@ -750,6 +787,23 @@ int part_from_graph(Graph &g_in, int parts, int rank, int algorithm, double c, d
                                               algorithm == PR_ALGO_IFP2, P->deg.as<int32_t>(),
                                               P->row_len.as<int32_t>(), P->dtc.as<int32_t>(), P->dang.as<uint8_t>(),
                                               P->recv.as<uint8_t>());
+        // sparse boundary exchange: each vertex's share
+        // goes only to the ranks that read it (PUSHRANK_SPARSE_EXCHANGE=0: all)
+        const char *se = getenv("PUSHRANK_SPARSE_EXCHANGE");
+        if (parts > 1 && !(se && atoi(se) == 0) && owned) {
+            DevBuf m32, pop;
+            if ((rc = ensure(m32, 4 * owned)) || (rc = ensure(pop, 8)) || (rc = ensure(P->dmask, owned))) break;
+            cudaMemsetAsync(m32.ptr, 0, 4 * owned, st);
+            cudaMemsetAsync(pop.ptr, 0, 8, st);
+            k_part_dmask<<<grid_for(r.m, 256) > 65535 ? 65535 : grid_for(r.m, 256), 256, 0, st>>>(
+                r.in_off.as<int64_t>(), r.in_src.as<int32_t>(), n, r.m, map, lo, hi, m32.as<unsigned>());
+            k_part_mask8<<<gv, 256, 0, st>>>(m32.as<unsigned>(), owned, P->dmask.as<uint8_t>(),
+                                             pop.as<unsigned long long>());
+            unsigned long long np = 0;
+            cudaMemcpyAsync(&np, pop.ptr, 8, cudaMemcpyDeviceToHost, st);
+            if (cudaStreamSynchronize(st) != cudaSuccess) { rc = fail(PR_ERR_CUDA, "partition exchange mask"); break; }
+            P->exch_entries = (int64_t)np;
+        }
         if ((rc = ensure(P->h, 8 * k1)) || (rc = ensure(P->reserved, 8 * k1)) || (rc = ensure(P->act, k1))) break;
         if ((rc = ensure(P->partials, sizeof(Partial) * (grid_for(owned, 256) +
                                                          (int64_t)ctx.sm_count * 4 * (PR_MAX_SECTIONS + 1) + 1))))
@@ -803,6 +857,11 @@ int part_export_rows(Part &P, int64_t *in_off, int64_t *in_src, int64_t *deg, in
     if (dang && k) PR_CUDA(cudaMemcpyAsync(dang, P.dang.ptr, k, cudaMemcpyDeviceToHost, st));
     if (recv && k) PR_CUDA(cudaMemcpyAsync(recv, P.recv.ptr, k, cudaMemcpyDeviceToHost, st));
     PR_CUDA(cudaStreamSynchronize(st));
+    return PR_OK;
+}
+
+int part_exchange_entries(Part &P, int64_t *entries) {
+    *entries = P.exch_entries >= 0 ? P.exch_entries : (int64_t)P.owned * (P.parts > 0 ? P.parts : 1);
     return PR_OK;
 }
 

@@ -749,6 +749,14 @@ class CudaLocalStep:
         self._lib.check(self.L.pr_part_init_fused(self.h, self._ct.c_void_p(stats_row.data_ptr())),
                         "pr_part_init_fused")
 
+    def exchange_entries(self) -> int:
+        """Shares the fused exchange stores per dense round at most (the sparse
+        boundary exchange of a device-built partition; owned * parts when
+        every replica receives every share)."""
+        e = self._ct.c_int64()
+        self._lib.check(self.L.pr_part_exchange_entries(self.h, self._ct.byref(e)), "pr_part_exchange_entries")
+        return int(e.value)
+
     def skip_if_done(self, prev_row):
         """The next fast round skips its sweep if ``prev_row`` (the previous
         round's all-reduced statistics, device memory) has no active vertex."""

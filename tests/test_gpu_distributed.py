@@ -239,5 +239,13 @@ def test_device_partitions_emulated(algorithm):
     vd, rd = D.run_emulated(g, 3, algorithm, build="device")
     vh, rh = D.run_emulated(g, 3, algorithm, build="host")
     assert np.abs(vd - vh).sum() <= 1e-9 and rd == rh
+    # device partitions carry the sparse exchange masks: the fused stores
+    # reach only the replicas that read a share, and the result is still
+    # bit-identical to the all-gather form
+    vg, rg = D.run_emulated(g, 3, algorithm, build="device", fused=False)
+    assert np.array_equal(vd, vg) and rd == rg
+    part = D.partition_device(g, 3, 1, algorithm, 0.85, 1e-10)
+    step = D.CudaLocalStep(part, 0.85, 1e-10, algorithm, device=0, fast=True)
+    assert 0 < step.exchange_entries() < 3 * part.owned
     top = lambda v: np.lexsort((np.arange(v.size), -v))[:100]   # noqa: E731
     assert np.array_equal(top(vd), top(vh))
