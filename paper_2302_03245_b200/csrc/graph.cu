@@ -782,8 +782,13 @@ int ensure_run_layout(Graph &g) {
     {
         const double l2 = (double)(ctx.l2_bytes ? ctx.l2_bytes : (size_t)126 << 20);
         bool sort_rows = 4.0 * (double)m + 8.0 * (double)n > 16.0 * l2;
-        if (const char *e = getenv("PUSHRANK_SORT_ROWS")) sort_rows = atoi(e) != 0;
-        if (!rc && sort_rows) rc = sort_csc_rows(ctx, r->in_off, r->in_src, n, m);
+        // PUSHRANK_SORT_ROWS=0/1 forces it off / on now; by default it waits
+        // for the graph's second fast solve (run_rounds)
+        if (const char *e = getenv("PUSHRANK_SORT_ROWS")) {
+            if (!rc && atoi(e) != 0) rc = sort_csc_rows(ctx, r->in_off, r->in_src, n, m);
+        } else {
+            r->sort_deferred = sort_rows;
+        }
     }
     DevBuf len;
     if (!rc) rc = ensure(len, 8 * (n + 1));

@@ -1145,6 +1145,18 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
         phase_mark(ctx.stream, "run: layout");
     }
     Graph &g = *gp;
+    if (!exact && g.sort_deferred && g.fast_solves >= 1) {
+        // the graph is being reused: sort its rows' sources now and rebuild
+        // the schedules that copied them
+        PR_TRY(sort_csc_rows(ctx, g.in_off, g.in_src, g.n, g.m));
+        g.sort_deferred = false;
+        for (auto &S : g.sched) {
+            S.built = false;
+            S.unit_blocks = 0;
+            S.nsec = 0;
+        }
+        phase_mark(ctx.stream, "run: deferred row sort");
+    }
     const int32_t *perm = exact ? nullptr : g_in.perm.as<int32_t>();
     if (algo == PR_ALGO_IFP2) {
         PR_TRY(preprocess_ifp2_device(g));
@@ -1506,6 +1518,7 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
         // device-counted solve kernels + the host-launched un-permute copies
         res->launches = (int64_t)hc.launches + (d_reserved ? 1 : 0) + (d_pending ? 1 : 0);
     }
+    if (!exact) g.fast_solves += 1;
     if (hc.done == 2)
         return fail(PR_ERR_NOT_SETTLED,
                     "sync simulation did not settle in " + std::to_string(p.max_rounds) + " iterations");
