@@ -95,7 +95,8 @@ typedef struct pr_run_params {
     /* Optional per-round observer (sync_simulate's on_iteration(t, reserved,
      * pushing), engines.py:453-454).  EXACT mode only.  The device loop runs
      * in batches: every state is snapshotted into a device ring (up to 64
-     * states, ~1 GiB) that the host drains with one copy per batch and then
+     * states, 256 MiB) that the host drains into page-locked memory with one
+     * copy per batch and then
      * calls on_round for each state in order (host_loop = 1: round by round).
      * The host arrays are valid for the duration of the call. */
     void (*on_round)(void *user, int64_t t, const double *reserved, const double *pending);

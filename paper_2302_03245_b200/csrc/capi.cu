@@ -167,6 +167,7 @@ int pr_ctx_destroy(pr_ctx *ctx) {
     release_execs(ctx->c);
     ctx->c.scratch.release();
     ctx->c.flush.release();
+    if (ctx->c.obs_host) cudaFreeHost(ctx->c.obs_host);
     cudaStreamDestroy(ctx->c.stream);
     delete ctx;
     return PR_OK;

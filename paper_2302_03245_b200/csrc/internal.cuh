@@ -74,6 +74,10 @@ struct Ctx {
         uint64_t used = 0;
     } execs[8];
     uint64_t exec_tick = 0;
+    // page-locked host side of the observed-run ring (sync_simulate's
+    // on_iteration): grown on demand, freed with the context
+    void *obs_host = nullptr;
+    size_t obs_host_bytes = 0;
 };
 void release_execs(Ctx &ctx);
 

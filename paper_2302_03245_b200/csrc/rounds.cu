@@ -1341,11 +1341,20 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     PR_CUDA(cudaEventRecord(e0, st));
     int64_t obs_k = 0;
     if (observed) {
-        // ring of K states (reserved | pending), K <= 64, within ~1 GiB
-        obs_k = ((int64_t)1 << 30) / (16 * (n > 0 ? n : 1));
+        // ring of K states (reserved | pending), K <= 64, within 256 MiB,
+        // drained into a page-locked host buffer of the same size
+        obs_k = ((int64_t)1 << 28) / (16 * (n > 0 ? n : 1));
         if (obs_k > 64) obs_k = 64;
         if (obs_k < 1) obs_k = 1;
         PR_TRY(ensure(g.obs_ring, 16 * n * obs_k));
+        const size_t hb = (size_t)(16 * n * obs_k);
+        if (ctx.obs_host_bytes < hb) {
+            if (ctx.obs_host) cudaFreeHost(ctx.obs_host);
+            ctx.obs_host = nullptr;
+            ctx.obs_host_bytes = 0;
+            PR_CUDA(cudaMallocHost(&ctx.obs_host, hb));
+            ctx.obs_host_bytes = hb;
+        }
         A.obs_batch = obs_k;
         A.obs_ring = g.obs_ring.as<double>();
         A.use_graph = 0;
@@ -1383,7 +1392,7 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
         if (!observed) {
             PR_CUDA(cudaGraphLaunch(slot->exec, st));
         } else {
-            std::vector<double> ring((size_t)(2 * n * obs_k));
+            double *ring = static_cast<double *>(ctx.obs_host);
             RunCtl hc;
             for (;;) {
                 PR_CUDA(cudaMemcpyAsync(&hc, A.ctl, sizeof(hc), cudaMemcpyDeviceToHost, st));
@@ -1393,12 +1402,11 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
                 PR_CUDA(cudaMemcpyAsync(&hc, A.ctl, sizeof(hc), cudaMemcpyDeviceToHost, st));
                 PR_CUDA(cudaStreamSynchronize(st));
                 if (hc.obs_count > 0)
-                    PR_CUDA(cudaMemcpyAsync(ring.data(), A.obs_ring, 16 * n * hc.obs_count, cudaMemcpyDeviceToHost,
-                                            st));
+                    PR_CUDA(cudaMemcpyAsync(ring, A.obs_ring, 16 * n * hc.obs_count, cudaMemcpyDeviceToHost, st));
                 PR_CUDA(cudaStreamSynchronize(st));
                 // reference semantics: called after round t's update (engines.py:453-454)
                 for (int64_t j = 0; j < hc.obs_count; ++j)
-                    p.on_round(p.user, hc.obs_t0 + j, ring.data() + 2 * j * n, ring.data() + (2 * j + 1) * n);
+                    p.on_round(p.user, hc.obs_t0 + j, ring + 2 * j * n, ring + (2 * j + 1) * n);
             }
         }
     } else {
