@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=0.0,
                     help="seconds per bounded CPU sample (0: full solves below C5, 6 s at C5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-full", action="store_true",
+                    help="also run one complete CPU solve (all host threads) at C5 for the time-to-solution and "
+                         "pushes-per-solve comparison (minutes of CPU)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--push-switch", type=float, default=0.0,
                     help="AUTO policy: push when the next round's work < this fraction of (E_D+|D|) (0 = library default)")
@@ -413,10 +416,16 @@ def run_ours(args):
                               if budget else f"median of {head['samples']} full solves")),
                 "plan": plan}
             # time-based context beside GTEPS (the engines push different edge counts)
-            if head["complete_solve"]:
-                line["vs_cpu_time_to_solution"] = head["wall_s"] * 1e3 / line["time_to_l1_ms"]
-            line["pushes_per_solve"] = {"ours": int(r0.push_ops), "cpu_reference": head["push_ops"]
-                                        if head["complete_solve"] else None}
+            full = head if head["complete_solve"] else None
+            if full is None and args.cpu_full:
+                # refdriver builds the IFP2 split / dangling-target counts itself
+                ops, wall, comp, kind = _ref_solve(host, args.algo, os.cpu_count() or 1, None, None, None)
+                full = {"wall_s": wall, "push_ops": int(ops), "complete_solve": bool(comp), "kind": kind}
+                plan[f"{args.algo}_k{os.cpu_count() or 1}_full_solve"] = full
+            if full is not None and full["complete_solve"]:
+                line["vs_cpu_time_to_solution"] = full["wall_s"] * 1e3 / line["time_to_l1_ms"]
+            line["pushes_per_solve"] = {"ours": int(r0.push_ops),
+                                        "cpu_reference": full["push_ops"] if full else None}
         except Exception as e:  # baseline failure must not hide the GPU number
             line["cpu_baseline"] = {"value": None, "unit": "GTEPS", "cores": os.cpu_count(), "kind": "port",
                                     "sample": f"failed: {e!r}"}

@@ -272,6 +272,9 @@ constexpr int64_t HUB_CHUNK = PR_HUB_CHUNK;    // edges per hub unit (256 thread
 constexpr int64_t ROW_COST = 8;                // per-row drain cost in edge units (unit sizing)
 constexpr int64_t UNITS_PER_BLOCK = PR_UNITS_PB;  // target work units per block of the persistent grid
 constexpr int64_t LONG_UNIT = 100000;           // edge-units: past this, UNITS_PER_BLOCK per section
+#ifndef PR_MIN_UNIT
+#define PR_MIN_UNIT 10000
+#endif
 
 // PUSHRANK_TIMING=1: host-side phase timings (synchronising) on stderr
 void phase_mark(cudaStream_t st, const char *what);

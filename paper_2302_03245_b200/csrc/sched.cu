@@ -216,7 +216,10 @@ int ensure_units(Graph &g, int which, int64_t blocks, int nsec) {
     // of each section launch is short (C5 4896 -> 4538 us per sweep; C3's
     // short units lose with more of them: 9.9 -> 11.0 ms at 2x)
     if (nsec > 1 && T > LONG_UNIT) T = total / (blocks * UNITS_PER_BLOCK * nsec);
-    if (T < 400 * ROW_COST) T = 400 * ROW_COST;  // >= 3200 edge-units per unit
+    // smallest unit, in edge-units: each unit costs a dispatch barrier, so
+    // L2-resident sweeps want fewer, larger ones (measured against 3200:
+    // 8K C2 -7%, 16K C4 -7%; C3 and C5 units are larger anyway)
+    if (T < PR_MIN_UNIT) T = PR_MIN_UNIT;
     int64_t cnt[PR_MAX_SECTIONS][3];
     int64_t n_units = 0;
     for (int k = 0; k < nsec; ++k) {
