@@ -177,6 +177,9 @@ int pr_write_ranking_csv(pr_ctx *ctx, const double *values, const int64_t *origi
 int pr_format_score(double value, char *out);
 int pr_graph_destroy(pr_graph *g);
 int pr_graph_info(const pr_graph *g, int64_t *n, int64_t *m);
+/* Bytes pr_graph_upload / pr_graph_attach_out_targets copied host -> device
+ * (the int64 index arrays travel partly narrowed to int32 on host threads). */
+int pr_graph_h2d_bytes(const pr_graph *g, int64_t *bytes);
 /* Graph arrays back to the host (int64, reference layout); NULL skips one. */
 int pr_graph_export(pr_graph *g, int64_t *out_offsets, int64_t *out_targets,
                     int64_t *in_offsets, int64_t *in_sources);

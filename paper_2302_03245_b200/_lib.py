@@ -92,6 +92,7 @@ SIGNATURES = {
     "pr_host_free": (ctypes.c_int, [c_vp]),
     "pr_graph_destroy": (ctypes.c_int, [c_vp]),
     "pr_graph_info": (ctypes.c_int, [c_vp, _PI64, _PI64]),
+    "pr_graph_h2d_bytes": (ctypes.c_int, [c_vp, _PI64]),
     "pr_graph_export": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pr_classify": (ctypes.c_int, [c_vp, ctypes.POINTER(ClassCounts)]),
     "pr_classify_export": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),

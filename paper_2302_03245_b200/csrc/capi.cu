@@ -168,6 +168,7 @@ int pr_ctx_destroy(pr_ctx *ctx) {
     ctx->c.scratch.release();
     ctx->c.flush.release();
     if (ctx->c.obs_host) cudaFreeHost(ctx->c.obs_host);
+    uploader_destroy(ctx->c);
     cudaStreamDestroy(ctx->c.stream);
     delete ctx;
     return PR_OK;
@@ -316,6 +317,13 @@ int pr_graph_info(const pr_graph *g, int64_t *n, int64_t *m) {
     CHECK_PTR(g, "graph");
     if (n) *n = g->g->n;
     if (m) *m = g->g->m;
+    return PR_OK;
+}
+
+int pr_graph_h2d_bytes(const pr_graph *g, int64_t *bytes) {
+    CHECK_PTR(g, "graph");
+    CHECK_PTR(bytes, "bytes");
+    *bytes = g->g->h2d_bytes;
     return PR_OK;
 }
 

@@ -731,10 +731,7 @@ int attach_out_targets(Graph &g, const int64_t *out_tgt) {
     cudaStream_t st = ctx.stream;
     PR_TRY(ensure(g.out_tgt, 4 * (g.m ? g.m : 1)));
     if (g.m) {
-        DevBuf stage;
-        PR_TRY(ensure(stage, 8 * g.m));
-        PR_CUDA(cudaMemcpyAsync(stage.ptr, out_tgt, 8 * g.m, cudaMemcpyHostToDevice, st));
-        k_narrow<<<gs_grid(ctx, g.m), 256, 0, st>>>(stage.as<int64_t>(), g.m, g.out_tgt.as<int32_t>());
+        PR_TRY(upload_narrow(ctx, out_tgt, g.m, g.out_tgt.as<int32_t>(), &g.h2d_bytes));
         PR_CUDA(cudaStreamSynchronize(st));
         PR_CUDA(cudaGetLastError());
     }
@@ -941,23 +938,20 @@ int upload_graph(Ctx &ctx, int64_t n, int64_t m, const int64_t *out_off, const i
     g->raw = m;
     g->has_csr = out_tgt != nullptr || m == 0;
     int rc = alloc_graph_arrays(*g);
-    DevBuf stage;
-    if (!rc) rc = ensure(stage, 8 * (m > 0 ? m : 1));
     if (!rc) {
-        cudaError_t e = cudaMemcpyAsync(g->out_off.ptr, out_off, 8 * (n + 1), cudaMemcpyHostToDevice, st);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(g->in_off.ptr, in_off, 8 * (n + 1), cudaMemcpyHostToDevice, st);
-        if (e == cudaSuccess && m) {
-            if (out_tgt) {
-                e = cudaMemcpyAsync(stage.ptr, out_tgt, 8 * m, cudaMemcpyHostToDevice, st);
-                k_narrow<<<gs_grid(ctx, m), 256, 0, st>>>(stage.as<int64_t>(), m, g->out_tgt.as<int32_t>());
-            }
-            if (e == cudaSuccess) e = cudaMemcpyAsync(stage.ptr, in_src, 8 * m, cudaMemcpyHostToDevice, st);
-            k_narrow<<<gs_grid(ctx, m), 256, 0, st>>>(stage.as<int64_t>(), m, g->in_src.as<int32_t>());
+        // the offsets travel on the copy lane of the index upload (hostio.cu)
+        // while the host threads narrow the indices
+        const RawCopy offs[2] = {{g->out_off.ptr, out_off, (size_t)(8 * (n + 1))},
+                                 {g->in_off.ptr, in_off, (size_t)(8 * (n + 1))}};
+        g->h2d_bytes = 16 * (n + 1);
+        if (m && out_tgt) rc = upload_narrow(ctx, out_tgt, m, g->out_tgt.as<int32_t>(), &g->h2d_bytes);
+        if (!rc) rc = upload_narrow(ctx, in_src, m, g->in_src.as<int32_t>(), &g->h2d_bytes, offs, 2);
+        if (!rc) {
+            k_degree<<<gs_grid(ctx, n), 256, 0, st>>>(g->out_off.as<int64_t>(), n, g->out_deg.as<int32_t>());
+            cudaError_t e = cudaStreamSynchronize(st);
+            if (e == cudaSuccess) e = cudaGetLastError();
+            if (e != cudaSuccess) rc = fail(PR_ERR_CUDA, std::string("graph upload: ") + cudaGetErrorString(e));
         }
-        k_degree<<<gs_grid(ctx, n), 256, 0, st>>>(g->out_off.as<int64_t>(), n, g->out_deg.as<int32_t>());
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        if (e == cudaSuccess) e = cudaGetLastError();
-        if (e != cudaSuccess) rc = fail(PR_ERR_CUDA, std::string("graph upload: ") + cudaGetErrorString(e));
     }
     if (rc) { delete g; return rc; }
     *out = g;

@@ -56,6 +56,8 @@ struct DevBuf {
 // grows (never shrinks) a buffer; contents are not preserved
 int ensure(DevBuf &b, size_t bytes);
 
+struct Uploader;  // hostio.cu
+
 struct Ctx {
     int device = 0;
     int sm_count = 148;
@@ -78,7 +80,20 @@ struct Ctx {
     // on_iteration): grown on demand, freed with the context
     void *obs_host = nullptr;
     size_t obs_host_bytes = 0;
+    // host threads, page-locked staging and copy streams of the pipelined
+    // index upload (hostio.cu), created on the first large upload
+    Uploader *up = nullptr;
 };
+void uploader_destroy(Ctx &ctx);
+// int64 host indices -> int32 device array (hostio.cu); *h2d += PCIe bytes.
+// extra: plain host -> device copies queued on the same copy lanes first.
+struct RawCopy {
+    void *dst;
+    const void *src;
+    size_t bytes;
+};
+int upload_narrow(Ctx &ctx, const int64_t *h, int64_t count, int32_t *d, int64_t *h2d,
+                  const RawCopy *extra = nullptr, int n_extra = 0);
 void release_execs(Ctx &ctx);
 
 // Per-block partial statistics of one round (reduced in fixed order).
@@ -129,6 +144,7 @@ struct RunCtl {
 struct Graph {
     Ctx *ctx = nullptr;
     int64_t n = 0, m = 0, raw = 0;
+    int64_t h2d_bytes = 0;   // bytes copied host -> device by pr_graph_upload / attach_out_targets
     DevBuf orig_ids;  // int64 [n] first-appearance id table (ingest.cu); empty = identity
     // run layout only: vertices [live_end, n) are the dangling ones (classes
     // out=0&in>0, isolated), so their in-edges are the CSC tail

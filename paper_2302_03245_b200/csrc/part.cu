@@ -29,6 +29,8 @@
 #include <cstring>
 #include <vector>
 
+#include <type_traits>
+
 #include "internal.cuh"
 #include "reduce.cuh"
 #include "bins.cuh"
@@ -563,6 +565,13 @@ static int finish_stats(Part &P, unsigned blocks, int64_t *ints, double *floats)
 
 template <class T>
 static int upload_as(Ctx &ctx, DevBuf &dst, const int64_t *src, int64_t count) {
+    if constexpr (std::is_same<T, int32_t>::value) {
+        // host-thread narrowing into page-locked staging (hostio.cu)
+        PR_TRY(ensure(dst, 4 * (count > 0 ? count : 1)));
+        PR_TRY(upload_narrow(ctx, src, count, dst.as<int32_t>(), nullptr));
+        PR_CUDA(cudaStreamSynchronize(ctx.stream));
+        return PR_OK;
+    }
     std::vector<T> tmp((size_t)(count > 0 ? count : 1));
     for (int64_t i = 0; i < count; ++i) tmp[(size_t)i] = (T)src[i];
     PR_TRY(ensure(dst, sizeof(T) * (count > 0 ? count : 1)));

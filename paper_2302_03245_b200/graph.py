@@ -70,7 +70,7 @@ class DeviceGraph:
                                                _lib.ptr(arrs["in_offsets"]), _lib.ptr(arrs["in_sources"]),
                                                ctypes.byref(h)), "upload")
         dev = cls(h, ctx)
-        dev.h2d_bytes = sum(a.nbytes for k, a in arrs.items() if not (lazy and k == "out_targets"))
+        dev.h2d_bytes = dev._copied_bytes()
         if lazy:
             dev._pending_out_targets = arrs["out_targets"]
         return dev
@@ -80,8 +80,15 @@ class DeviceGraph:
         a = self._pending_out_targets
         if a is not None:
             _lib.check(_lib.load().pr_graph_attach_out_targets(self.handle, _lib.ptr(a)), "attach_out_targets")
-            self.h2d_bytes += a.nbytes
+            self.h2d_bytes = self._copied_bytes()
             self._pending_out_targets = None
+
+    def _copied_bytes(self) -> int:
+        """Bytes the library copied host -> device for this graph (the int64
+        index arrays partly travel narrowed to int32, hostio.cu)."""
+        b = ctypes.c_int64()
+        _lib.check(_lib.load().pr_graph_h2d_bytes(self.handle, ctypes.byref(b)), "h2d_bytes")
+        return int(b.value)
 
     @classmethod
     def rmat(cls, scale: int, edge_factor: int, a=0.57, b=0.19, c=0.19, seed: int = 0, ctx=None):

@@ -2,6 +2,7 @@
 // part of the engine).  pr_debug_gather runs variants of a pure gather-sum
 // over the run layout's compacted CSC (IFP2 schedule) to separate the
 // memory system's limit from the segmented-reduction overhead.
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.cuh"
@@ -135,6 +136,43 @@ __global__ void ub_gather_synth(int64_t edges, int64_t n, const double *__restri
     if (acc == 123.456) out[0] = acc;
 }
 
+// v7-v9: the gather split by source id at H (the run layout's hottest
+// sources are the low ids; each row's sources are sorted, so a row's hot
+// sources are a prefix of it):
+//   MODE 0: cold only -- gathers of ids < H are skipped (no load): the floor
+//           of a main pass that leaves the hot prefix to another pass
+//   MODE 1: hot only  -- only ids < H are gathered (L1 then holds x[0, H))
+//   MODE 2: both, hot ids from a shared-memory copy of x[0, H) filled per block
+template <int MODE>
+__global__ void ub_gather_split(const int32_t *__restrict__ csc, int64_t edges, const double *__restrict__ x,
+                                int H, double *__restrict__ out) {
+    extern __shared__ double xs[];
+    if (MODE == 2) {
+        for (int i = threadIdx.x; i < H; i += blockDim.x) xs[i] = __ldg(&x[i]);
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31;
+    double acc = 0.0;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = warp * 256; base < edges; base += nw * 256) {
+        int idx[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) idx[q] = base + lane + 32 * q < edges ? __ldcs(&csc[base + lane + 32 * q]) : -1;
+        double t[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const bool hot = (unsigned)idx[q] < (unsigned)H;
+            if (MODE == 0) t[q] = idx[q] >= 0 && !hot ? __ldg(&x[idx[q]]) : 0.0;
+            else if (MODE == 1) t[q] = hot ? __ldg(&x[idx[q]]) : 0.0;
+            else t[q] = idx[q] < 0 ? 0.0 : hot ? xs[idx[q]] : __ldg(&x[idx[q]]);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc += t[q];
+    }
+    if (acc == 123.456) out[0] = acc;
+}
+
 int debug_gather(Graph &g0, int variant, int iters, int blocks_per_sm, double *ms_out) {
     PR_TRY(ensure_run_layout(g0));
     Graph &g = *g0.run;
@@ -148,6 +186,9 @@ int debug_gather(Graph &g0, int variant, int iters, int blocks_per_sm, double *m
     PR_TRY(ensure(out, 8));
     PR_CUDA(cudaMemsetAsync(x.ptr, 0, 8 * g.n, st));
     unsigned grid = (unsigned)(ctx.sm_count * (blocks_per_sm > 0 ? blocks_per_sm : 8));
+    const int H = getenv("PR_UB_H") ? atoi(getenv("PR_UB_H")) : 16384;
+    if (variant == 9 && 8 * H > 48 * 1024)
+        PR_CUDA(cudaFuncSetAttribute(ub_gather_split<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * H));
     cudaEvent_t e0, e1;
     PR_CUDA(cudaEventCreate(&e0));
     PR_CUDA(cudaEventCreate(&e1));
@@ -161,6 +202,9 @@ int debug_gather(Graph &g0, int variant, int iters, int blocks_per_sm, double *m
             case 4: ub_gather_groups8<<<grid, 256, 0, st>>>(S.csc.as<int32_t>(), S.edges, x.as<double>(), out.as<double>()); break;
             case 5: ub_gather_synth<0><<<grid, 256, 0, st>>>(S.edges, g.n, x.as<double>(), out.as<double>()); break;
             case 6: ub_gather_synth<1><<<grid, 256, 0, st>>>(S.edges, g.n, x.as<double>(), out.as<double>()); break;
+            case 7: ub_gather_split<0><<<grid, 256, 0, st>>>(S.csc.as<int32_t>(), S.edges, x.as<double>(), H, out.as<double>()); break;
+            case 8: ub_gather_split<1><<<grid, 256, 0, st>>>(S.csc.as<int32_t>(), S.edges, x.as<double>(), H, out.as<double>()); break;
+            case 9: ub_gather_split<2><<<grid, 256, 8 * H, st>>>(S.csc.as<int32_t>(), S.edges, x.as<double>(), H, out.as<double>()); break;
             default: ub_stream<<<grid, 256, 0, st>>>(S.csc.as<int32_t>(), S.edges, out.as<double>()); break;
             }
         }

@@ -22,9 +22,11 @@ L = _lib.load()
 L.pr_debug_gather.restype = ctypes.c_int
 L.pr_debug_gather.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
 names = {0: "gather8 thread-contig", 1: "gather16 thread-contig", 2: "gather lane-interleaved", 3: "index stream only",
-         4: "lane-interleaved, 8-lane LDGs", 5: "uniform random gather", 6: "sequential gather"}
+         4: "lane-interleaved, 8-lane LDGs", 5: "uniform random gather", 6: "sequential gather",
+         7: "cold only (id >= H)", 8: "hot only (id < H)", 9: "hot from smem, cold global"}
+bps_list = [int(b) for b in os.environ.get("UB_BPS", "4,8").split(",")]
 for v in [int(a) for a in (sys.argv[2].split(",") if len(sys.argv) > 2 else range(7))]:
-    for bps in (4, 8):
+    for bps in bps_list:
         ms = ctypes.c_double()
         _lib.check(L.pr_debug_gather(g.dev.handle, v, 20, bps, ctypes.byref(ms)))
-        print(f"{cfg} {names[v]:26s} blocks/SM={bps:2d}: {ms.value*1e3:8.1f} us")
+        print(f"{cfg} H={os.environ.get('PR_UB_H', 16384)} {names[v]:26s} blocks/SM={bps:2d}: {ms.value*1e3:8.1f} us")
