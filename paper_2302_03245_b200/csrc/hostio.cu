@@ -10,17 +10,27 @@
 //     buffered per thread;
 //   * copy lane: the tail goes over PCIe as raw int64 on copy stream 1 (no
 //     host work) into a device staging buffer and is narrowed by k_narrow.
-// Both lanes run at once.  The split balances the host threads' narrowing
-// rate c against PCIe (b ~ 55 GB/s): f = 2c / (2b + c) of the elements take
-// the host lane.  Measured on the B200 box (16 host threads, AVX2 streaming
-// stores): c ~ 85-90 GB/s of int64 input, so f ~ 0.9; the C5 upload (1.06 G
-// in-sources + both offset arrays, 9.56 GB as int64) takes ~121 ms instead
-// of 175 ms.  Pageable host memory takes the host lane only (a pageable
-// cudaMemcpy stages through the driver anyway).  The values are identical to
-// the single-copy path (tests/test_gpu_upload.py).
+// Both lanes run at once and meet in the middle: the host threads claim
+// chunks from the head of the array, the copy lane claims pieces from its
+// tail, until the claims meet.  With host narrowing rate c (GB/s of int64
+// input) and PCIe rate b (~55 GB/s) the best share of the host lane is
+// f = 2c / (2b + c): its int32 copies use c/2 of the link and the raw lane the
+// rest.  c differs from host to host (16 threads with AVX2 streaming stores:
+// 30-90 GB/s on the B200 boxes seen), so it is measured while the upload
+// runs -- the time each thread spends inside the narrowing loop -- and the
+// copy lane only claims a piece while its share stays below 1 - f; whatever
+// the estimate, the array is consumed from both ends, so a wrong guess costs
+// a late piece, not a stalled lane.  PUSHRANK_UPLOAD_HOSTFRAC pins a static
+// split (tests, A/B).  Fast host (c ~ 90): f ~ 0.9, the C5 upload (1.06 G
+// in-sources + both offset arrays, 9.56 GB as int64) takes ~121 ms instead of
+// 175 ms for the plain copy.  Pageable host memory takes the host lane only
+// (a pageable cudaMemcpy stages through the driver anyway).  The values are
+// identical to the single-copy path (tests/test_gpu_upload.py).
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
 #include <functional>
 #include <mutex>
@@ -224,67 +234,141 @@ int upload_narrow(Ctx &ctx, const int64_t *h, int64_t count, int32_t *d, int64_t
     Uploader *u = nullptr;
     PR_TRY(uploader(ctx, &u));
     const int T = u->pool.size();
-    // share of the elements narrowed on the host (module comment)
-    double f = 1.0;
-    if (page_locked(h)) {
-        const double c = std::min(11.0 * T, 90.0), b = 55.0;
-        f = 2.0 * c / (2.0 * b + c);
-        if (const char *e = getenv("PUSHRANK_UPLOAD_RATE")) {
-            // measured host narrowing rate (GB/s of int64 input) for the split
-            const double cc = atof(e);
-            if (cc > 0) f = 2.0 * cc / (2.0 * b + cc);
-        }
-    }
-    if (const char *e = getenv("PUSHRANK_UPLOAD_HOSTFRAC")) f = atof(e);
-    f = std::min(1.0, std::max(0.0, f));
     const int64_t CH = u->chunk;
-    int64_t split = (int64_t)(f * (double)count);
-    split = split >= count ? count : (split / CH) * CH;
+    const int64_t n_chunks = (count + CH - 1) / CH;
+    const bool pinned = page_locked(h);
+    // static split (tests, A/B): the first `fixed` chunks take the host lane
+    int64_t fixed = -1;
+    if (const char *e = getenv("PUSHRANK_UPLOAD_HOSTFRAC")) {
+        const double f = std::min(1.0, std::max(0.0, atof(e)));
+        fixed = f >= 1.0 ? n_chunks : (int64_t)(f * (double)count) / CH;
+    } else if (!pinned || T < 2) {
+        fixed = n_chunks;   // host lane only
+    }
+    // copy lane pieces: RAW chunks each, two device staging slots in rotation
+    const int64_t RAW = std::max<int64_t>(1, env_i64("PUSHRANK_UPLOAD_RAW_CHUNKS", 8));
+    const double b = 55.0;                                   // PCIe, GB/s
+    double c0 = std::min(11.0 * T, 90.0);                    // first guess of the narrowing rate
+    if (const char *e = getenv("PUSHRANK_UPLOAD_RATE"))
+        if (atof(e) > 0) c0 = atof(e);
+    const bool raw_lane = fixed < n_chunks;
     // both copy streams start after the allocations queued on ctx.stream
-    cudaEvent_t ev_start, ev_done[2];
+    cudaEvent_t ev_start, ev_done[2], ev_raw[2];
     PR_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
     PR_CUDA(cudaEventCreateWithFlags(&ev_done[0], cudaEventDisableTiming));
     PR_CUDA(cudaEventCreateWithFlags(&ev_done[1], cudaEventDisableTiming));
+    PR_CUDA(cudaEventCreateWithFlags(&ev_raw[0], cudaEventDisableTiming));
+    PR_CUDA(cudaEventCreateWithFlags(&ev_raw[1], cudaEventDisableTiming));
     DevBuf stage;
     int rc = PR_OK;
-    if (split < count) rc = ensure(stage, 8 * (count - split));
+    const int64_t piece = RAW * CH;
+    if (raw_lane) rc = ensure(stage, 2 * 8 * (size_t)piece);
+    int64_t host_elems = 0, raw_elems = 0;
     if (rc == PR_OK) {
         cudaError_t e = cudaEventRecord(ev_start, st);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(u->cs[0], ev_start, 0);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(u->cs[1], ev_start, 0);
-        // copy lane: the caller's extra raw copies, then the raw int64 tail,
-        // narrowed on the device
+        // copy lane first: the caller's extra raw copies
         for (int k = 0; e == cudaSuccess && k < n_extra; ++k)
             e = cudaMemcpyAsync(extra[k].dst, extra[k].src, extra[k].bytes, cudaMemcpyHostToDevice, u->cs[1]);
-        if (e == cudaSuccess && split < count) {
-            e = cudaMemcpyAsync(stage.ptr, h + split, 8 * (count - split), cudaMemcpyHostToDevice, u->cs[1]);
-            if (e == cudaSuccess) {
-                k_narrow<<<narrow_grid(ctx, count - split), 256, 0, u->cs[1]>>>(stage.as<int64_t>(), count - split,
-                                                                              d + split);
-                e = cudaGetLastError();
-            }
-        }
-        // host lane: every pool thread narrows its chunks k = t, t + T, ...
-        // into its own slots and queues their copies on copy stream 0
-        if (e == cudaSuccess && split > 0) {
+        if (e == cudaSuccess) {
+            // claims: chunks [0, head) belong to the host lane, [tail, n_chunks) to the copy lane
+            std::mutex mu;
+            int64_t head = 0, tail = n_chunks;
             std::atomic<int> err{0};
-            u->pool.run([&](int t, int nt) {
-                int j = 0;
-                for (int64_t k = t; k * CH < split && !err.load(std::memory_order_relaxed); k += nt, ++j) {
-                    const int s = Uploader::SLOTS * t + (j % Uploader::SLOTS);
-                    cudaError_t x = cudaSuccess;
-                    if (u->used[s]) x = cudaEventSynchronize(u->ev[s]);
-                    const int64_t off = k * CH, len = std::min(CH, split - off);
-                    if (x == cudaSuccess) {
-                        narrow_host(h + off, u->slot[s], len);
-                        x = cudaMemcpyAsync(d + off, u->slot[s], 4 * len, cudaMemcpyHostToDevice, u->cs[0]);
-                    }
-                    if (x == cudaSuccess) x = cudaEventRecord(u->ev[s], u->cs[0]);
-                    u->used[s] = 1;
-                    if (x != cudaSuccess) err.store((int)x);
+            std::atomic<int64_t> narrowed{0}, narrow_ns{0};
+            using clk = std::chrono::steady_clock;
+            // one chunk of the host lane on thread t (its j-th); false when none is left
+            auto host_one = [&](int t, int j) -> bool {
+                int64_t k;
+                {
+                    std::lock_guard<std::mutex> l(mu);
+                    if (head >= (fixed >= 0 ? fixed : tail)) return false;
+                    k = head++;
                 }
+                const int s = Uploader::SLOTS * t + (j % Uploader::SLOTS);
+                cudaError_t x = cudaSuccess;
+                if (u->used[s]) x = cudaEventSynchronize(u->ev[s]);
+                const int64_t off = k * CH, len = std::min(CH, count - off);
+                if (x == cudaSuccess) {
+                    const auto t0 = clk::now();
+                    narrow_host(h + off, u->slot[s], len);
+                    narrow_ns.fetch_add(std::chrono::duration_cast<std::chrono::nanoseconds>(clk::now() - t0).count());
+                    narrowed.fetch_add(len);
+                    x = cudaMemcpyAsync(d + off, u->slot[s], 4 * len, cudaMemcpyHostToDevice, u->cs[0]);
+                }
+                if (x == cudaSuccess) x = cudaEventRecord(u->ev[s], u->cs[0]);
+                u->used[s] = 1;
+                if (x != cudaSuccess) err.store((int)x);
+                return true;
+            };
+            auto host_lane = [&](int t, int j) {
+                while (!err.load(std::memory_order_relaxed) && host_one(t, j)) ++j;
+            };
+            // thread 0: the copy lane; while that is ahead of its share, one host chunk at a time
+            auto copy_lane = [&]() -> int {
+                int64_t claimed = 0;   // chunks this lane has taken
+                int hj = 0;            // host chunks thread 0 has narrowed
+                for (int j = 0; !err.load(std::memory_order_relaxed);) {
+                    int64_t k0 = 0, take = 0;
+                    bool done = false;
+                    {
+                        std::lock_guard<std::mutex> l(mu);
+                        const int64_t lo = fixed >= 0 ? std::max(fixed, head) : head;
+                        if (lo >= tail) {
+                            done = true;
+                        } else {
+                            take = std::min(RAW, tail - lo);
+                            if (fixed < 0) {
+                                // share of the host lane from its measured narrowing rate
+                                const int64_t ns = narrow_ns.load(), el = narrowed.load();
+                                const double c = el >= T * CH && ns > 0 ? 8.0 * (double)el / (double)ns * T : c0;
+                                const double f = 2.0 * c / (2.0 * b + c);
+                                if ((double)(claimed + take) > (1.0 - f) * (double)n_chunks + 0.5)
+                                    take = 0;   // ahead of its share: leave the rest to the host threads for now
+                            }
+                            if (take > 0) {
+                                tail -= take;
+                                k0 = tail;
+                            }
+                        }
+                    }
+                    if (done) break;
+                    if (take == 0) {
+                        if (host_one(0, hj)) ++hj;
+                        continue;
+                    }
+                    cudaError_t x = cudaSuccess;
+                    if (j >= 2) x = cudaEventSynchronize(ev_raw[j & 1]);   // its staging slot is free again
+                    const int64_t off = k0 * CH, len = std::min(count, (k0 + take) * CH) - off;
+                    int64_t *slot = stage.as<int64_t>() + (int64_t)(j & 1) * piece;
+                    if (x == cudaSuccess) x = cudaMemcpyAsync(slot, h + off, 8 * len, cudaMemcpyHostToDevice, u->cs[1]);
+                    if (x == cudaSuccess) {
+                        k_narrow<<<narrow_grid(ctx, len), 256, 0, u->cs[1]>>>(slot, len, d + off);
+                        x = cudaGetLastError();
+                    }
+                    if (x == cudaSuccess) x = cudaEventRecord(ev_raw[j & 1], u->cs[1]);
+                    if (x != cudaSuccess) err.store((int)x);
+                    raw_elems += len;
+                    claimed += take;
+                    ++j;
+                }
+                return hj;
+            };
+            const auto t_begin = clk::now();
+            u->pool.run([&](int t, int) {
+                // thread 0 drives the copy lane when there is one, then helps narrowing
+                host_lane(t, t == 0 && raw_lane ? copy_lane() : 0);
             });
+            host_elems = narrowed.load();
             if (err.load()) e = (cudaError_t)err.load();
+            if (getenv("PUSHRANK_TIMING")) {
+                const double wall = std::chrono::duration<double>(clk::now() - t_begin).count();
+                const double ns = (double)narrow_ns.load();
+                fprintf(stderr, "[upload] %lld elements: host lane %.1f%% (%d threads, %.1f GB/s per thread of int64 in), "
+                        "copy lane %.1f%%, queued in %.1f ms\n", (long long)count, 100.0 * host_elems / count, T,
+                        ns > 0 ? 8.0 * host_elems / ns : 0.0, 100.0 * raw_elems / count, 1e3 * wall);
+            }
         }
         if (e == cudaSuccess) e = cudaEventRecord(ev_done[0], u->cs[0]);
         if (e == cudaSuccess) e = cudaEventRecord(ev_done[1], u->cs[1]);
@@ -297,12 +381,14 @@ int upload_narrow(Ctx &ctx, const int64_t *h, int64_t count, int32_t *d, int64_t
             rc = fail(PR_ERR_CUDA, std::string("upload: ") + cudaGetErrorString(e));
         }
     }
-    // the staging buffer's free is ordered after the tail's narrowing (ctx.stream waits on it)
+    // the staging slots' free is ordered after the copy lane's narrowing (ctx.stream waits on it)
     stage.release();
     cudaEventDestroy(ev_start);
-    cudaEventDestroy(ev_done[0]);
-    cudaEventDestroy(ev_done[1]);
-    if (rc == PR_OK && h2d) *h2d += 4 * split + 8 * (count - split);
+    for (int k = 0; k < 2; ++k) {
+        cudaEventDestroy(ev_done[k]);
+        cudaEventDestroy(ev_raw[k]);
+    }
+    if (rc == PR_OK && h2d) *h2d += 4 * host_elems + 8 * raw_elems;
     return rc;
 }
 

@@ -1,6 +1,6 @@
 """The pipelined index upload (csrc/hostio.cu): host-narrowed chunks and the
-raw int64 tail must give the same device graph as a plain copy, for every
-split of the array between the two lanes, from page-locked and pageable
+raw int64 tail must give the same device graph as a plain copy, for the
+adaptive split and for every static split of the array between the two lanes, from page-locked and pageable
 host memory, with chunk sizes that do not divide the array."""
 
 import os
@@ -29,8 +29,12 @@ ref = {k: np.ascontiguousarray(getattr(g, k)) for k in ("out_offsets", "out_targ
 pinned = {k: torch.from_numpy(v).pin_memory().numpy() for k, v in ref.items()}
 m = int(g.m)
 for host in (ref, pinned):
-    for frac in ("0", "0.37", "0.77", "1"):
-        os.environ["PUSHRANK_UPLOAD_HOSTFRAC"] = frac
+    for frac in (None, "0", "0.37", "0.77", "1"):
+        # None: the adaptive split (both lanes claim chunks until they meet)
+        if frac is None:
+            os.environ.pop("PUSHRANK_UPLOAD_HOSTFRAC", None)
+        else:
+            os.environ["PUSHRANK_UPLOAD_HOSTFRAC"] = frac
         for lazy in (True, False):
             dev = DeviceGraph.upload(SimpleNamespace(n=g.n, m=m, **host), lazy_out_targets=lazy)
             out = dev.export()
