@@ -13,6 +13,12 @@ namespace pr {
 
 // Gauss-Seidel sections of a dense sweep (rounds.cu): at most this many
 #define PR_MAX_SECTIONS 8
+// Gauss-Seidel sections of a dense sweep from the round's working set ws
+// (bytes) against L2 (rounds.cu "Gauss-Seidel sections"): none while the
+// round is short (C2, C4), 2 past 1.5x L2 (C3: 3 / 4 sections 10.6 / 11.0 ms
+// against 9.9), 6 past 16x (C5 IFP2 4 / 5 / 6 / 7 / 8 sections: 461 / 475 /
+// 441 / 462 / 448 ms; IFP1 4 / 6 / 7: 491 / 451 / 489 ms)
+static inline int gs_sections_default(double ws, double l2) { return ws > 16.0 * l2 ? 6 : ws > 1.5 * l2 ? 2 : 1; }
 
 // ---------------------------------------------------------------- errors
 void set_error(const std::string &msg);

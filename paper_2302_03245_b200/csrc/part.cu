@@ -990,7 +990,7 @@ static int ensure_part_sched(Part &P) {
         // rank-local Gauss-Seidel sections, as the engine chooses them
         // (rounds.cu): IFP2 on rows that are the local ids in order (a
         // run-layout partition), 2 past 1.5x L2 of round working set, 4 past 16x
-        P.nsec = ws > 16.0 * l2 ? 4 : ws > 1.5 * l2 ? 2 : 1;
+        P.nsec = gs_sections_default(ws, l2);
         if (const char *e = getenv("PUSHRANK_GS_SECTIONS")) P.nsec = atoi(e);
         if (P.nsec < 1) P.nsec = 1;
         if (P.nsec > PR_MAX_SECTIONS) P.nsec = PR_MAX_SECTIONS;

@@ -1196,10 +1196,11 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     // Sections cut rounds (C2: 174 -> 98 at 4 sections) but each adds a
     // launch, a ramp and a reduction to the sweep, so they pay only when a
     // round is long: 2 sections past 1.5x L2 of round working set (C3: 14.8 ->
-    // 11.5 ms), 4 past 16x (C5: 813 -> 598 ms), none below (C2, C4).
+    // 11.5 ms), 6 past 16x (C5: 813 -> 598 ms at 4 sections in round 1; 461 ->
+    // 441 ms from 4 to 6 with this round's kernels), none below (C2, C4).
     int nsec = 1;
     if ((algo == PR_ALGO_IFP2 || algo == PR_ALGO_IFP1) && g.class0_end >= 0) {
-        nsec = ws > 16.0 * l2 ? 4 : ws > 1.5 * l2 ? 2 : 1;
+        nsec = gs_sections_default(ws, l2);
         if (const char *e = getenv("PUSHRANK_GS_SECTIONS")) nsec = atoi(e);
         if (nsec < 1) nsec = 1;
         if (nsec > PR_MAX_SECTIONS) nsec = PR_MAX_SECTIONS;

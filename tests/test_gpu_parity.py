@@ -387,13 +387,13 @@ def test_config_engines_parity(config):
 
 def test_forced_c5_code_path_parity(monkeypatch):
     """C5's code path at a size the oracle finishes in about a minute: R-MAT
-    scale 23 (134 M edges) with 4 Gauss-Seidel sections, source-sorted CSC
+    scale 23 (134 M edges) with 6 Gauss-Seidel sections, source-sorted CSC
     rows and the streamed (evict-first) k_pull forced as at C5.  Device vs
     host edge generators, integer preprocessing bit-exact, IFP2 and IFP1
     (auto + pull) against the oracle twin.  The full C5 run of the same
     script is profiles/r02_parity_c5.json."""
     import full_size_parity as F
-    monkeypatch.setenv("PUSHRANK_GS_SECTIONS", "4")
+    monkeypatch.setenv("PUSHRANK_GS_SECTIONS", "6")
     monkeypatch.setenv("PUSHRANK_SORT_ROWS", "1")
     monkeypatch.setenv("PUSHRANK_PREFETCH", "0")
     v = F.run("rmat", scale=23, modes=("auto", "pull"), xi=1e-10)
@@ -403,7 +403,7 @@ def test_forced_c5_code_path_parity(monkeypatch):
 
 def test_c5_full_size_properties():
     """C5 (R-MAT scale 26, 1.06 B edges; too large for the oracle): size-
-    independent properties of the fast IFP2 engine (4 Gauss-Seidel sections):
+    independent properties of the fast IFP2 engine (6 Gauss-Seidel sections):
     mass 1, m_d dangling pushes, agreement with 210 power iterations (L1 and
     top-100), and the ranking order against numpy."""
     from paper_2302_03245_b200 import serialize
