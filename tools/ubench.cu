@@ -144,7 +144,7 @@ __global__ void ub_gather_synth(int64_t edges, int64_t n, const double *__restri
 //   MODE 1: hot only  -- only ids < H are gathered (L1 then holds x[0, H))
 //   MODE 2: both, hot ids from a shared-memory copy of x[0, H) filled per block
 template <int MODE>
-__global__ void ub_gather_split(const int32_t *__restrict__ csc, int64_t edges, const double *__restrict__ x,
+__global__ void __launch_bounds__(1024, 1) ub_gather_split(const int32_t *__restrict__ csc, int64_t edges, const double *__restrict__ x,
                                 int H, double *__restrict__ out) {
     extern __shared__ double xs[];
     if (MODE == 2) {
@@ -165,7 +165,18 @@ __global__ void ub_gather_split(const int32_t *__restrict__ csc, int64_t edges, 
             const bool hot = (unsigned)idx[q] < (unsigned)H;
             if (MODE == 0) t[q] = idx[q] >= 0 && !hot ? __ldg(&x[idx[q]]) : 0.0;
             else if (MODE == 1) t[q] = hot ? __ldg(&x[idx[q]]) : 0.0;
-            else t[q] = idx[q] < 0 ? 0.0 : hot ? xs[idx[q]] : __ldg(&x[idx[q]]);
+            else {
+                // explicit predicated LDS / LDG.NC: a C++ select between the two pointers becomes one
+                // generic load, which replays per address space (measured 16 ms per sweep at H = 4096)
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(xs) + 8u * (unsigned)(hot ? idx[q] : 0);
+                const double *ga = x + (idx[q] >= 0 && !hot ? idx[q] : 0);
+                double v;
+                asm("{ .reg .pred p; setp.ne.u32 p, %3, 0;\n"
+                    "  @p ld.shared.f64 %0, [%1];\n"
+                    "  @!p ld.global.nc.f64 %0, [%2]; }"
+                    : "=d"(v) : "r"(sa), "l"(ga), "r"((unsigned)hot));
+                t[q] = idx[q] < 0 ? 0.0 : v;
+            }
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc += t[q];
@@ -187,6 +198,7 @@ int debug_gather(Graph &g0, int variant, int iters, int blocks_per_sm, double *m
     PR_CUDA(cudaMemsetAsync(x.ptr, 0, 8 * g.n, st));
     unsigned grid = (unsigned)(ctx.sm_count * (blocks_per_sm > 0 ? blocks_per_sm : 8));
     const int H = getenv("PR_UB_H") ? atoi(getenv("PR_UB_H")) : 16384;
+    const int TH = getenv("PR_UB_THREADS") ? atoi(getenv("PR_UB_THREADS")) : 256;   // v7-v9 block size
     if (variant == 9 && 8 * H > 48 * 1024)
         PR_CUDA(cudaFuncSetAttribute(ub_gather_split<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * H));
     cudaEvent_t e0, e1;
@@ -202,9 +214,9 @@ int debug_gather(Graph &g0, int variant, int iters, int blocks_per_sm, double *m
             case 4: ub_gather_groups8<<<grid, 256, 0, st>>>(S.csc.as<int32_t>(), S.edges, x.as<double>(), out.as<double>()); break;
             case 5: ub_gather_synth<0><<<grid, 256, 0, st>>>(S.edges, g.n, x.as<double>(), out.as<double>()); break;
             case 6: ub_gather_synth<1><<<grid, 256, 0, st>>>(S.edges, g.n, x.as<double>(), out.as<double>()); break;
-            case 7: ub_gather_split<0><<<grid, 256, 0, st>>>(S.csc.as<int32_t>(), S.edges, x.as<double>(), H, out.as<double>()); break;
-            case 8: ub_gather_split<1><<<grid, 256, 0, st>>>(S.csc.as<int32_t>(), S.edges, x.as<double>(), H, out.as<double>()); break;
-            case 9: ub_gather_split<2><<<grid, 256, 8 * H, st>>>(S.csc.as<int32_t>(), S.edges, x.as<double>(), H, out.as<double>()); break;
+            case 7: ub_gather_split<0><<<grid, TH, 0, st>>>(S.csc.as<int32_t>(), S.edges, x.as<double>(), H, out.as<double>()); break;
+            case 8: ub_gather_split<1><<<grid, TH, 0, st>>>(S.csc.as<int32_t>(), S.edges, x.as<double>(), H, out.as<double>()); break;
+            case 9: ub_gather_split<2><<<grid, TH, 8 * H, st>>>(S.csc.as<int32_t>(), S.edges, x.as<double>(), H, out.as<double>()); break;
             default: ub_stream<<<grid, 256, 0, st>>>(S.csc.as<int32_t>(), S.edges, out.as<double>()); break;
             }
         }
