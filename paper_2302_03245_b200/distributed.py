@@ -25,6 +25,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 
 STAT_INTS = ("nact", "work", "push_ops", "push_dang", "conv_all", "conv_scan")
@@ -240,8 +242,10 @@ class Comm:
         self.torch, self.dist = torch, dist
         self.device = device
         # one rank: every collective is the identity (all-gather of the own
-        # slice into itself, sum over one rank) -- issue none
-        self.solo = dist.get_world_size() == 1
+        # slice into itself, sum over one rank) -- issue none, unless
+        # PUSHRANK_SOLO_COLLECTIVES=1 asks for them (tests: the NCCL calls and
+        # their capture into the batch graphs, exercised on a one-GPU box)
+        self.solo = dist.get_world_size() == 1 and os.environ.get("PUSHRANK_SOLO_COLLECTIVES", "0") != "1"
 
     def _staged(self, t) -> bool:
         # gloo has no CUDA all-gather: device tensors go through host copies

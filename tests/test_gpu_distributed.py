@@ -249,3 +249,71 @@ def test_device_partitions_emulated(algorithm):
     assert 0 < step.exchange_entries() < 3 * part.owned
     top = lambda v: np.lexsort((np.arange(v.size), -v))[:100]   # noqa: E731
     assert np.array_equal(top(vd), top(vh))
+
+
+def _worker_nccl(port, algorithm, fused, q):
+    """One NCCL rank with the collectives forced on (PUSHRANK_SOLO_COLLECTIVES):
+    the in-place all-gather and the statistics all-reduce are real NCCL calls
+    on the library stream, and the steady-state batch is captured into a CUDA
+    graph with them inside -- the code path bench.py --gpus N runs, on the
+    one GPU this box has.  Two solves on the same step: the second replays
+    the captured graph from its second batch on."""
+    import torch
+    import torch.distributed as dist
+    import paper_2302_03245_b200 as P
+    from paper_2302_03245_b200 import distributed as D
+    from paper_2302_03245_b200 import synthetic
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["PUSHRANK_SOLO_COLLECTIVES"] = "1"
+    os.environ["PUSHRANK_GS_SECTIONS"] = "2"
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        n, src, dst = synthetic.make("c2", seed=0)
+        g = P.from_edges(n, src, dst)
+        part = D.partition_device(g, 1, 0, algorithm, 0.85, 1e-10)
+        step = D.CudaLocalStep(part, 0.85, 1e-10, algorithm, device=0, fast=True)
+        comm = D.Comm(device=torch.device("cuda", 0))
+        assert not comm.solo
+        ok = step.setup_fused(comm) if fused else False
+        out = []
+        for _ in range(2):
+            vals, rows, info = D.run_partitioned_queued(step, comm, part, algorithm, 0.85, 1e-10, batch=6, fused=ok)
+            out.append((vals.copy(), info["rounds"]))
+        captured = step._queued["graph"] is not None
+        if ok:
+            step.close_fused(comm)
+        q.put((ok, captured, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_nccl_collectives_in_captured_batches(fused):
+    """NCCL at one rank with every collective issued: the batch graphs carry
+    the all-gather / all-reduce nodes, the replayed solve is bit-identical to
+    the first one, and both match the sync twin."""
+    import torch.multiprocessing as mp
+    from paper_2302_03245_b200 import distributed as D
+    from paper_2302_03245_b200 import synthetic
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_worker_nccl, args=(_port(), "ifp2", fused, q))
+    p.start()
+    ok, captured, out = q.get(timeout=900)
+    p.join(timeout=120)
+    assert p.exitcode == 0
+    assert captured, "the steady-state batch was not captured into a CUDA graph"
+    assert ok == fused
+    (v1, r1), (v2, r2) = out
+    assert np.array_equal(v1, v2) and r1 == r2
+    n, src, dst = synthetic.make("c2", seed=0)
+    g = oracle.from_edges(n, src, dst)
+    order = D.run_order(np.diff(g.out_offsets), np.diff(g.in_offsets))
+    vals = np.empty(n)
+    vals[order] = v1
+    o = oracle.sync_simulate(g, "ifp2", threshold=1e-10)
+    assert np.abs(vals - o.values).sum() <= 1e-9
+    top = lambda v: np.lexsort((np.arange(v.size), -v))[:100]   # noqa: E731
+    assert np.array_equal(top(vals), top(o.values))
