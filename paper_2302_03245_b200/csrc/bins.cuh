@@ -2,9 +2,10 @@
 //
 // Rows are sorted by descending in-degree and cut into block work units of
 // near-equal cost (edges + ROW_COST * rows); a unit never mixes bins:
-//   * hub unit    -- HUB_CHUNK edges of one row with > HUB_DEG edges, 16
-//                    coalesced gathers per thread; the last chunk of a row to
-//                    arrive adds the chunk sums in chunk order;
+//   * hub unit    -- HUB_CHUNK edges of one row with > HUB_DEG edges, summed
+//                    HUB_STEP at a time (16 coalesced gathers per thread in
+//                    flight) with one block reduction per unit; the last chunk
+//                    of a row to arrive adds the chunk sums in chunk order;
 //   * warp unit   -- rows with THREAD_DEG < d <= HUB_DEG; warp w takes rows
 //                    w, w+8, ...; lanes stride a row with 8 gathers in flight;
 //   * thread unit -- rows with d <= THREAD_DEG; thread t takes rows t, t+256,
@@ -297,15 +298,19 @@ __device__ __forceinline__ void bins_run(const BinView &B, const int64_t u_lo, c
             const int64_t rb = B.doff[r], re = B.doff[r + 1];
             const int64_t c0 = rb + c * HUB_CHUNK;
             const int64_t c1 = c0 + HUB_CHUNK < re ? c0 + HUB_CHUNK : re;
-            int idx[HUB_CHUNK / 256];
-#pragma unroll
-            for (int q = 0; q < HUB_CHUNK / 256; ++q) {
-                const int64_t e = c0 + tid + 256 * q;
-                idx[q] = e < c1 ? ld_idx<STREAM>(&B.csc[e]) : -1;
-            }
+            // HUB_STEP edges at a time (16 gathers per thread in flight), no
+            // barrier until the whole chunk is summed
             double acc = 0.0;
+            for (int64_t s0 = c0; s0 < c1; s0 += HUB_STEP) {
+                int idx[HUB_STEP / 256];
 #pragma unroll
-            for (int q = 0; q < HUB_CHUNK / 256; ++q) acc += idx[q] >= 0 ? ld_src<SRC>(x, idx[q]) : 0.0;
+                for (int q = 0; q < HUB_STEP / 256; ++q) {
+                    const int64_t e = s0 + tid + 256 * q;
+                    idx[q] = e < c1 ? ld_idx<STREAM>(&B.csc[e]) : -1;
+                }
+#pragma unroll
+                for (int q = 0; q < HUB_STEP / 256; ++q) acc += idx[q] >= 0 ? ld_src<SRC>(x, idx[q]) : 0.0;
+            }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             __syncthreads();
@@ -399,11 +404,12 @@ template <bool STREAM, int SRC, class ThreadRow, class SingleRow>
 __device__ __forceinline__ void bins_run_plain(const BinView &B, const int64_t u_lo, const int64_t u_hi, const Src x,
                                                ThreadRow &thread_row, SingleRow &single_row) {
     __shared__ double red[8];
-    __shared__ int64_t next_unit;
+    __shared__ int64_t next_unit[2];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int64_t warp_rows = B.n_hub + B.n_warp;
     // dynamic unit dispatch: first unit = blockIdx.x, then one atomic per unit
     // (units are ordered heaviest first); the round finaliser resets the counter
+    int ring = 0;
     for (int64_t u = u_lo + blockIdx.x; u < u_hi;) {
 #if PR_DYNAMIC_UNITS
         // claim the following unit now; the atomic's latency hides behind this unit
@@ -417,15 +423,19 @@ __device__ __forceinline__ void bins_run_plain(const BinView &B, const int64_t u
             const int64_t rb = B.doff[r], re = B.doff[r + 1];
             const int64_t c0 = rb + c * HUB_CHUNK;
             const int64_t c1 = c0 + HUB_CHUNK < re ? c0 + HUB_CHUNK : re;
-            int idx[HUB_CHUNK / 256];
-#pragma unroll
-            for (int q = 0; q < HUB_CHUNK / 256; ++q) {
-                const int64_t e = c0 + tid + 256 * q;
-                idx[q] = e < c1 ? ld_idx<STREAM>(&B.csc[e]) : -1;
-            }
+            // HUB_STEP edges at a time (16 gathers per thread in flight), no
+            // barrier until the whole chunk is summed
             double acc = 0.0;
+            for (int64_t s0 = c0; s0 < c1; s0 += HUB_STEP) {
+                int idx[HUB_STEP / 256];
 #pragma unroll
-            for (int q = 0; q < HUB_CHUNK / 256; ++q) acc += idx[q] >= 0 ? ld_src<SRC>(x, idx[q]) : 0.0;
+                for (int q = 0; q < HUB_STEP / 256; ++q) {
+                    const int64_t e = s0 + tid + 256 * q;
+                    idx[q] = e < c1 ? ld_idx<STREAM>(&B.csc[e]) : -1;
+                }
+#pragma unroll
+                for (int q = 0; q < HUB_STEP / 256; ++q) acc += idx[q] >= 0 ? ld_src<SRC>(x, idx[q]) : 0.0;
+            }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             __syncthreads();
@@ -471,10 +481,11 @@ __device__ __forceinline__ void bins_run_plain(const BinView &B, const int64_t u
             }
         }
 #if PR_DYNAMIC_UNITS
-        if (tid == 0) next_unit = u_lo + (int64_t)gridDim.x + (int64_t)claim;
+        // two-slot ring: one barrier per unit
+        if (tid == 0) next_unit[ring] = u_lo + (int64_t)gridDim.x + (int64_t)claim;
         __syncthreads();
-        u = next_unit;
-        __syncthreads();
+        u = next_unit[ring];
+        ring ^= 1;
 #else
         u += gridDim.x;
 #endif

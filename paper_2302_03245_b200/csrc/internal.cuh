@@ -277,7 +277,7 @@ constexpr int CSC_PAD = 1024;  // int32 padding past the compacted CSC for vecto
 #endif
 constexpr int64_t THREAD_DEG = PR_THREAD_DEG;   // rows up to this in-degree: one thread each
 #ifndef PR_HUB_CHUNK
-#define PR_HUB_CHUNK 4096
+#define PR_HUB_CHUNK 16384
 #endif
 // thread-row bin stored SELL-32 (sched.cu sell_layout); 0 = row-major CSR (A/B builds)
 #ifndef PR_SELL
@@ -289,8 +289,13 @@ constexpr int64_t THREAD_DEG = PR_THREAD_DEG;   // rows up to this in-degree: on
 #ifndef PR_UNITS_PB
 #define PR_UNITS_PB 8
 #endif
-constexpr int64_t HUB_DEG = PR_HUB_CHUNK;      // rows above: cut into HUB_CHUNK-edge block units
-constexpr int64_t HUB_CHUNK = PR_HUB_CHUNK;    // edges per hub unit (256 threads x HUB_CHUNK/256)
+#ifndef PR_HUB_DEG
+#define PR_HUB_DEG 4096
+#endif
+constexpr int64_t HUB_DEG = PR_HUB_DEG;        // rows above: cut into HUB_CHUNK-edge block units
+constexpr int64_t HUB_CHUNK = PR_HUB_CHUNK;    // edges per hub unit, summed HUB_STEP at a time
+constexpr int64_t HUB_STEP = 4096;             // 256 threads x 16 gathers in flight
+static_assert(PR_HUB_CHUNK % 4096 == 0, "hub chunks are whole steps");
 constexpr int64_t ROW_COST = 8;                // per-row drain cost in edge units (unit sizing)
 constexpr int64_t UNITS_PER_BLOCK = PR_UNITS_PB;  // target work units per block of the persistent grid
 constexpr int64_t LONG_UNIT = 100000;           // edge-units: past this, UNITS_PER_BLOCK per section

@@ -924,6 +924,10 @@ struct Plan {
     bool exact;
     unsigned g_all, g_red, g_total, g_pull, g_push, g_scan;
     const void *k_pull_fn;   // k_pull<STREAM, PREFETCH> chosen by the round's working set
+    // per section: the launch's kernel and grid (sections of thread rows can
+    // take the form that loads a row's drain inputs before its gathers)
+    const void *k_pull_sec[PR_MAX_SECTIONS];
+    unsigned g_pull_sec[PR_MAX_SECTIONS];
 };
 
 void release_execs(Ctx &ctx) {
@@ -1014,8 +1018,8 @@ static int build_graph(Plan &P, cudaGraph_t *out_g, cudaGraphExec_t *out_exec) {
         for (int k = 0; k < sweeps; ++k)
             for (int sec = 0; sec < A.nsec; ++sec) {
                 A.sec = sec;  // the node copies its arguments here
-                PR_TRY(add_kernel(b_pull, &n_a, prev ? &prev : nullptr, prev ? 1 : 0, (void *)P.k_pull_fn, P.g_pull,
-                                  256, args));
+                PR_TRY(add_kernel(b_pull, &n_a, prev ? &prev : nullptr, prev ? 1 : 0, (void *)P.k_pull_sec[sec],
+                                  P.g_pull_sec[sec], 256, args));
                 prev = n_a;
             }
         A.sec = 0;
@@ -1313,6 +1317,36 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
     P.g_all = grid_for(n, 256);
     P.g_pull = (unsigned)pull_blocks;
     P.k_pull_fn = k_pull_fn;
+    for (int k = 0; k < PR_MAX_SECTIONS; ++k) {
+        P.k_pull_sec[k] = k_pull_fn;
+        P.g_pull_sec[k] = (unsigned)pull_blocks;
+    }
+    // A section made of thread rows (C5's last: 21 M rows of ~7 in-edges, all
+    // of the sweep's per-vertex drain traffic) is bound by each thread's chain
+    // of dependent loads -- bounds, indices, shares, drain inputs -- not by
+    // the gathers' request rate (ncu: long scoreboard 77%, L1->L2 requests 66%
+    // against 80-83% in the warp-row sections).  Its launch uses the form that
+    // issues a row's drain loads before its gathers, at 3 blocks/SM, while the
+    // other sections keep the plain form at 4.  PUSHRANK_PREFETCH_THREADS=0/1.
+    {
+        bool pf_threads = S.nsec > 1 && !prefetch;
+        if (const char *e = getenv("PUSHRANK_PREFETCH_THREADS")) pf_threads = S.nsec > 1 && !prefetch && atoi(e) != 0;
+        if (pf_threads) {
+            const void *k_pf = stream ? (const void *)k_pull<true, true, true> : (const void *)k_pull<false, true, true>;
+            int b = 0;
+            PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_pf, 256, 0));
+            if (b < 1) b = 1;
+            const int64_t t0 = S.n_hub + S.n_warp;
+            for (int k = 0; k < S.nsec; ++k) {
+                const int64_t lo = S.sec_row[k], hi = S.sec_row[k + 1];
+                const int64_t thr = hi - (lo > t0 ? lo : t0);
+                if (hi > lo && (double)thr > 0.9 * (double)(hi - lo)) {
+                    P.k_pull_sec[k] = k_pf;
+                    P.g_pull_sec[k] = (unsigned)((int64_t)ctx.sm_count * b);
+                }
+            }
+        }
+    }
     // L1 / shared-memory split of the dense round: PUSHRANK_CARVEOUT=percent
     // of the unified array given to shared memory (A/B; default: driver's)
     if (const char *e = getenv("PUSHRANK_CARVEOUT"))
@@ -1443,7 +1477,7 @@ int run_rounds(Graph &g_in, const pr_run_params &p, double *d_values, double *d_
                 void *kargs[] = {&A};
                 for (int sec = 0; sec < A.nsec; ++sec) {
                     A.sec = sec;
-                    PR_CUDA(cudaLaunchKernel(P.k_pull_fn, dim3(P.g_pull), dim3(256), kargs, 0, st));
+                    PR_CUDA(cudaLaunchKernel(P.k_pull_sec[sec], dim3(P.g_pull_sec[sec]), dim3(256), kargs, 0, st));
                 }
                 A.sec = 0;
             } else {
