@@ -175,7 +175,9 @@ __device__ __forceinline__ int drain_loaded(const RunArgs &A, const VtxIn &q, do
         // (c*h)/deg with two roundings, never c*h*inv_deg (engines.py:444, _kernels.pyx:97)
         s_out[v] = dv > 0 ? __ddiv_rn(__dmul_rn(A.c, hv), (double)dv) : 0.0;
         A.reserved[v] = __dadd_rn(rv, __dmul_rn(A.frac, hv));
-        A.h[v] = 0.0;
+        // a vertex active in consecutive rounds already holds 0 (the dense
+        // phase: nearly every row, every round): no store
+        if (q.h != 0.0) A.h[v] = 0.0;
         p.nact += 1;
         p.work += (int64_t)dv + 1;
         p.push_ops += len;
