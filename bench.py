@@ -289,7 +289,7 @@ def run_reference(args):
               f"{args.steps} full {args.algo} solves of {args.config} (xi={XI}), mean")
     line = {"impl": "reference", "metric": "GTEPS", "value": value, "unit": "GTEPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(walls),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": config_desc(args, g.n, g.m),
             "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": threads, "kind": kind,
                              "sample": sample, "model": cpu_model()},
@@ -397,7 +397,7 @@ def run_ours(args):
     launches = sum(r.launches for r in results)
     line = {"metric": "GTEPS", "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_desc(args, g.n, g.m),
             "time_to_l1_ms": statistics.median(dev_ms), "round_loop_ms": statistics.median(loop_ms),
             "rounds": int(r0.rounds), "pull_rounds": int(r0.pull_rounds), "push_rounds": int(r0.push_rounds),
