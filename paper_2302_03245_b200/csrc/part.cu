@@ -41,6 +41,8 @@
 
 namespace pr {
 
+constexpr int64_t PART_ROW_COST = 8;   // default per-row weight of the partition bounds
+
 #define PR_MAX_PEERS 8   // fused exchange: ranks whose replicas a round stores into
 
 // an owned vertex that is not a row of the pull schedule
@@ -637,9 +639,27 @@ int part_create(Ctx &ctx, int64_t owned, int64_t slot, const int64_t *in_off, co
 // set in the run layout's row order (the fast local step's schedule does not
 // depend on it).
 
-// w[v] = in_degree(v) + ROW_COST; w[n] = 0 (exclusive scan -> cum[0..n])
-__global__ void k_part_weights(const int64_t *__restrict__ in_off, int64_t n, int64_t *__restrict__ w) {
-    GRID_STRIDE(v, n + 1) w[v] = v < n ? in_off[v + 1] - in_off[v] + ROW_COST : 0;
+// per-row weight of a receiving vertex, in edge units (distributed.ROW_COST reads the same variable)
+static int64_t part_row_cost() {
+    const char *e = getenv("PUSHRANK_PART_ROW_COST");
+    const int64_t v = e && *e ? atoll(e) : PART_ROW_COST;
+    return v > 0 ? v : PART_ROW_COST;
+}
+
+// w[v] = in_degree(v) + ROW_COST for the vertices a round gathers into
+// (in-degree > 0; IFP2: and out-degree > 0), 0 for the others, which are
+// drained in rounds 0-1 only (distributed.receiving_rows); w[n] = 0
+// (exclusive scan -> cum[0..n])
+__global__ void k_part_weights(const int64_t *__restrict__ in_off, const int32_t *__restrict__ out_deg, int ifp2,
+                               int64_t row_cost, int64_t n, int64_t *__restrict__ w) {
+    GRID_STRIDE(v, n + 1) {
+        int64_t x = 0;
+        if (v < n) {
+            const int64_t d = in_off[v + 1] - in_off[v];
+            if (d > 0 && (!ifp2 || out_deg[v] > 0)) x = d + row_cost;
+        }
+        w[v] = x;
+    }
 }
 
 // b[k] = first v with cum[v] >= floor(cum[n] * k / parts) (np.searchsorted
@@ -750,7 +770,8 @@ int part_from_graph(Graph &g_in, int parts, int rank, int algorithm, double c, d
         PR_TRY(ensure(cum, 8 * (n + 1)));
         PR_TRY(ensure(db, 8 * (PR_MAX_PEERS + 1)));
         k_part_weights<<<grid_for(n + 1, 256) > 4096 ? 4096 : grid_for(n + 1, 256), 256, 0, st>>>(
-            r.in_off.as<int64_t>(), n, w.as<int64_t>());
+            r.in_off.as<int64_t>(), r.out_deg.as<int32_t>(), algorithm == PR_ALGO_IFP2 ? 1 : 0, part_row_cost(), n,
+            w.as<int64_t>());
         PR_TRY(cub_run(ctx, [&](void *t, size_t &bytes) {
             return cub::DeviceScan::ExclusiveSum(t, bytes, w.as<int64_t>(), cum.as<int64_t>(), (int)(n + 1), st);
         }));

@@ -74,6 +74,17 @@ def test_edge_balanced_ranges():
     assert max(loads) - min(loads) <= w.max()
     with pytest.raises(ValueError):
         D.edge_balanced_ranges(deg, 0)
+    # only receiving rows weigh: the in-degree-0 tail and (IFP2) the dangling
+    # receivers cost a rank nothing after rounds 0-1
+    outd = np.array([3, 2, 0, 1, 0, 4, 1, 0, 2, 2], np.int64)
+    for algo in ("ifp1", "ifp2"):
+        rec = D.receiving_rows(deg, outd, algo)
+        assert rec.tolist() == [bool(d > 0 and (algo == "ifp1" or o > 0)) for d, o in zip(deg, outd)]
+        b = D.edge_balanced_ranges(deg, 3, rec)
+        assert b[0] == 0 and b[-1] == deg.size and np.all(np.diff(b) >= 0)
+        w = np.where(rec, deg + D.ROW_COST, 0)
+        loads = [w[b[i]:b[i + 1]].sum() for i in range(3)]
+        assert sum(loads) == w.sum() and max(loads) - min(loads) <= 2 * w.max()
 
 
 def test_partition_covers_graph():

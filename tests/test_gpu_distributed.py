@@ -211,7 +211,8 @@ def test_two_process_ipc_fused_exchange(algorithm):
     n, src, dst = synthetic.make("c2", seed=0)
     g = oracle.from_edges(n, src, dst)
     order = D.run_order(np.diff(g.out_offsets), np.diff(g.in_offsets))
-    host_bounds = D.edge_balanced_ranges(np.diff(g.in_offsets)[order], 2)
+    ind, outd = np.diff(g.in_offsets)[order], np.diff(g.out_offsets)[order]
+    host_bounds = D.edge_balanced_ranges(ind, 2, D.receiving_rows(ind, outd, algorithm))
     assert fused[0][2] == host_bounds.tolist()
     vals = {}
     for name, res in (("fused", fused), ("gathered", gathered)):
