@@ -41,6 +41,10 @@
 
 namespace pr {
 
+// resident blocks per SM of the plain k_part_pull form (registers: 64 at 4, 85 at 3)
+#ifndef PR_PART_BLOCKS
+#define PR_PART_BLOCKS 4
+#endif
 constexpr int64_t PART_ROW_COST = 8;   // default per-row weight of the partition bounds
 
 #define PR_MAX_PEERS 8   // fused exchange: ranks whose replicas a round stores into
@@ -311,7 +315,7 @@ __device__ __forceinline__ void part_bins(const PartArgs &A, const BinView &T, c
 }
 
 template <bool STREAM, bool PREFETCH>
-__global__ void __launch_bounds__(256, PREFETCH ? 3 : 4) k_part_pull(PartArgs A, BinView T, const int32_t *outside,
+__global__ void __launch_bounds__(256, PREFETCH ? 3 : PR_PART_BLOCKS) k_part_pull(PartArgs A, BinView T, const int32_t *outside,
                                                                     int64_t n_outside, const PullSec S,
                                                                     const ShareOut s_mine) {
     if (S.prev9 && S.prev9[3] == 0.0) {
@@ -1007,7 +1011,7 @@ static int ensure_part_sched(Part &P) {
         const double l2 = (double)(ctx.l2_bytes ? ctx.l2_bytes : (size_t)126 << 20);
         P.stream_csc = ws > 0.6 * l2;
         P.prefetch = ws < 4.0 * l2;
-        P.blocks = (int64_t)ctx.sm_count * (P.prefetch ? 3 : 4);
+        P.blocks = (int64_t)ctx.sm_count * (P.prefetch ? 3 : PR_PART_BLOCKS);
         // rank-local Gauss-Seidel sections, as the engine chooses them
         // (rounds.cu): IFP2 on rows that are the local ids in order (a
         // run-layout partition), 2 past 1.5x L2 of round working set, 4 past 16x
