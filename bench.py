@@ -516,12 +516,18 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
     # e2e: partition upload + solve + owned values back, every step
     dist.barrier()
     t0 = time.perf_counter()
+    e2e_fused = False
     for _ in range(2):
-        # (the all-gather form: a fresh partition per step would otherwise pay
-        # the replicas' cudaMalloc/IPC mapping every step, which a resident
-        # partition does once)
+        # a fresh partition per step, replicas and peer mappings included
+        # (cudaMalloc + IPC open, tens of ms): still far cheaper than the
+        # all-gather form, whose every round moves P x slot shares per rank
+        # (the slot is the largest rank's vertex count, 59 M at P = 8 since the
+        # bounds stopped weighing vertices no round gathers into)
         s2 = D.CudaLocalStep(host_part, DAMPING, XI, args.algo, device=local, fast=True)
-        solve(s2, host_values=True, fused=False)
+        e2e_fused = bool(want_fused and s2.setup_fused(comm))
+        solve(s2, host_values=True, fused=e2e_fused)
+        if e2e_fused:
+            s2.close_fused(comm)
         del s2
     torch.cuda.synchronize()
     te = torch.tensor([(time.perf_counter() - t0) / 2], dtype=torch.float64, device=red_dev)
@@ -548,7 +554,8 @@ def run_partitioned_bench(args, g, rank, world, local, preprocess_s):
                         "h2d_bytes_per_step": int(8 * (host_part.owned + 1) + 4 * host_part.in_sources.size
                                                   + 12 * host_part.owned + 2 * host_part.owned),
                         "d2h_bytes_per_step": int(8 * part.owned), "ms_per_step": 1e3 * e2e_s,
-                        "path": "per step: partition upload (pr_part_create) + rounds (all-gather exchange) + owned values D2H"},
+                        "path": "per step: partition upload (pr_part_create) + replicas and peer mappings + rounds ("
+                                + ("fused" if e2e_fused else "all-gather") + " exchange) + owned values D2H"},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": None,
                              "kernel": "partitioned round loop per GPU (k_part_pull + exchange + statistics), "
