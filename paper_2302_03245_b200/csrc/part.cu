@@ -1007,7 +1007,9 @@ static int ensure_part_sched(Part &P) {
         P.which = P.algorithm == PR_ALGO_IFP2 ? 1 : 0;
         if ((rc = ensure_sched(*g, P.which))) break;
         // the same working-set rules as the engine's k_pull (rounds.cu)
-        const double ws = 4.0 * (double)g->sched[P.which].edges + 8.0 * (double)P.slot + 44.0 * (double)P.owned;
+        // (44 B per scheduled row, as there: the owned vertices outside the schedule are not swept)
+        const double ws = 4.0 * (double)g->sched[P.which].edges + 8.0 * (double)P.slot +
+                          44.0 * (double)g->sched[P.which].count;
         const double l2 = (double)(ctx.l2_bytes ? ctx.l2_bytes : (size_t)126 << 20);
         P.stream_csc = ws > 0.6 * l2;
         P.prefetch = ws < 4.0 * l2;
