@@ -950,7 +950,13 @@ void release_execs(Ctx &ctx) {
 // handles.  Unrolling the bodies into plain kernel nodes matters: measured
 // per round, WHILE{SWITCH{kernel}} costs 11.7 us, WHILE{kernel} 7.6 us and
 // WHILE{kernel x8} 3.7 us (tools_graph_overhead.py).
-constexpr int PULL_UNROLL = 8, PUSH_UNROLL = 4;
+#ifndef PR_PULL_UNROLL
+#define PR_PULL_UNROLL 8
+#endif
+#ifndef PR_PUSH_UNROLL
+#define PR_PUSH_UNROLL 4
+#endif
+constexpr int PULL_UNROLL = PR_PULL_UNROLL, PUSH_UNROLL = PR_PUSH_UNROLL;
 
 static int add_while(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t *dep, cudaGraphConditionalHandle h,
                      cudaGraph_t *body) {
