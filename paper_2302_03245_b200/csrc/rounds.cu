@@ -458,6 +458,10 @@ __device__ __forceinline__ void clear_seeds(const RunArgs &A, int64_t t) {
 #ifndef PULL_MIN_BLOCKS
 #define PULL_MIN_BLOCKS 4
 #endif
+// resident blocks per SM of the prefetching form (80 registers at 3)
+#ifndef PR_PF_BLOCKS
+#define PR_PF_BLOCKS 3
+#endif
 __device__ __forceinline__ void stamp_round_start(RunCtl *ctl) {
     if (threadIdx.x == 0 && atomicExch(&ctl->k_started, 1u) == 0u) ctl->t_k0 = globaltimer();
 }
@@ -502,7 +506,7 @@ __device__ __forceinline__ bool round_is(const RunArgs &A, int mode) {
 
 // GS: the launch is one Gauss-Seidel section of a sweep
 template <bool STREAM, bool PREFETCH, bool GS>
-__global__ void __launch_bounds__(256, PREFETCH ? PULL_MIN_BLOCKS - 1 : PULL_MIN_BLOCKS) k_pull(RunArgs A) {
+__global__ void __launch_bounds__(256, PREFETCH ? PR_PF_BLOCKS : PULL_MIN_BLOCKS) k_pull(RunArgs A) {
     count_launch(A);
     if (A.use_graph && !round_is(A, 0)) return;
     stamp_round_start(A.ctl);
